@@ -1,0 +1,307 @@
+"""bench.py — throughput of the B200 state-vector hot path (driver contract).
+
+Default (N=1): BASELINE.json configs[3] "C4", the config the metric is quoted on: a 30-qubit
+random circuit (depth 40: Haar 1q matrix on every qubit + CZ bricks, 1780 gates, seed 3040) on a
+complex128 state (16 GiB), plus the 50-term JW-shaped Hamiltonian (seed 3030).
+  step  = sv_reset + sv_apply_circuit(C4) + sv_expectation(H)   (all inputs resident; 16 GiB > L2,
+          so no L2 flush is needed between steps)
+  value = C4 gates / step time  (gates/s, higher is better)
+Extra keys: effective state-vector GB/s, achieved HBM GB/s of the plan and its fraction of the
+measured peak, the adjoint-gradient throughput at 30q (C4g: 30q HEA, 2 layers, 120 params),
+roofline of the dominant kernel (the fused forward pass), the CPU oracle baseline, e2e through the
+C-ABI with host buffers, clocks during the timed region.
+
+--impl reference: the CPU oracle (oracle/, test infrastructure) timed on the host cores on a
+bounded sample of the same workload (the tier's reference arm).
+
+Multi-GPU (torchrun, N>1): replicas only for now — every rank runs the same 1-GPU step on its own
+GPU (no collective); scaling "weak". See DESIGN.md §Multi-GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+
+
+def _peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (getattr(self, "out", "") or "").splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[4], parts[5], parts[6], parts[7]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[2 + j].lower().startswith("active")})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def _ham_terms(ham):
+    return len(ham)
+
+
+def cpu_oracle_sample(config: str, seconds_target: float = 15.0):
+    """The oracle as it stands, timed on the host cores on a bounded sample of the workload:
+    the first G gates of the config's circuit at full width (n=30 for C4), G chosen to take about
+    `seconds_target` seconds. Returns (gates/s, cores, sample description)."""
+    import oracle
+    w = W.config(config)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    psi = oracle.zero_state(w.n)
+    # calibrate on 1 gate, then run the sample
+    t0 = time.perf_counter()
+    psi = oracle.apply_circuit(w.n, w.gates[:1], w.params, psi)
+    t1 = time.perf_counter() - t0
+    G = int(max(1, min(len(w.gates) - 1, seconds_target / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.apply_circuit(w.n, w.gates[1:1 + G], w.params, psi)
+    dt = time.perf_counter() - t0
+    return G / dt, cores, f"oracle.apply_circuit on gates 1..{G} of {config} at n={w.n} ({dt:.1f} s)"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    w = W.config(args.config)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    # each step: a bounded sample (the first G gates of the circuit at full width)
+    psi = oracle.zero_state(w.n)
+    t0 = time.perf_counter()
+    psi = oracle.apply_circuit(w.n, w.gates[:1], w.params, psi)
+    t1 = time.perf_counter() - t0
+    G = int(max(1, min(len(w.gates), 20.0 / max(1, args.steps + args.warmup) / max(t1, 1e-3))))
+    for _ in range(args.warmup):
+        oracle.apply_circuit(w.n, w.gates[:G], w.params, psi)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.apply_circuit(w.n, w.gates[:G], w.params, psi)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = G / (ms / 1e3)
+    sample = f"first {G} gates of {args.config} at n={w.n} per step"
+    line = {"metric": "gates/sec (30q random circuit, C4)", "value": value, "unit": "gates/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic", "config": {"workload": args.config, "n_qubits": w.n, "gates": len(w.gates),
+                                            "sample_gates": G},
+            "cpu_baseline": {"value": value, "unit": "gates/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-grad", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2406_17248_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = W.config(args.config)
+    n = w.n
+    ga = P.GateArray(w.gates)
+    pa = P.PauliArray(w.ham)
+    sv = P.StateVector(n)
+    stream = torch.cuda.Stream()  # a real stream object: its handle is passed to the library
+    torch.cuda.set_stream(stream)
+    P.sv_set_stream(sv.h, stream.cuda_stream)
+
+    def step():
+        sv.reset()
+        P.sv_apply_circuit(sv.h, ga, w.params)
+        return P.sv_expectation(sv.h, pa)
+
+    # warm-up (also builds the plan caches inside the library's allocator)
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    P.sv_reset_stats(sv.h)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evc0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    evc1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        E = None
+        for i in range(args.steps):
+            sv.reset()
+            evc0[i].record(stream)
+            P.sv_apply_circuit(sv.h, ga, w.params)
+            evc1[i].record(stream)
+            E = P.sv_expectation(sv.h, pa)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    circ_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(evc0, evc1)]))
+    st = P.sv_get_stats(sv.h)
+    if dist:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    n_gates = len(w.gates)
+    value = world * n_gates / (ms_step / 1e3)
+    passes = st["gate_passes"] // args.steps
+    hbm_peak, peak_src = _peaks()
+    amps = float(1 << n)
+    # effective SV bytes: what unfused single-gate sweeps would move: 32 B x 2^(n-c) per gate
+    eff_bytes = sum(32.0 * amps / (1 << len(g.controls)) for g in w.gates)
+    plan_bytes = st["algorithmic_bytes"] / args.steps
+    pass_ms = circ_ms / max(passes, 1)
+    pass_bytes = 32.0 * amps
+    achieved = pass_bytes / (pass_ms / 1e3) / 1e9
+    clocks = clk.summary()
+
+    # e2e: same step through the public C-ABI with host inputs (gate / term arrays marshalled from
+    # host memory every step; plan upload H2D and the expectation D2H inside the timed region)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ga_h = P.GateArray(w.gates)
+        pa_h = P.PauliArray(w.ham)
+        sv.reset()
+        P.sv_apply_circuit(sv.h, ga_h, w.params)
+        P.sv_expectation(sv.h, pa_h)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    h2d = ga.nbytes + pa.nbytes + w.params.nbytes
+    e2e = {"value": world * n_gates / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": 8}
+
+    grad = None
+    if not args.no_grad and args.config == "C4" and rank == 0:
+        wg = W.config("C4g")
+        gag, pag = P.GateArray(wg.gates), P.PauliArray(wg.ham)
+        svg = sv  # same handle: psi0 = |0>
+        sv.reset()
+        P.sv_expectation_with_grad(svg.h, gag, wg.params, pag)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = 2
+        for _ in range(reps):
+            Eg, gg = P.sv_expectation_with_grad(svg.h, gag, wg.params, pag)
+        dtg = (time.perf_counter() - t0) / reps
+        grad = {"workload": "C4g: 30q HEA 2 layers RY/RZ + CNOT ladder, 120 params, 50-term JW H",
+                "grad_evals_per_s": 1.0 / dtg, "ms_per_eval": 1e3 * dtg, "E": Eg}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        try:
+            v, cores, sample = cpu_oracle_sample(args.config)
+            cpu = {"value": v, "unit": "gates/s", "cores": cores, "kind": "oracle", "sample": sample}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "gates/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "gates/sec (30q random circuit C4 evolution + 50-term <H>), SV GB/s, grad evals/sec",
+            "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128 (f64)", "data": "synthetic",
+            "config": {"workload": args.config, "n_qubits": n, "gates": n_gates, "ham_terms": len(w.ham),
+                       "state_bytes": int(16 * amps), "l2": "inputs (16 GiB state) larger than L2; no flush",
+                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+            "circuit_ms": circ_ms, "passes_per_circuit": passes, "E": E,
+            "sv_effective_gbs": eff_bytes / (circ_ms / 1e3) / 1e9,
+            "plan_hbm_gbs": plan_bytes / (ms_step / 1e3) / 1e9,
+            "plan_hbm_frac": plan_bytes / (ms_step / 1e3) / 1e9 / hbm_peak,
+            "roofline": {"bound": "hbm", "kernel": "k_pass<false> (fused forward tile pass)",
+                         "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": pass_bytes, "avg_launch_ms": pass_ms},
+            "grad": grad,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(st["kernel_launches"]),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    sv.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

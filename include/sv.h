@@ -1,0 +1,191 @@
+/*
+ * sv.h — C ABI of the B200-native state-vector hot path (after MindSpore Quantum's "mqvector",
+ * arXiv:2406.17248). Plain C types only: no torch, no CUDA types in any signature.
+ *
+ * Citations: P:n = PAPER.md line n (the paper text), S:n = SPEC.md line n, "reading cN" = the
+ * DESIGN.md "Readings of the paper" entry N.
+ *
+ * What the library computes:
+ *   a1  sv_create / sv_reset: the state psi = |0...0> of n qubits, 2^n complex128 amplitudes,
+ *       interleaved (re, im), qubit 0 = least-significant index bit (Fig. 3, P:38-78, P:70-74;
+ *       reading c2).
+ *   a2  host side of every apply call: validate, bind angles (angle = coeff * params[param] +
+ *       offset), classify by the paper's gate taxonomy — X-like anti-diagonal [[0,a],[b,0]]
+ *       (§3.1 eq. P:80-87), Z-like diagonal [[a,0],[0,b]] (§3.1 eq. P:88-94), general 1-/2-qubit
+ *       matrix gates (§7.1 gate list P:579) — with an arbitrary control set on any gate
+ *       (Fig. 1 "Any control on any gate") — and plan fused passes.
+ *   a3  sv_apply_gate / sv_apply_circuit: "Evolution of Circuit" (Fig. 1): psi <- U_N..U_1 psi.
+ *   a4  sv_expectation: "Expectation of Observable" (Fig. 1): <psi|H|psi> for a real Pauli
+ *       sum H (pure-state form of <H> = tr(rho H), §3.2).
+ *   a5-a7 sv_expectation_with_grad: "Gradient calculation" (Fig. 1) by the adjoint method
+ *       ("optimized adjoint method", §7.2; §4.1 body absent -> reading c8): E and dE/dtheta.
+ *
+ * Conventions: rotations R_P(t) = exp(-i t P / 2) for P in {X, Y, Z, XX, YY, ZZ} (reading
+ * c1); PS(t) = diag(1, e^{i t}); H uses the correctly-rounded 1/sqrt(2) = 0.7071067811865476; a
+ * two-qubit matrix's index bit j <-> targets[j] (reading c5).
+ *
+ * Errors: every entry point returns sv_status (0 = SV_OK). No exceptions cross the ABI. On error
+ * nothing is applied (a circuit is validated as a whole before any device work) and
+ * sv_last_error() returns a thread-local description. Asynchronous CUDA/NCCL failures surface at
+ * the next synchronous call as SV_E_CUDA / SV_E_NCCL and poison the handle (SV_E_POISONED after).
+ *
+ * Ownership: the caller owns every array it passes; nothing is retained after a call returns.
+ * A handle owns its device memory (cudaMalloc on the device current at creation). Handles are
+ * single-owner (not thread-safe); distinct handles may be used concurrently.
+ *
+ * Synchrony: sv_apply_* enqueue work on the handle's stream and return (asynchronous to the host,
+ * stream-ordered). sv_expectation*, sv_get_state* synchronize the stream before returning.
+ */
+#ifndef SV_H_
+#define SV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sv_state_s* sv_handle;
+typedef int32_t sv_status;
+
+enum {
+  SV_OK = 0,
+  SV_E_ARG = 1,                    /* null pointer, bad size, unknown kind, bad world size ...      */
+  SV_E_QUBIT_RANGE = 2,            /* a target / control / Pauli index >= n                  */
+  SV_E_TARGET_CONTROL_OVERLAP = 3, /* controls intersect targets                      */
+  SV_E_DUPLICATE_TARGET = 4,       /* two-qubit gate with targets[0] == targets[1]           */
+  SV_E_PARAM_RANGE = 5,            /* param index outside [0, n_params) (S:66 MissingParameter)      */
+  SV_E_NOT_DIFFERENTIABLE = 6,     /* a param on a kind without a generator                  */
+  SV_E_NOT_UNITARY = 7,            /* user matrix not unitary within 1e-10 in _with_grad     */
+  SV_E_OOM = 8,                    /* device allocation failed (construction-time error)      */
+  SV_E_CUDA = 9,
+  SV_E_NCCL = 10,
+  SV_E_POISONED = 11               /* a previous asynchronous failure poisoned this handle           */
+};
+
+/* Gate kinds, grouped by the paper's taxonomy (§3.1; reading c6). CNOT = SV_X with one
+ * control, CZ = SV_Z with one control. */
+enum sv_kind {
+  /* X-like: anti-diagonal [[0,a],[b,0]] */
+  SV_X = 0, SV_Y = 1, SV_XLIKE = 2,
+  /* Z-like: diagonal [[a,0],[0,b]] */
+  SV_Z = 3, SV_S = 4, SV_SDG = 5, SV_T = 6, SV_TDG = 7, SV_ZLIKE = 8, SV_RZ = 9, SV_PS = 10,
+  /* general 2x2 */
+  SV_H = 11, SV_RX = 12, SV_RY = 13, SV_MAT1 = 14,
+  /* two-qubit (RZZ is diagonal) */
+  SV_SWAP = 15, SV_RXX = 16, SV_RYY = 17, SV_RZZ = 18, SV_MAT2 = 19,
+  SV_NUM_KINDS = 20
+};
+
+/* One gate. targets[1] is ignored for one-qubit kinds. controls: bit q set <=> qubit q is a
+ * control (arbitrary set, disjoint from targets). param: index into params, or -1 for a
+ * fixed gate; angle = coeff * params[param] + offset when param >= 0, else offset (rotation kinds
+ * only; SV_E_ARG if a non-rotation kind carries param >= 0 outside _with_grad, where it is
+ * SV_E_NOT_DIFFERENTIABLE). mat: XLIKE/ZLIKE -> (a_re, a_im, b_re, b_im); MAT1 -> 8 doubles
+ * (2x2 row-major interleaved); MAT2 -> 32 doubles (4x4, index bit j <-> targets[j]); NULL for
+ * other kinds. */
+typedef struct {
+  int32_t kind;
+  int32_t targets[2];
+  uint64_t controls;
+  int32_t param;
+  double coeff;
+  double offset;
+  const double* mat;
+} sv_gate;
+
+/* One Pauli term coeff * i^{popc(x&z)} X^x Z^z: qubit q carries X if x_q=1,z_q=0; Y if both;
+ * Z if x_q=0,z_q=1. Real coeff => H Hermitian by construction; identity term allowed. */
+typedef struct {
+  uint64_t x_mask;
+  uint64_t z_mask;
+  double coeff;
+} sv_pauli;
+
+/* Counters since creation (or the last sv_reset_stats), for bench / roofline reporting. */
+typedef struct {
+  int64_t kernel_launches;       /* every kernel this library launched                           */
+  int64_t gate_passes;           /* fused forward gate passes (one HBM read+write of the state)   */
+  int64_t adjoint_passes;        /* fused reverse passes over (psi, lambda)                       */
+  int64_t expectation_passes;    /* Pauli-group passes (expectation and lambda = H psi)           */
+  int64_t exchanges;             /* sharded: global<->local qubit swaps                           */
+  double algorithmic_bytes;      /* HBM bytes the executed plan must move   */
+  int64_t gates_applied;         /* gates of the user's circuits applied (forward only)           */
+} sv_stats;
+
+/* Option keys for sv_set_option (A/B evidence; defaults are the tuned values). */
+enum {
+  SV_OPT_TILE_QUBITS = 1,        /* k: qubits per fused tile (0 = auto)                           */
+  SV_OPT_FUSION = 2,             /* 1 (default) fuse gates into tile passes; 0 one pass per gate  */
+  SV_OPT_LOW_QUBITS = 3          /* qubits 0..L-1 always in a tile (coalescing granule), default 3 */
+};
+
+/* a1: |0...0> on n_qubits (1 <= n <= 40 subject to memory), current CUDA device, new stream. */
+sv_status sv_create(int32_t n_qubits, sv_handle* out);
+
+/* Sharded state (SPMD, one process per GPU): the top log2(world) qubits are global; rank r holds
+ * the 2^(n - log2 world) amplitudes whose global bits equal r. nccl_id points at the 128-byte
+ * ncclUniqueId rank 0 created with sv_nccl_unique_id and broadcast (e.g. via torch.distributed).
+ * world in {1, 2, 4, 8, ...} (power of two). Every rank must then make identical calls. */
+sv_status sv_create_sharded(int32_t n_qubits, int32_t rank, int32_t world, const void* nccl_id, sv_handle* out);
+
+/* Writes a fresh ncclUniqueId (128 bytes) into out (call on rank 0 only). */
+sv_status sv_nccl_unique_id(void* out, int32_t out_bytes);
+
+/* Loopback sharding on ONE GPU: `world` virtual shards, each its own device buffer, exchanges as
+ * device-to-device copies. Same planner and exchange schedule as sv_create_sharded; used to test
+ * the sharded path without several GPUs. */
+sv_status sv_create_virtual_shards(int32_t n_qubits, int32_t world, sv_handle* out);
+
+sv_status sv_destroy(sv_handle h);
+
+/* Use this CUDA stream (a cudaStream_t passed as void*) for all subsequent work; NULL = the
+ * handle's own stream. The caller keeps the stream alive while the handle uses it. */
+sv_status sv_set_stream(sv_handle h, void* cuda_stream);
+
+sv_status sv_set_option(sv_handle h, int32_t key, int64_t value);
+
+sv_status sv_get_num_qubits(sv_handle h, int32_t* out);
+
+/* psi <- |0...0>. Asynchronous. */
+sv_status sv_reset(sv_handle h);
+
+/* Full state in logical qubit order, 2*2^n doubles (re, im interleaved), from / to HOST memory.
+ * For sharded handles every rank passes the full array (set) / receives it (get, gathered). */
+sv_status sv_set_state(sv_handle h, const double* host_amps);
+sv_status sv_get_state(sv_handle h, double* host_amps);
+
+/* Same, from / to DEVICE memory (device pointer on the handle's device), single-GPU handles. */
+sv_status sv_set_state_device(sv_handle h, const void* dev_amps);
+sv_status sv_get_state_device(sv_handle h, void* dev_amps);
+
+/* a3: apply one gate / a circuit (array order = evolution order) in place. */
+sv_status sv_apply_gate(sv_handle h, const sv_gate* g, const double* params, int32_t n_params);
+sv_status sv_apply_circuit(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params,
+                           int32_t n_params);
+
+/* a4: *out_value = <psi|H|psi>, H = sum_t terms[t]. Synchronous. Empty H -> 0. */
+sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, double* out_value);
+
+/* a5-a7: evolves a COPY of the current state psi0 through the circuit, returns
+ * E = <psi|H|psi> and out_grad[p] = dE/dparams[p] for p < n_params (chain rule over every
+ * occurrence: sum_k coeff_k dE/dangle_k, reading c11). The handle's state is unchanged.
+ * Needs two workspace vectors of 2^n amplitudes (allocated on first use, kept). Synchronous. */
+sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params,
+                                   int32_t n_params, const sv_pauli* terms, int64_t n_terms,
+                                   double* out_value, double* out_grad);
+
+sv_status sv_get_stats(sv_handle h, sv_stats* out);
+sv_status sv_reset_stats(sv_handle h);
+
+/* Thread-local text of the last non-OK status on this thread ("" if none). */
+const char* sv_last_error(void);
+
+/* Library version string. */
+const char* sv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SV_H_ */

@@ -1,0 +1,40 @@
+/*
+ * sv_debug.h — host-only introspection of the fused-pass planner (no GPU needed). Used by the CPU
+ * test-suite to check planner invariants and by bench/profiling tools to report pass and stage
+ * counts. Same conventions as sv.h.
+ */
+#ifndef SV_DEBUG_H_
+#define SV_DEBUG_H_
+
+#include <stdint.h>
+
+#include "sv.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t k;            /* tile qubits of the pass                                             */
+  int32_t low;          /* qubits 0..low-1 are tile positions 0..low-1 (contiguous chunk)       */
+  int32_t R;            /* register qubits per thread (0 = shared-memory kernel)                 */
+  int32_t n_ops;        /* ops (gates) applied by the pass                                       */
+  int32_t n_stages;     /* register stages (R > 0)                                               */
+  int32_t n_grad;       /* adjoint overlap slots in the pass                                     */
+  uint64_t tile_mask;   /* physical qubits of the tile                                           */
+  uint64_t nondiag_mask;/* qubits on which the pass' ops act non-diagonally (subset of tile_mask) */
+} sv_pass_info;
+
+/* Plans `gates` for an n-qubit single-GPU state exactly as sv_apply_circuit (adjoint = 0) or the
+ * reverse sweep of sv_expectation_with_grad (adjoint = 1) would, with tile_qubits (0 = auto) and
+ * fusion (1 = on). Writes up to `cap` pass records to out and the pass count to *n_passes.
+ * Errors as sv_apply_circuit's validation. Host only; no CUDA call. */
+sv_status sv_plan_info(int32_t n_qubits, const sv_gate* gates, int64_t n_gates, const double* params,
+                       int32_t n_params, int32_t adjoint, int32_t tile_qubits, int32_t fusion, sv_pass_info* out,
+                       int64_t cap, int64_t* n_passes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SV_DEBUG_H_ */

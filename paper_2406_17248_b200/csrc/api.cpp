@@ -1,0 +1,488 @@
+// api.cpp — the C ABI (include/sv.h): handles, validation, orchestration of plans and kernels.
+//
+// Every numerical step runs in kernels.cu; this file only validates, binds (gates.cpp), plans
+// (plan.cpp), uploads plan data and launches. Sharding (sv_create_sharded / virtual shards) lives
+// in shard.cpp.
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "sv.h"
+#include "sv_internal.h"
+#include "sv_handle.h"
+
+namespace sv {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(sv_state_s* h, cudaError_t e, const char* where) {
+  if (h) h->poisoned = true;
+  return fail(SV_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool DevBuf::ensure(size_t bytes) {
+  if (bytes <= cap) return true;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  size_t want = bytes < 4096 ? 4096 : bytes;
+  if (cudaMalloc(&p, want) != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return false;
+  }
+  cap = want;
+  return true;
+}
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+
+int check_handle(sv_state_s* h) {
+  if (!h) return fail(SV_E_ARG, "null handle");
+  if (h->poisoned) return fail(SV_E_POISONED, "handle poisoned by an earlier CUDA/NCCL failure");
+  return SV_OK;
+}
+
+// Validates and binds a whole circuit (all-or-nothing).
+int bind_circuit(sv_state_s* h, const sv_gate* gates, int64_t n_gates, const double* params, int32_t n_params,
+                 bool for_grad, std::vector<BoundGate>* out) {
+  if (n_gates < 0 || (n_gates > 0 && !gates)) return fail(SV_E_ARG, "bad gate array");
+  if (n_params < 0) return fail(SV_E_ARG, "negative n_params");
+  out->resize((size_t)n_gates);
+  std::string err;
+  for (int64_t i = 0; i < n_gates; ++i) {
+    int rc = bind_gate(h->n, &gates[i], params, n_params, for_grad, &(*out)[(size_t)i], &err);
+    if (rc != SV_OK) return fail(rc, "gate " + std::to_string(i) + ": " + err);
+  }
+  return SV_OK;
+}
+
+// Uploads a plan's ops and matrices (stream-ordered: the copy runs after earlier kernels that read
+// the same buffers).
+int upload_plan(sv_state_s* h, const Plan& plan) {
+  // one buffer: [ops | stages | mats], each section 64-byte aligned; one H2D copy
+  auto al = [](size_t x) { return (x + 63) & ~size_t(63); };
+  const size_t ob = plan.ops.size() * sizeof(DevOp), sb = plan.stages.size() * sizeof(StageDesc),
+               mb = plan.mats.size() * sizeof(double);
+  const size_t so = al(ob), mo = so + al(sb), total = mo + al(mb);
+  if (!h->d_ops.ensure(total + 64)) return fail(SV_E_OOM, "plan buffers");
+  h->h_stage.assign(total, 0);
+  std::memcpy(h->h_stage.data(), plan.ops.data(), ob);
+  std::memcpy(h->h_stage.data() + so, plan.stages.data(), sb);
+  std::memcpy(h->h_stage.data() + mo, plan.mats.data(), mb);
+  h->plan_stages_off = so;
+  h->plan_mats_off = mo;
+  cudaError_t e = cudaSuccess;
+  if (total) e = cudaMemcpyAsync(h->d_ops.p, h->h_stage.data(), total, cudaMemcpyHostToDevice, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "plan upload");
+  return SV_OK;
+}
+
+// Runs all passes of a plan on psi (and lam for the adjoint plan).
+int run_plan(sv_state_s* h, const Plan& plan, double* psi, double* lam, double* d_partials, int grid) {
+  for (size_t i = 0; i < plan.passes.size(); ++i) {
+    const PassDesc& pd = plan.passes[i];
+    const int next_mat = (i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size();
+    PassLaunch L;
+    L.pd = &pd;
+    L.d_ops = static_cast<const DevOp*>(h->d_ops.p);
+    L.d_stages = reinterpret_cast<const StageDesc*>(static_cast<const char*>(h->d_ops.p) + h->plan_stages_off);
+    L.d_mats = reinterpret_cast<const double*>(static_cast<const char*>(h->d_ops.p) + h->plan_mats_off);
+    L.d_partials = d_partials;
+    L.nmats = next_mat - pd.mat_begin;
+    L.grid = grid > 0 ? grid : pass_grid(h->n_local, pd.k, lam != nullptr);
+    L.n_local = h->n_local;
+    L.rank_bits = 0;
+    cudaError_t e = launch_pass(psi, lam, L, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "pass launch");
+    h->stats.kernel_launches += 1;
+    const double amps = (double)(1ull << h->n_local);
+    if (lam) {
+      h->stats.adjoint_passes += 1;
+      h->stats.algorithmic_bytes += 64.0 * amps;
+    } else {
+      h->stats.gate_passes += 1;
+      h->stats.algorithmic_bytes += 32.0 * amps;
+    }
+  }
+  return SV_OK;
+}
+
+int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg) {
+  if (bg.empty()) return SV_OK;
+  Plan plan;
+  build_plan(bg, h->n_local, h->opts, false, &plan);
+  int rc = upload_plan(h, plan);
+  if (rc != SV_OK) return rc;
+  rc = run_plan(h, plan, h->psi, nullptr, nullptr, 0);
+  if (rc != SV_OK) return rc;
+  h->stats.gates_applied += (int64_t)bg.size();
+  return SV_OK;
+}
+
+// ---- Pauli sums ----
+
+
+
+int group_terms(sv_state_s* h, const sv_pauli* terms, int64_t n_terms, PauliGroups* g) {
+  if (n_terms < 0 || (n_terms > 0 && !terms)) return fail(SV_E_ARG, "bad term array");
+  const uint64_t lim = h->n >= 64 ? ~0ull : ((1ull << h->n) - 1);
+  std::map<uint64_t, std::vector<int64_t>> by_x;
+  for (int64_t t = 0; t < n_terms; ++t) {
+    if ((terms[t].x_mask & ~lim) || (terms[t].z_mask & ~lim)) return fail(SV_E_QUBIT_RANGE, "Pauli term on a qubit >= n");
+    by_x[terms[t].x_mask].push_back(t);
+  }
+  for (auto& kv : by_x) {
+    // chunks of <= 256 terms per launch
+    for (size_t off = 0; off < kv.second.size(); off += 256) {
+      g->xs.push_back(kv.first);
+      g->begin.push_back((int)g->z.size());
+      for (size_t j = off; j < kv.second.size() && j < off + 256; ++j) {
+        const sv_pauli& p = terms[kv.second[j]];
+        g->z.push_back(p.z_mask);
+        // i^{popc(x & z)}: Y = i X Z on each qubit with both bits set
+        const int ph = __builtin_popcountll(p.x_mask & p.z_mask) & 3;
+        const double re[4] = {1, 0, -1, 0}, im[4] = {0, 1, 0, -1};
+        g->c.push_back(p.coeff * re[ph]);
+        g->c.push_back(p.coeff * im[ph]);
+      }
+      g->end.push_back((int)g->z.size());
+    }
+  }
+  return SV_OK;
+}
+
+// Launches one Pauli-group pass per group over psi; lam (optional) receives H psi.
+// Writes per-CTA partials of group g to d_partials[g * grid ...].
+int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid) {
+  const size_t zb = (G.z.size() * 8 + 15) & ~size_t(15), cb = G.c.size() * 8;  // complex coeffs 16-B aligned
+  if (!h->d_terms.ensure(zb + cb + 16)) return fail(SV_E_OOM, "term buffers");
+  h->h_stage.resize(zb + cb + 16);
+  std::memcpy(h->h_stage.data(), G.z.data(), G.z.size() * 8);
+  std::memcpy(h->h_stage.data() + zb, G.c.data(), cb);
+  cudaError_t e = cudaMemcpyAsync(h->d_terms.p, h->h_stage.data(), zb + cb, cudaMemcpyHostToDevice, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "term upload");
+  const uint64_t* dz = static_cast<const uint64_t*>(h->d_terms.p);
+  const double* dc = reinterpret_cast<const double*>(static_cast<const char*>(h->d_terms.p) + zb);
+  const double amps = (double)(1ull << h->n_local);
+  for (size_t gi = 0; gi < G.xs.size(); ++gi) {
+    e = launch_pauli_group(psi, lam, gi > 0, h->n_local, G.xs[gi], dz + G.begin[gi], dc + 2 * G.begin[gi],
+                           G.end[gi] - G.begin[gi], d_partials + gi * (size_t)grid, grid, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "pauli group launch");
+    h->stats.kernel_launches += 1;
+    h->stats.expectation_passes += 1;
+    h->stats.algorithmic_bytes += (lam == nullptr ? 16.0 : (gi == 0 ? 32.0 : 48.0)) * amps;
+  }
+  return SV_OK;
+}
+
+}  // namespace sv
+
+using namespace sv;
+
+extern "C" {
+
+const char* sv_last_error(void) { return g_last_error.c_str(); }
+const char* sv_version(void) { return "paper_2406_17248_b200 sv 0.1 (sm_100a)"; }
+
+sv_status sv_create(int32_t n_qubits, sv_handle* out) {
+  if (!out) return fail(SV_E_ARG, "null out");
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > 40) return fail(SV_E_ARG, "n_qubits must be in [1, 40]");
+  sv_state_s* h = new sv_state_s();
+  h->n = n_qubits;
+  h->n_local = n_qubits;
+  cudaGetDevice(&h->device);
+  cudaError_t e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete h; return fail(SV_E_CUDA, std::string("stream: ") + cudaGetErrorString(e)); }
+  h->stream = h->own_stream;
+  const size_t bytes = (size_t(16) << n_qubits);
+  if (!h->state.ensure(bytes)) {
+    cudaStreamDestroy(h->own_stream);
+    delete h;
+    return fail(SV_E_OOM, "cannot allocate the state vector (" + std::to_string(bytes) + " bytes)");
+  }
+  h->psi = static_cast<double*>(h->state.p);
+  e = launch_init_zero(h->psi, int64_t(1) << n_qubits, true, h->stream);
+  if (e != cudaSuccess) { sv_destroy(h); return fail(SV_E_CUDA, cudaGetErrorString(e)); }
+  h->stats.kernel_launches += 1;
+  *out = h;
+  return SV_OK;
+}
+
+sv_status sv_destroy(sv_handle h) {
+  if (!h) return SV_OK;
+  cudaStreamSynchronize(h->stream);
+  h->state.release();
+  h->work_psi.release();
+  h->work_lam.release();
+  h->d_ops.release();
+  h->d_mats.release();
+  h->d_terms.release();
+  h->d_partials.release();
+  h->d_out.release();
+  destroy_sharding(h);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+  return SV_OK;
+}
+
+sv_status sv_set_stream(sv_handle h, void* stream) {
+  if (!h) return fail(SV_E_ARG, "null handle");
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
+  return SV_OK;
+}
+
+sv_status sv_set_option(sv_handle h, int32_t key, int64_t value) {
+  if (!h) return fail(SV_E_ARG, "null handle");
+  switch (key) {
+    case SV_OPT_TILE_QUBITS:
+      if (value < 0 || value > kMaxTileQubits) return fail(SV_E_ARG, "tile qubits out of range");
+      h->opts.tile_qubits = (int)value;
+      return SV_OK;
+    case SV_OPT_FUSION: h->opts.fusion = value != 0; return SV_OK;
+    case SV_OPT_LOW_QUBITS:
+      if (value < 0 || value > 8) return fail(SV_E_ARG, "low qubits out of range");
+      h->opts.low_qubits = (int)value;
+      return SV_OK;
+    default: return fail(SV_E_ARG, "unknown option");
+  }
+}
+
+sv_status sv_get_num_qubits(sv_handle h, int32_t* out) {
+  if (!h || !out) return fail(SV_E_ARG, "null argument");
+  *out = h->n;
+  return SV_OK;
+}
+
+sv_status sv_reset(sv_handle h) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (h->world > 1) return shard_reset(h);
+  cudaError_t e = launch_init_zero(h->psi, int64_t(1) << h->n_local, true, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "reset");
+  h->stats.kernel_launches += 1;
+  return SV_OK;
+}
+
+sv_status sv_set_state(sv_handle h, const double* host) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!host) return fail(SV_E_ARG, "null host buffer");
+  if (h->world > 1) return shard_set_state(h, host);
+  cudaError_t e = cudaMemcpyAsync(h->psi, host, size_t(16) << h->n, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "set_state");
+  return SV_OK;
+}
+
+sv_status sv_get_state(sv_handle h, double* host) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!host) return fail(SV_E_ARG, "null host buffer");
+  if (h->world > 1) return shard_get_state(h, host);
+  cudaError_t e = cudaMemcpyAsync(host, h->psi, size_t(16) << h->n, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "get_state");
+  return SV_OK;
+}
+
+sv_status sv_set_state_device(sv_handle h, const void* dev) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!dev) return fail(SV_E_ARG, "null device buffer");
+  if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
+  cudaError_t e = cudaMemcpyAsync(h->psi, dev, size_t(16) << h->n, cudaMemcpyDeviceToDevice, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "set_state_device");
+  return SV_OK;
+}
+
+sv_status sv_get_state_device(sv_handle h, void* dev) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!dev) return fail(SV_E_ARG, "null device buffer");
+  if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
+  cudaError_t e = cudaMemcpyAsync(dev, h->psi, size_t(16) << h->n, cudaMemcpyDeviceToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "get_state_device");
+  return SV_OK;
+}
+
+sv_status sv_apply_gate(sv_handle h, const sv_gate* g, const double* params, int32_t n_params) {
+  return sv_apply_circuit(h, g, 1, params, n_params);
+}
+
+sv_status sv_apply_circuit(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params, int32_t n_params) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  std::vector<BoundGate> bg;
+  rc = bind_circuit(h, gates, n_gates, params, n_params, false, &bg);
+  if (rc) return rc;
+  if (h->world > 1) return shard_apply(h, bg);
+  return apply_bound(h, bg);
+}
+
+sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, double* out_value) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!out_value) return fail(SV_E_ARG, "null out_value");
+  PauliGroups G;
+  rc = group_terms(h, terms, n_terms, &G);
+  if (rc) return rc;
+  if (h->world > 1) return shard_expectation(h, G, out_value);
+  *out_value = 0.0;
+  if (G.xs.empty()) return SV_OK;
+  const int grid = pauli_grid(h->n_local);
+  const size_t ng = G.xs.size();
+  if (!h->d_partials.ensure(ng * grid * 8) || !h->d_out.ensure(ng * 8)) return fail(SV_E_OOM, "partials");
+  double* dp = static_cast<double*>(h->d_partials.p);
+  rc = run_groups(h, G, h->psi, nullptr, dp, grid);
+  if (rc) return rc;
+  cudaError_t e = launch_reduce_slots(dp, (int)ng, grid, static_cast<double*>(h->d_out.p), h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "reduce");
+  h->stats.kernel_launches += 1;
+  std::vector<double> gv(ng);
+  e = cudaMemcpyAsync(gv.data(), h->d_out.p, ng * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "expectation");
+  double E = 0.0;
+  for (double v : gv) E += v;
+  *out_value = E;
+  return SV_OK;
+}
+
+sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params,
+                                   int32_t n_params, const sv_pauli* terms, int64_t n_terms, double* out_value,
+                                   double* out_grad) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!out_value || (n_params > 0 && !out_grad)) return fail(SV_E_ARG, "null output");
+  std::vector<BoundGate> bg;
+  rc = bind_circuit(h, gates, n_gates, params, n_params, true, &bg);
+  if (rc) return rc;
+  PauliGroups G;
+  rc = group_terms(h, terms, n_terms, &G);
+  if (rc) return rc;
+  if (h->world > 1) return shard_expectation_with_grad(h, bg, n_params, G, out_value, out_grad);
+  const size_t bytes = size_t(16) << h->n_local;
+  if (!h->work_psi.ensure(bytes) || !h->work_lam.ensure(bytes)) return fail(SV_E_OOM, "gradient workspaces");
+  double* psi = static_cast<double*>(h->work_psi.p);
+  double* lam = static_cast<double*>(h->work_lam.p);
+  cudaError_t e = cudaMemcpyAsync(psi, h->psi, bytes, cudaMemcpyDeviceToDevice, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "copy psi0");
+  h->stats.algorithmic_bytes += 2.0 * (double)bytes;
+  // 1. forward
+  Plan fwd, rev;
+  build_plan(bg, h->n_local, h->opts, false, &fwd);
+  build_plan(bg, h->n_local, h->opts, true, &rev);
+  rc = upload_plan(h, fwd);
+  if (rc) return rc;
+  rc = run_plan(h, fwd, psi, nullptr, nullptr, 0);
+  if (rc) return rc;
+  h->stats.gates_applied += (int64_t)bg.size();
+  // 2. lambda = H psi, E partials
+  const int pgrid = pauli_grid(h->n_local);
+  const size_t ng = G.xs.size();
+  int rk = rev.passes.empty() ? 1 : rev.passes[0].k;
+  const int agrid = pass_grid(h->n_local, rk, true);
+  const size_t ns = (size_t)rev.n_grad_slots;
+  const size_t part_doubles = ng * pgrid + ns * agrid;
+  if (!h->d_partials.ensure(part_doubles * 8 + 8) || !h->d_out.ensure((ng + ns) * 8 + 8)) return fail(SV_E_OOM, "partials");
+  double* dp = static_cast<double*>(h->d_partials.p);
+  if (ng == 0) {
+    e = cudaMemsetAsync(lam, 0, bytes, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "zero lambda");
+  } else {
+    rc = run_groups(h, G, psi, lam, dp, pgrid);
+    if (rc) return rc;
+  }
+  // 3. reverse sweep over (psi, lambda)
+  if (!rev.passes.empty()) {
+    rc = upload_plan(h, rev);
+    if (rc) return rc;
+    rc = run_plan(h, rev, psi, lam, dp + ng * pgrid, agrid);
+    if (rc) return rc;
+  }
+  // 4. reductions
+  double* dout = static_cast<double*>(h->d_out.p);
+  e = launch_reduce_slots(dp, (int)ng, pgrid, dout, h->stream);
+  if (e == cudaSuccess && ns) e = launch_reduce_slots(dp + ng * pgrid, (int)ns, agrid, dout + ng, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "reduce");
+  h->stats.kernel_launches += (ng ? 1 : 0) + (ns ? 1 : 0);
+  std::vector<double> hv(ng + ns);
+  if (ng + ns) {
+    e = cudaMemcpyAsync(hv.data(), dout, (ng + ns) * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "gradient readback");
+  }
+  double E = 0.0;
+  for (size_t g = 0; g < ng; ++g) E += hv[g];
+  *out_value = E;
+  for (int32_t p = 0; p < n_params; ++p) out_grad[p] = 0.0;
+  // chain rule, in reverse-sweep slot order (fixed): g[p] += coeff_k * 2 Re d_k
+  for (size_t s = 0; s < ns; ++s) out_grad[rev.slot_param[s]] += rev.slot_coeff[s] * 2.0 * hv[ng + s];
+  return SV_OK;
+}
+
+sv_status sv_get_stats(sv_handle h, sv_stats* out) {
+  if (!h || !out) return fail(SV_E_ARG, "null argument");
+  *out = h->stats;
+  return SV_OK;
+}
+
+sv_status sv_reset_stats(sv_handle h) {
+  if (!h) return fail(SV_E_ARG, "null argument");
+  std::memset(&h->stats, 0, sizeof(h->stats));
+  return SV_OK;
+}
+
+}  // extern "C"
+
+#include "sv_debug.h"
+
+extern "C" sv_status sv_plan_info(int32_t n_qubits, const sv_gate* gates, int64_t n_gates, const double* params,
+                                  int32_t n_params, int32_t adjoint, int32_t tile_qubits, int32_t fusion,
+                                  sv_pass_info* out, int64_t cap, int64_t* n_passes) {
+  if (n_qubits < 1 || n_qubits > 40 || !n_passes) return fail(SV_E_ARG, "bad arguments");
+  sv_state_s tmp;
+  tmp.n = tmp.n_local = n_qubits;
+  std::vector<BoundGate> bg;
+  int rc = bind_circuit(&tmp, gates, n_gates, params, n_params, adjoint != 0, &bg);
+  if (rc) return rc;
+  PlanOptions o;
+  o.tile_qubits = tile_qubits;
+  o.fusion = fusion != 0;
+  Plan plan;
+  build_plan(bg, n_qubits, o, adjoint != 0, &plan);
+  *n_passes = (int64_t)plan.passes.size();
+  for (size_t i = 0; i < plan.passes.size() && (int64_t)i < cap; ++i) {
+    const PassDesc& pd = plan.passes[i];
+    sv_pass_info& r = out[i];
+    r.k = pd.k;
+    r.low = pd.low;
+    r.R = pd.R;
+    r.n_ops = pd.op_end - pd.op_begin;
+    r.n_stages = pd.stage_end - pd.stage_begin;
+    r.n_grad = pd.n_grad;
+    r.tile_mask = 0;
+    for (int p = 0; p < pd.k; ++p) r.tile_mask |= 1ull << pd.tq[p];
+    r.nondiag_mask = 0;
+    for (int j = pd.op_begin; j < pd.op_end; ++j) {
+      const DevOp& op = plan.ops[j];
+      if (op.type == OP_D1 || op.type == OP_D2) continue;
+      r.nondiag_mask |= 1ull << op.qa;
+      if (op.qb >= 0) r.nondiag_mask |= 1ull << op.qb;
+    }
+  }
+  return SV_OK;
+}

@@ -1,0 +1,439 @@
+// kernels.cu — sm_100a kernels of the state-vector hot path.
+//
+//  k_pass<DUAL=false>  fused forward gate pass: each CTA loads 2^k amplitudes of
+//                      one tile into shared memory (contiguous 16*2^L-byte chunks, 16-byte
+//                      coalesced loads), applies every op of the pass in order, writes the tile
+//                      back: one HBM read + write of the state for all gates of the pass.
+//  k_pass<DUAL=true>   fused adjoint pass (a6): the same on psi and lambda together; before
+//                      un-applying a parametrised op it accumulates Re<lambda|D|psi> over the tile
+//                      into a per-CTA partial (fixed order: deterministic).
+//  k_pauli_group       one read pass per x-mask group of Pauli terms (a4/a5): pairs (i, i^x) read
+//                      once, every term of the group evaluated from the index bits; optionally
+//                      writes/accumulates lambda = H psi; per-CTA partials of <psi|H_group|psi>.
+//  k_reduce_slots      fixed-order reduction of per-CTA partials (a7).
+//
+// Gate classes follow the paper (§3.1): X-like (anti-diagonal, "swap with scaling"),
+// Z-like (diagonal, "no pairing"), general 2x2 pairs, two-qubit quads.
+#include <cstdint>
+
+#include "cx.cuh"
+#include "sv_internal.h"
+
+namespace sv {
+namespace {
+
+__device__ __forceinline__ uint32_t insert_zero(uint32_t j, int p) {
+  const uint32_t lo = j & ((1u << p) - 1u);
+  return ((j >> p) << (p + 1)) | lo;
+}
+__device__ __forceinline__ uint64_t insert_zero64(uint64_t j, int p) {
+  const uint64_t lo = j & ((1ull << p) - 1ull);
+  return ((j >> p) << (p + 1)) | lo;
+}
+
+constexpr int kThreads = 256;
+
+// Block-wide sum; result valid in thread 0. scratch: >= kThreads/32 doubles.
+__device__ double block_sum(double v, double* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += scratch[i];
+  }
+  return r;
+}
+
+struct PassArgs {
+  int32_t k, low, nops, n_outer;
+  int8_t tq[kMaxTileQubits + 3];
+  int8_t oq[64];
+  int64_t ntiles;
+  const DevOp* ops;
+  const double* mats;
+  int32_t nmats;
+  double* partials;
+  int32_t grid;
+};
+
+// Applies one op to a tile buffer t (2^k amplitudes in shared memory).
+__device__ __forceinline__ void apply_op(double2* t, const DevOp& o, const double2* m, int k, uint64_t base) {
+  const uint32_t N = 1u << k;
+  const uint32_t ct = (uint32_t)o.ctile;
+  switch (o.type) {
+    case OP_M1: {
+      const int p = o.pa;
+      const double2 m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
+      for (uint32_t j = threadIdx.x; j < (N >> 1); j += blockDim.x) {
+        const uint32_t i0 = insert_zero(j, p), i1 = i0 | (1u << p);
+        if ((i0 & ct) != ct) continue;
+        const double2 v0 = t[i0], v1 = t[i1];
+        t[i0] = cfma(m00, v0, cmul(m01, v1));
+        t[i1] = cfma(m10, v0, cmul(m11, v1));
+      }
+      break;
+    }
+    case OP_AX1: {  // X-like: new[i0] = a old[i1], new[i1] = b old[i0]
+      const int p = o.pa;
+      const double2 a = m[0], b = m[1];
+      for (uint32_t j = threadIdx.x; j < (N >> 1); j += blockDim.x) {
+        const uint32_t i0 = insert_zero(j, p), i1 = i0 | (1u << p);
+        if ((i0 & ct) != ct) continue;
+        const double2 v0 = t[i0], v1 = t[i1];
+        t[i0] = cmul(a, v1);
+        t[i1] = cmul(b, v0);
+      }
+      break;
+    }
+    case OP_D1: {  // Z-like: per-amplitude scale, no pairing
+      const double2 a = m[0], b = m[1];
+      if (o.pa < 0) {
+        const double2 f = ((base >> o.qa) & 1ull) ? b : a;
+        for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+          if ((e & ct) != ct) continue;
+          t[e] = cmul(f, t[e]);
+        }
+      } else {
+        const int p = o.pa;
+        for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+          if ((e & ct) != ct) continue;
+          t[e] = cmul(((e >> p) & 1u) ? b : a, t[e]);
+        }
+      }
+      break;
+    }
+    case OP_D2: {
+      for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+        if ((e & ct) != ct) continue;
+        const uint32_t b0 = o.pa >= 0 ? ((e >> o.pa) & 1u) : (uint32_t)((base >> o.qa) & 1ull);
+        const uint32_t b1 = o.pb >= 0 ? ((e >> o.pb) & 1u) : (uint32_t)((base >> o.qb) & 1ull);
+        t[e] = cmul(m[b0 | (b1 << 1)], t[e]);
+      }
+      break;
+    }
+    case OP_M2: {
+      const int pa = o.pa, pb = o.pb;
+      const int plo = pa < pb ? pa : pb, phi = pa < pb ? pb : pa;
+      for (uint32_t j = threadIdx.x; j < (N >> 2); j += blockDim.x) {
+        const uint32_t i00 = insert_zero(insert_zero(j, plo), phi);
+        if ((i00 & ct) != ct) continue;
+        const uint32_t idx[4] = {i00, i00 | (1u << pa), i00 | (1u << pb), i00 | (1u << pa) | (1u << pb)};
+        double2 v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = t[idx[c]];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double2 acc = cmul(m[r * 4 + 0], v[0]);
+#pragma unroll
+          for (int c = 1; c < 4; ++c) acc = cfma(m[r * 4 + c], v[c], acc);
+          t[idx[r]] = acc;
+        }
+      }
+      break;
+    }
+    case OP_SWAP: {
+      const int pa = o.pa, pb = o.pb;
+      const int plo = pa < pb ? pa : pb, phi = pa < pb ? pb : pa;
+      for (uint32_t j = threadIdx.x; j < (N >> 2); j += blockDim.x) {
+        const uint32_t i00 = insert_zero(insert_zero(j, plo), phi);
+        if ((i00 & ct) != ct) continue;
+        const uint32_t i01 = i00 | (1u << pa), i10 = i00 | (1u << pb);
+        const double2 v = t[i01];
+        t[i01] = t[i10];
+        t[i10] = v;
+      }
+      break;
+    }
+  }
+}
+
+// Re <lam| (Pi_C (x) G) |psi> over one tile, this thread's share.
+__device__ __forceinline__ double overlap_op(const double2* ps, const double2* la, const DevOp& o, const double2* g,
+                                             int k, uint64_t base) {
+  const uint32_t N = 1u << k;
+  const uint32_t ct = (uint32_t)o.ctile;
+  double acc = 0.0;
+  if (o.gen_diag) {
+    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+      if ((e & ct) != ct) continue;
+      uint32_t idx = o.pa >= 0 ? ((e >> o.pa) & 1u) : (uint32_t)((base >> o.qa) & 1ull);
+      if (o.gen_dim == 4) idx |= (o.pb >= 0 ? ((e >> o.pb) & 1u) : (uint32_t)((base >> o.qb) & 1ull)) << 1;
+      acc += re_conj_mul(la[e], cmul(g[idx], ps[e]));
+    }
+  } else if (o.gen_dim == 2) {
+    const int p = o.pa;
+    for (uint32_t j = threadIdx.x; j < (N >> 1); j += blockDim.x) {
+      const uint32_t i0 = insert_zero(j, p), i1 = i0 | (1u << p);
+      if ((i0 & ct) != ct) continue;
+      const double2 v0 = ps[i0], v1 = ps[i1];
+      acc += re_conj_mul(la[i0], cfma(g[0], v0, cmul(g[1], v1)));
+      acc += re_conj_mul(la[i1], cfma(g[2], v0, cmul(g[3], v1)));
+    }
+  } else {
+    const int pa = o.pa, pb = o.pb;
+    const int plo = pa < pb ? pa : pb, phi = pa < pb ? pb : pa;
+    for (uint32_t j = threadIdx.x; j < (N >> 2); j += blockDim.x) {
+      const uint32_t i00 = insert_zero(insert_zero(j, plo), phi);
+      if ((i00 & ct) != ct) continue;
+      const uint32_t idx[4] = {i00, i00 | (1u << pa), i00 | (1u << pb), i00 | (1u << pa) | (1u << pb)};
+      double2 v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = ps[idx[c]];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double2 w = cmul(g[r * 4], v[0]);
+#pragma unroll
+        for (int c = 1; c < 4; ++c) w = cfma(g[r * 4 + c], v[c], w);
+        acc += re_conj_mul(la[idx[r]], w);
+      }
+    }
+  }
+  return acc;
+}
+
+template <bool DUAL>
+__global__ void __launch_bounds__(kThreads) k_pass(double2* __restrict__ psi, double2* __restrict__ lam, PassArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t N = 1u << a.k;
+  double2* tp = reinterpret_cast<double2*>(smem_raw);
+  double2* tl = DUAL ? tp + N : nullptr;
+  DevOp* s_ops = reinterpret_cast<DevOp*>(tp + (DUAL ? 2 * N : N));
+  double* s_mats = reinterpret_cast<double*>(s_ops + a.nops);
+  const int nhi = 1 << (a.k - a.low);
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(s_mats + ((a.nmats + 1) & ~1));
+  double* s_acc = reinterpret_cast<double*>(s_hi + nhi);  // per-op grad accumulators (DUAL)
+  double* s_red = s_acc + (DUAL ? a.nops : 0);
+
+  // ---- per-CTA setup: op list, matrices, high-offset table ----
+  {
+    const int op_words = a.nops * (int)(sizeof(DevOp) / 8);
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(a.ops);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(s_ops);
+    for (int i = threadIdx.x; i < op_words; i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < a.nmats; i += blockDim.x) s_mats[i] = a.mats[i];
+    for (int h = threadIdx.x; h < nhi; h += blockDim.x) {
+      uint64_t off = 0;
+      for (int b = 0; b < a.k - a.low; ++b)
+        if ((h >> b) & 1) off |= 1ull << a.tq[a.low + b];
+      s_hi[h] = off;
+    }
+    if (DUAL)
+      for (int i = threadIdx.x; i < a.nops; i += blockDim.x) s_acc[i] = 0.0;
+  }
+  __syncthreads();
+  const uint32_t lowmask = (1u << a.low) - 1u;
+
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    uint64_t base = 0;
+    for (int j = 0; j < a.n_outer; ++j)
+      if ((tile >> j) & 1) base |= 1ull << a.oq[j];
+    // ---- load (consecutive threads -> consecutive amplitudes of a 16*2^L-byte chunk) ----
+    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+      const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
+      tp[e] = psi[gi];
+      if (DUAL) tl[e] = lam[gi];
+    }
+    __syncthreads();
+    // ---- ops ----
+    for (int i = 0; i < a.nops; ++i) {
+      const DevOp& o = s_ops[i];
+      const bool outer_ok = (base & o.couter) == o.couter;
+      if (DUAL && o.grad_slot >= 0) {
+        double part = outer_ok ? overlap_op(tp, tl, o, reinterpret_cast<const double2*>(s_mats + o.gen_off), a.k, base)
+                               : 0.0;
+        part = block_sum(part, s_red);
+        if (threadIdx.x == 0) s_acc[i] += part;
+        __syncthreads();
+      }
+      if (!outer_ok) continue;
+      const double2* m = reinterpret_cast<const double2*>(s_mats + o.mat_off);
+      apply_op(tp, o, m, a.k, base);
+      if (DUAL) apply_op(tl, o, m, a.k, base);
+      __syncthreads();
+    }
+    // ---- store ----
+    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+      const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
+      psi[gi] = tp[e];
+      if (DUAL) lam[gi] = tl[e];
+    }
+    __syncthreads();
+  }
+  if (DUAL && threadIdx.x == 0) {
+    for (int i = 0; i < a.nops; ++i)
+      if (s_ops[i].grad_slot >= 0) a.partials[(int64_t)s_ops[i].grad_slot * a.grid + blockIdx.x] = s_acc[i];
+  }
+}
+
+__global__ void k_init(double2* psi, int64_t n, bool one) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    psi[i] = make_double2((one && i == 0) ? 1.0 : 0.0, 0.0);
+}
+
+// mode 0: E partials only; 1: lam = H_g psi; 2: lam += H_g psi.
+__global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restrict__ psi, double2* __restrict__ lam,
+                                                          int mode, int n, uint64_t x, const uint64_t* __restrict__ z,
+                                                          const double2* __restrict__ c, int nterms,
+                                                          double* __restrict__ partials) {
+  __shared__ uint64_t s_z[256];
+  __shared__ double2 s_c[256];
+  __shared__ double s_red[kThreads / 32];
+  for (int i = threadIdx.x; i < nterms; i += blockDim.x) { s_z[i] = z[i]; s_c[i] = c[i]; }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  if (x == 0) {
+    const int64_t N = 1ll << n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+      double2 C = make_double2(0.0, 0.0);
+      for (int j = 0; j < nterms; ++j) {
+        const double sg = (__popcll(i & s_z[j]) & 1) ? -1.0 : 1.0;
+        C.x = fma(sg, s_c[j].x, C.x);
+        C.y = fma(sg, s_c[j].y, C.y);
+      }
+      const double2 v = psi[i];
+      const double2 w = cmul(C, v);
+      acc += re_conj_mul(v, w);
+      if (mode == 1) lam[i] = w;
+      else if (mode == 2) { double2 l = lam[i]; l.x += w.x; l.y += w.y; lam[i] = l; }
+    }
+  } else {
+    const int h = 63 - __clzll(x);
+    const int64_t P = 1ll << (n - 1);
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += stride) {
+      const uint64_t i = insert_zero64((uint64_t)p, h), ip = i ^ x;
+      double2 Ci = make_double2(0.0, 0.0), Cp = make_double2(0.0, 0.0);
+      for (int j = 0; j < nterms; ++j) {
+        // (P psi)[i] = c_j (-1)^{popc((i^x) & z)} psi[i^x]  (c_j includes i^{popc(x&z)})
+        const double si = (__popcll(ip & s_z[j]) & 1) ? -1.0 : 1.0;
+        const double sp = (__popcll(i & s_z[j]) & 1) ? -1.0 : 1.0;
+        Ci.x = fma(si, s_c[j].x, Ci.x); Ci.y = fma(si, s_c[j].y, Ci.y);
+        Cp.x = fma(sp, s_c[j].x, Cp.x); Cp.y = fma(sp, s_c[j].y, Cp.y);
+      }
+      const double2 vi = psi[i], vp = psi[ip];
+      const double2 wi = cmul(Ci, vp), wp = cmul(Cp, vi);
+      acc += re_conj_mul(vi, wi) + re_conj_mul(vp, wp);
+      if (mode == 1) { lam[i] = wi; lam[ip] = wp; }
+      else if (mode == 2) {
+        double2 a = lam[i], b = lam[ip];
+        a.x += wi.x; a.y += wi.y; b.x += wp.x; b.y += wp.y;
+        lam[i] = a; lam[ip] = b;
+      }
+    }
+  }
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+// out[s] = sum_{j < per} partials[s*per + j], fixed order (strided per-thread sums, then a fixed tree).
+__global__ void __launch_bounds__(kThreads) k_reduce_slots(const double* __restrict__ partials, int per,
+                                                           double* __restrict__ out) {
+  __shared__ double s_red[kThreads / 32];
+  const double* p = partials + (int64_t)blockIdx.x * per;
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < per; j += blockDim.x) acc += p[j];
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+
+size_t pass_smem_bytes(int k, int low, int nops, int nmats, bool dual) {
+  const size_t N = size_t(1) << k;
+  size_t b = N * 16 * (dual ? 2 : 1);
+  b += (size_t)nops * sizeof(DevOp);
+  b += (size_t)((nmats + 1) & ~1) * 8;
+  b += (size_t(1) << (k - low)) * 8;
+  b += (dual ? (size_t)nops * 8 : 0) + (kThreads / 32) * 8;
+  return b;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+}  // namespace
+
+int pass_grid(int n_local, int k, bool dual) {
+  const int64_t ntiles = 1ll << (n_local - k);
+  const int64_t want = (int64_t)num_sms() * 2 * ((k <= 10) ? 2 : 1);
+  return (int)(ntiles < want ? ntiles : want);
+}
+
+cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStream_t s) {
+  const PassDesc& pd = *L.pd;
+  if (pd.R > 0) return launch_pass_reg(psi, lam, L, s);
+  PassArgs a;
+  a.k = pd.k;
+  a.low = pd.low;
+  a.nops = pd.op_end - pd.op_begin;
+  for (int i = 0; i < kMaxTileQubits + 3; ++i) a.tq[i] = pd.tq[i];
+  uint64_t tmask = 0;
+  for (int p = 0; p < pd.k; ++p) tmask |= 1ull << pd.tq[p];
+  a.n_outer = 0;
+  for (int q = 0; q < L.n_local; ++q)
+    if (!((tmask >> q) & 1ull)) a.oq[a.n_outer++] = (int8_t)q;
+  a.ntiles = 1ll << (L.n_local - pd.k);
+  a.ops = L.d_ops + pd.op_begin;
+  a.mats = L.d_mats + pd.mat_begin;
+  a.nmats = L.nmats;
+  a.partials = L.d_partials;
+  a.grid = L.grid;
+  const bool dual = lam != nullptr;
+  const size_t smem = pass_smem_bytes(a.k, a.low, a.nops, a.nmats, dual);
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[dual]) {
+    cudaError_t e = dual ? cudaFuncSetAttribute(k_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
+                         : cudaFuncSetAttribute(k_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[dual] = true;
+  }
+  if (dual)
+    k_pass<true><<<L.grid, kThreads, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
+  else
+    k_pass<false><<<L.grid, kThreads, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s) {
+  int64_t blocks = (n_amps + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_init<<<(int)blocks, kThreads, 0, s>>>(reinterpret_cast<double2*>(psi), n_amps, one_at_zero);
+  return cudaGetLastError();
+}
+
+int pauli_grid(int n_local) {
+  const int64_t work = (1ll << n_local) / kThreads / 4;
+  const int64_t cap = (int64_t)num_sms() * 4;
+  int64_t g = work < cap ? work : cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_pauli_group(const double* psi, double* lam, bool lam_accumulate, int n_local, uint64_t x,
+                               const uint64_t* d_z, const double* d_c, int nterms, double* d_partials, int grid,
+                               cudaStream_t s) {
+  const int mode = lam == nullptr ? 0 : (lam_accumulate ? 2 : 1);
+  k_pauli_group<<<grid, kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<double2*>(lam), mode,
+                                          n_local, x, d_z, reinterpret_cast<const double2*>(d_c), nterms, d_partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out, cudaStream_t s) {
+  if (n_slots <= 0) return cudaSuccess;
+  k_reduce_slots<<<n_slots, kThreads, 0, s>>>(d_partials, per_slot, d_out);
+  return cudaGetLastError();
+}
+
+}  // namespace sv

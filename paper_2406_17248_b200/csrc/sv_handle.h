@@ -1,0 +1,69 @@
+// sv_handle.h — the opaque handle behind sv_handle (include/sv.h) and helpers shared by api.cpp
+// and shard.cpp.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "sv.h"
+#include "sv_internal.h"
+
+namespace sv {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool ensure(size_t bytes);
+  void release();
+};
+
+struct ShardState;  // shard.cpp
+
+}  // namespace sv
+
+struct sv_state_s {
+  int n = 0;           // logical qubits
+  int n_local = 0;     // qubits held per shard (n - log2 world)
+  int world = 1, rank = 0;
+  int device = 0;
+  bool poisoned = false;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  sv::DevBuf state, work_psi, work_lam;
+  double* psi = nullptr;
+  sv::DevBuf d_ops, d_mats, d_terms, d_partials, d_out;
+  std::vector<char> h_stage;
+  size_t plan_stages_off = 0, plan_mats_off = 0;
+  sv::PlanOptions opts;
+  sv_stats stats{};
+  sv::ShardState* shard = nullptr;
+};
+
+namespace sv {
+
+int fail(int code, const std::string& msg);
+int cuda_fail(sv_state_s* h, cudaError_t e, const char* where);
+int check_handle(sv_state_s* h);
+int upload_plan(sv_state_s* h, const Plan& plan);
+int run_plan(sv_state_s* h, const Plan& plan, double* psi, double* lam, double* d_partials, int grid);
+int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg);
+
+struct PauliGroups {
+  std::vector<uint64_t> xs;           // distinct x-masks, ascending
+  std::vector<int> begin, end;        // term ranges per group in z / c
+  std::vector<uint64_t> z;
+  std::vector<double> c;              // complex coefficients c_t * i^{popc(x&z)} (re, im)
+};
+int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid);
+
+// shard.cpp
+void destroy_sharding(sv_state_s* h);
+int shard_reset(sv_state_s* h);
+int shard_set_state(sv_state_s* h, const double* host);
+int shard_get_state(sv_state_s* h, double* host);
+int shard_apply(sv_state_s* h, const std::vector<BoundGate>& bg);
+int shard_expectation(sv_state_s* h, const PauliGroups& G, double* out);
+int shard_expectation_with_grad(sv_state_s* h, const std::vector<BoundGate>& bg, int32_t n_params,
+                                const PauliGroups& G, double* out_value, double* out_grad);
+
+}  // namespace sv

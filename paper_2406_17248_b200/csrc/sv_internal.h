@@ -1,0 +1,156 @@
+// sv_internal.h — internal types shared by the host planner (plan.cpp, api.cpp) and the sm_100a
+// kernels (kernels.cu). Not part of the ABI (include/sv.h is).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace sv {
+
+struct Cx {
+  double re, im;
+};
+
+// ---------------------------------------------------------------------------------------------
+// Device-side op of a fused tile pass. A tile is the set of 2^k amplitudes whose indices agree on
+// every qubit outside the tile's qubit list tq[0..k) (tq[p] = physical qubit of tile position p,
+// tq[p] = p for p < L so the low L qubits form contiguous 16*2^L-byte chunks).
+//
+// Classes follow the paper's taxonomy (§3.1): X-like = anti-diagonal, Z-like = diagonal,
+// general 2x2, and two-qubit groups.
+enum OpType : int32_t {
+  OP_M1 = 0,   // general 2x2 on tile position pa                 mat: 8 doubles (row-major)
+  OP_AX1 = 1,  // X-like [[0,a],[b,0]] on tile position pa         mat: a, b (4 doubles)
+  OP_D1 = 2,   // Z-like diag(a,b) on physical qubit qa (any)      mat: a, b (4 doubles)
+  OP_M2 = 3,   // 4x4 on tile positions pa (index bit 0), pb (bit 1) mat: 32 doubles
+  OP_D2 = 4,   // diagonal 4 entries on physical qubits qa (bit0), qb (bit1)  mat: 8 doubles
+  OP_SWAP = 5, // SWAP of tile positions pa, pb                    mat: none
+};
+
+struct DevOp {
+  int32_t type;
+  int16_t pa, pb;      // tile positions of the targets (-1 when the target is outside the tile)
+  int16_t qa, qb;      // physical qubits of the targets (local index space)
+  int8_t ra, rb;       // register-kernel: register index of pa / pb in the op's stage (-1: thread bit / outer)
+  uint8_t cj;          // register-kernel: control mask over register indices of the op's stage
+  uint8_t pad0;
+  int32_t mat_off;     // offset (doubles) of the op's matrix in the pass' matrix block
+  int32_t grad_slot;   // >= 0: adjoint overlap slot (global across the reverse plan); -1 none
+  int32_t gen_off;     // offset of the generator matrix G (2x2 or 4x4 complex) for grad ops
+  int16_t gen_dim;     // 2 or 4 (generator acts on the targets) or 0
+  int16_t gen_diag;    // 1: generator diagonal (entries gen_off[0..gen_dim)), evaluated per element
+  int16_t stage;       // register-kernel: stage index within the pass
+  int16_t grad_local;  // index among the pass' grad ops (-1 none)
+  uint64_t ctile;      // control bits in tile-position space
+  uint64_t cthr;       // register-kernel: control bits on the thread-bit positions of the op's stage
+  uint64_t couter;     // control bits in local physical index space, outside the tile
+};
+static_assert(sizeof(DevOp) == 64, "DevOp layout");
+
+// Register-kernel stage: which tile positions the 2^R amplitudes a thread holds in registers span
+// (regpos), and the order of the remaining positions over thread-index bits (thrpos; bits 0..4 =
+// lane). Ops of a stage whose non-diagonal targets are all register positions run from registers.
+struct StageDesc {
+  int8_t regpos[4];
+  int8_t thrpos[12];
+  int32_t op_begin, op_end;  // range in the pass' op list (pass-relative)
+  uint16_t swz_reg[16];      // swizzled smem offset contribution of register index j (XOR-linear)
+};
+static_assert(sizeof(StageDesc) == 56, "StageDesc layout");
+
+
+constexpr int kMaxTileQubits = 13;
+constexpr int kMaxOpsPerPass = 256;
+constexpr int kMaxMatDoublesPerPass = 2048;
+
+struct PassDesc {
+  int32_t k;                // tile qubits
+  int32_t low;              // L: tq[p] = p for p < low
+  int8_t tq[kMaxTileQubits + 3];  // physical qubit of each tile position
+  int32_t op_begin, op_end; // range in the plan's op array
+  int32_t mat_begin;        // base offset of this pass' matrices in the plan's matrix array
+  int32_t n_grad;           // grad ops in this pass (adjoint)
+  int32_t R;                // register qubits per thread (0: shared-memory kernel)
+  int32_t stage_begin, stage_end;  // range in the plan's stage array
+};
+
+// A compiled plan: passes over one vector (forward) or two (adjoint).
+struct Plan {
+  std::vector<PassDesc> passes;
+  std::vector<DevOp> ops;
+  std::vector<double> mats;
+  std::vector<StageDesc> stages;
+  int n_grad_slots = 0;
+  std::vector<int32_t> slot_param;   // slot -> parameter index
+  std::vector<double> slot_coeff;    // slot -> chain-rule coefficient (coeff of the occurrence)
+};
+
+// ---------------------------------------------------------------------------------------------
+// Host-side gate after binding: class + entries, logical qubits.
+enum GateClass : int32_t { GC_XLIKE = 0, GC_ZLIKE = 1, GC_GEN1 = 2, GC_GEN2 = 3, GC_DIAG2 = 4, GC_SWAP = 5 };
+
+struct BoundGate {
+  int32_t cls;
+  int32_t kind;
+  int32_t t0, t1;        // logical targets (t1 = -1 for one-qubit)
+  uint64_t controls;     // logical control mask
+  Cx m[16];              // XLIKE/ZLIKE: m[0]=a, m[1]=b; GEN1: 2x2; GEN2: 4x4; DIAG2: m[0..3]
+  int32_t param;         // -1 fixed
+  double coeff;          // chain-rule coefficient
+  int32_t gen_dim;       // generator dimension for parametrised gates (2 / 4), else 0
+  Cx gen[16];            // D = (dU/dphi) U^dagger on the target space (2x2 or 4x4)
+};
+
+// Binding (gates.cpp). Returns SV status code; fills `out`. `err` receives a message.
+int bind_gate(int n, const void* sv_gate_ptr, const double* params, int32_t n_params, bool for_grad,
+              BoundGate* out, std::string* err);
+BoundGate dagger(const BoundGate& g);
+
+// Planner (plan.cpp). perm: logical qubit -> physical (local) qubit; n_local: local qubits.
+struct PlanOptions {
+  int tile_qubits = 0;   // 0 = auto
+  int low_qubits = 3;
+  bool fusion = true;
+  int kernel = 1;        // 1: register-blocked stage kernel where possible, 0: shared-memory kernel
+};
+int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual);
+void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOptions& o, bool reverse_for_adjoint,
+                Plan* plan);
+
+// ---------------------------------------------------------------------------------------------
+// Kernel launchers (kernels.cu).
+struct PassLaunch {
+  const PassDesc* pd;
+  const DevOp* d_ops;      // device pointer to the plan's ops
+  const double* d_mats;    // device pointer to the plan's matrices
+  const StageDesc* d_stages;  // device pointer to the plan's stages
+  double* d_partials;      // [n_slots][grid] adjoint overlap partials (or null)
+  int nmats;               // matrix doubles of this pass
+  int grid;                // CTAs
+  int n_local;
+  uint64_t rank_bits;      // (sharded) global index bits of this shard, for controls/diagonals on
+                           // global qubits folded by the planner (0 single-GPU)
+};
+cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
+cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
+int pass_grid(int n_local, int k, bool dual);
+
+cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
+
+// Pauli groups (kernels.cu): terms sharing one x-mask.
+struct PauliGroupDev {
+  uint64_t x;
+  int32_t term_begin, term_end;   // range in the z / coeff arrays
+};
+cudaError_t launch_pauli_group(const double* psi, double* lam, bool lam_accumulate, int n_local, uint64_t x,
+                               const uint64_t* d_z, const double* d_c /* complex coeff pairs */, int nterms,
+                               double* d_partials, int grid, cudaStream_t s);
+int pauli_grid(int n_local);
+cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out,
+                                cudaStream_t s);
+
+}  // namespace sv

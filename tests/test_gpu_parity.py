@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star; derivation in DESIGN.md §Tolerances): 1e-10 absolute per
+amplitude, 1e-9 on expectations and gradients.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-10
+E_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2406_17248_b200 as P
+    return P
+
+
+def _gpu_run(P, n, gates, params=None, psi0=None, opts=None):
+    sv = P.StateVector(n)
+    for k, v in (opts or {}).items():
+        sv.set_option(k, v)
+    if psi0 is not None:
+        sv.set_state(psi0)
+    sv.apply_circuit(gates, params)
+    out = sv.get_state()
+    sv.close()
+    return out
+
+
+def _assert_amps(got, ref, tol=AMP_TOL):
+    err = np.max(np.abs(got - ref)) if got.size else 0.0
+    assert err <= tol, f"max |gpu - oracle| = {err:.3e} > {tol:.0e}"
+
+
+# ----------------------------------------------------------------------------- single gates
+
+def _positions(n):
+    """Target positions covering the low (in-chunk), mid (tile) and high (outer) ranges."""
+    cand = {0, 1, 2, 3, 4, 5, 7, 11, 12, n - 2, n - 1}
+    return sorted(q for q in cand if 0 <= q < n)
+
+
+@pytest.mark.parametrize("kind", W.ALL_KINDS)
+@pytest.mark.parametrize("n", [1, 2, 5, 13, 16])
+def test_every_kind_every_position(P, kind, n):
+    rng = np.random.default_rng(n * 100 + W.ALL_KINDS.index(kind))
+    two = kind in W.KINDS_2Q
+    if two and n < 2:
+        pytest.skip("two-qubit kind needs n >= 2")
+    psi0 = W.random_state(n, int(rng.integers(1 << 30)))
+    gates = []
+    for t in _positions(n):
+        for nctrl in (0, 1, 2):
+            targets = [t]
+            if two:
+                others = [q for q in range(n) if q != t]
+                targets.append(int(rng.choice(others)))
+            free = [q for q in range(n) if q not in targets]
+            if nctrl > len(free):
+                continue
+            controls = tuple(int(c) for c in rng.choice(free, nctrl, replace=False)) if nctrl else ()
+            mat = None
+            if kind == "MAT1":
+                mat = W.haar_unitary(2, rng)
+            elif kind == "MAT2":
+                mat = W.haar_unitary(4, rng)
+            elif kind in ("XLIKE", "ZLIKE"):
+                mat = rng.standard_normal(2) + 1j * rng.standard_normal(2)
+            gates.append(W.Gate(kind, tuple(targets), controls, offset=float(rng.uniform(-7, 7)), mat=mat))
+    # one gate per call (sv_apply_gate) and the whole list fused (sv_apply_circuit)
+    ref = oracle.apply_circuit(n, gates, None, psi0)
+    _assert_amps(_gpu_run(P, n, gates, None, psi0), ref)
+    sv = P.StateVector(n)
+    sv.set_state(psi0)
+    for g in gates:
+        sv.apply_gate(g)
+    _assert_amps(sv.get_state(), ref)
+    sv.close()
+
+
+def test_all_controls_max(P):
+    """n-1 controls (a single pair updated) and controls on every tile/outer position."""
+    n = 15
+    psi0 = W.random_state(n, 3)
+    gates = [W.Gate("H", (t,), tuple(q for q in range(n) if q != t)) for t in (0, 6, 14)]
+    gates += [W.Gate("RXX", (2, 13), tuple(q for q in range(n) if q not in (2, 13)), offset=0.7)]
+    _assert_amps(_gpu_run(P, n, gates, None, psi0), oracle.apply_circuit(n, gates, None, psi0))
+
+
+# ----------------------------------------------------------------------------- circuits
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 6, 9, 12, 13, 14, 17, 20])
+def test_random_complex_circuits(P, n):
+    """The paper's "complex random circuit" shape (controls p=0.3) plus user matrices."""
+    w = W.random_complex(n, 10, seed=1000 + n, n_params=5,
+                         extra_kinds=("MAT1", "MAT2", "XLIKE", "ZLIKE", "PS", "SDG", "TDG"))
+    ref = oracle.apply_circuit(n, w.gates, w.params)
+    _assert_amps(_gpu_run(P, n, w.gates, w.params), ref)
+
+
+@pytest.mark.parametrize("opts", [{1: 4}, {1: 7}, {1: 10}, {2: 0}, {3: 0}, {3: 5}, {1: 13}])
+def test_plan_options_do_not_change_results(P, opts):
+    """Tile width, fusion on/off and the low-qubit granule only change the schedule."""
+    n = 16
+    w = W.random_complex(n, 6, seed=77, extra_kinds=("MAT2", "PS"))
+    ref = oracle.apply_circuit(n, w.gates, w.params)
+    _assert_amps(_gpu_run(P, n, w.gates, w.params, opts=opts), ref)
+
+
+def test_c4_shape_at_22q(P):
+    """C4's generator (Haar 1q + CZ bricks) at 22 qubits, depth 12."""
+    w = W.random_circuit(22, 12, seed=3040)
+    _assert_amps(_gpu_run(P, 22, w.gates), oracle.apply_circuit(22, w.gates))
+
+
+def test_mirror_and_norm_at_24q(P):
+    w = W.random_circuit(24, 6, seed=11)
+    gates = W.mirror(w.gates)
+    out = _gpu_run(P, 24, gates)
+    assert abs(out[0] - 1) < 1e-11 and np.max(np.abs(out[1:])) < 1e-11
+
+
+def test_empty_circuit_and_reset(P):
+    sv = P.StateVector(5)
+    sv.apply_circuit([])
+    st = sv.get_state()
+    assert st[0] == 1 and np.all(st[1:] == 0)
+    sv.apply_circuit([W.Gate("H", (0,))])
+    sv.reset()
+    st = sv.get_state()
+    assert st[0] == 1 and np.all(st[1:] == 0)
+    sv.close()
+
+
+# ----------------------------------------------------------------------------- expectation
+
+@pytest.mark.parametrize("n", [1, 3, 6, 12, 15, 20])
+def test_expectation_random(P, n):
+    psi = W.random_state(n, n)
+    ham = W.random_hamiltonian(n, 30, seed=n) + W.jw_hamiltonian(n, 20, seed=n) if n >= 4 else W.random_hamiltonian(n, 10, n)
+    ref = oracle.expectation(psi, ham)[0]
+    sv = P.StateVector(n)
+    sv.set_state(psi)
+    got = sv.expectation(ham)
+    sv.close()
+    assert abs(got - ref) < E_TOL
+
+
+def test_expectation_spec_values(P):
+    sv = P.StateVector(2)
+    sv.apply_circuit([W.Gate("H", (0,)), W.Gate("X", (1,), (0,))])
+    assert abs(sv.expectation([(1.0, {0: "X", 1: "X"})]) - 1.0) < 1e-14
+    assert sv.expectation([]) == 0.0
+    assert abs(sv.expectation([(0.25, {})]) - 0.25) < 1e-15
+    sv.close()
+
+
+# ----------------------------------------------------------------------------- gradients
+
+def test_c1_full(P):
+    """BASELINE configs[0]: amplitudes, E and gradient vs oracle and the closed form."""
+    w = W.c1_ghz_rx()
+    ref = oracle.apply_circuit(w.n, w.gates, w.params)
+    _assert_amps(_gpu_run(P, w.n, w.gates, w.params), ref)
+    sv = P.StateVector(w.n)
+    E, g = sv.expectation_with_grad(w.gates, w.params, w.ham)
+    th = w.params
+    assert abs(E - np.cos(th[0]) * np.cos(th[1])) < E_TOL
+    np.testing.assert_allclose(g, [-np.sin(th[0]) * np.cos(th[1]), -np.cos(th[0]) * np.sin(th[1]), 0, 0], atol=E_TOL)
+    # state untouched by _with_grad
+    st = sv.get_state()
+    assert st[0] == 1 and np.all(st[1:] == 0)
+    sv.close()
+
+
+@pytest.mark.parametrize("n,seed", [(1, 0), (2, 1), (4, 2), (6, 3), (9, 4), (13, 5), (15, 6)])
+def test_gradient_random_tasks(P, n, seed):
+    w = W.random_complex(n, 8, seed=500 + seed, n_params=6, extra_kinds=("PS", "MAT1", "MAT2"))
+    ham = W.random_hamiltonian(n, 8, seed)
+    psi0 = W.random_state(n, seed)
+    E0, g0 = oracle.adjoint_grad(n, w.gates, w.params, ham, psi0)
+    sv = P.StateVector(n)
+    sv.set_state(psi0)
+    E, g = sv.expectation_with_grad(w.gates, w.params, ham)
+    sv.close()
+    assert abs(E - E0) < E_TOL
+    np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
+
+
+def test_gradient_c2_hea_20q(P):
+    """C2: 20q HEA, 10 layers, 50-term JW-shaped H (400 params)."""
+    w = W.config("C2")
+    E0, g0 = oracle.adjoint_grad(w.n, w.gates, w.params, w.ham)
+    sv = P.StateVector(w.n)
+    E, g = sv.expectation_with_grad(w.gates, w.params, w.ham)
+    sv.close()
+    assert abs(E - E0) < E_TOL
+    np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
+
+
+def test_gradient_qaoa_p1_24q_closed_form(P):
+    """C3 graph at p=1: E and the shared-parameter gradient vs the Wang et al. closed form."""
+    from test_oracle import _qaoa_p1_closed_form
+    w = W.qaoa(24, 1, seed_graph=2403, seed_angles=2404)
+    edges = w.meta["edges"]
+    sv = P.StateVector(24)
+    E, g = sv.expectation_with_grad(w.gates, w.params, w.ham)
+    sv.close()
+    gam, bet = w.params
+    assert abs(E - _qaoa_p1_closed_form(edges, 24, gam, bet)) < E_TOL
+    h = 1e-6
+    dg = (_qaoa_p1_closed_form(edges, 24, gam + h, bet) - _qaoa_p1_closed_form(edges, 24, gam - h, bet)) / (2 * h)
+    db = (_qaoa_p1_closed_form(edges, 24, gam, bet + h) - _qaoa_p1_closed_form(edges, 24, gam, bet - h)) / (2 * h)
+    np.testing.assert_allclose(g, [dg, db], atol=1e-7)
+
+
+def test_gradient_qaoa_zero_params_24q(P):
+    w = W.config("C3")
+    sv = P.StateVector(24)
+    E, g = sv.expectation_with_grad(w.gates, np.zeros_like(w.params), w.ham)
+    sv.close()
+    assert abs(E + len(w.meta["edges"]) / 2) < E_TOL
+    np.testing.assert_allclose(g, 0, atol=E_TOL)
+
+
+# ----------------------------------------------------------------------------- errors
+
+def test_validation_errors(P):
+    sv = P.StateVector(3)
+    cases = [
+        (W.Gate("X", (3,)), "SV_E_QUBIT_RANGE"),
+        (W.Gate("X", (0,), (0,)), "SV_E_TARGET_CONTROL_OVERLAP"),
+        (W.Gate("SWAP", (1, 1)), "SV_E_DUPLICATE_TARGET"),
+        (W.Gate("RX", (0,), param=2), "SV_E_PARAM_RANGE"),
+        (W.Gate("H", (0,), param=0), "SV_E_ARG"),
+        (W.Gate("X", (0,), (5,)), "SV_E_QUBIT_RANGE"),
+    ]
+    for g, status in cases:
+        with pytest.raises(P.SvError) as ei:
+            sv.apply_circuit([W.Gate("H", (1,)), g], [0.1])
+        assert ei.value.status == status
+    # atomic: nothing applied by the failing calls
+    st = sv.get_state()
+    assert st[0] == 1
+    with pytest.raises(P.SvError) as ei:
+        sv.expectation_with_grad([W.Gate("MAT1", (0,), param=0, mat=np.eye(2))], [0.1], [(1.0, {0: "Z"})])
+    assert ei.value.status == "SV_E_NOT_DIFFERENTIABLE"
+    with pytest.raises(P.SvError) as ei:
+        sv.expectation_with_grad([W.Gate("MAT1", (0,), mat=2 * np.eye(2))], [], [(1.0, {0: "Z"})])
+    assert ei.value.status == "SV_E_NOT_UNITARY"
+    with pytest.raises(P.SvError) as ei:
+        sv.expectation([(1.0, {4: "Z"})])
+    assert ei.value.status == "SV_E_QUBIT_RANGE"
+    sv.close()
+
+
+def test_determinism(P):
+    w = W.config("C2")
+    sv = P.StateVector(w.n)
+    a = sv.expectation_with_grad(w.gates, w.params, w.ham)
+    b = sv.expectation_with_grad(w.gates, w.params, w.ham)
+    sv.close()
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
