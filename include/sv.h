@@ -117,7 +117,9 @@ typedef struct {
 enum {
   SV_OPT_TILE_QUBITS = 1,        /* k: qubits per fused tile (0 = auto)                           */
   SV_OPT_FUSION = 2,             /* 1 (default) fuse gates into tile passes; 0 one pass per gate  */
-  SV_OPT_LOW_QUBITS = 3          /* qubits 0..L-1 always in a tile (coalescing granule), default 3 */
+  SV_OPT_LOW_QUBITS = 3,         /* qubits 0..L-1 always in a tile (coalescing granule), default 3 */
+  SV_OPT_DENSE = 4,              /* 1 (default): fold register stages into dense FP64-MMA stages  */
+  SV_OPT_KERNEL = 5              /* 1 (default): register-blocked kernel; 0: shared-memory kernel */
 };
 
 /* a1: |0...0> on n_qubits (1 <= n <= 40 subject to memory), current CUDA device, new stream. */

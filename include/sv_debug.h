@@ -23,6 +23,8 @@ typedef struct {
   int32_t n_grad;       /* adjoint overlap slots in the pass                                     */
   uint64_t tile_mask;   /* physical qubits of the tile                                           */
   uint64_t nondiag_mask;/* qubits on which the pass' ops act non-diagonally (subset of tile_mask) */
+  int32_t n_dense;      /* stages executed as dense FP64-MMA stages                              */
+  int32_t mat_doubles;  /* matrix data of the pass (doubles)                                     */
 } sv_pass_info;
 
 /* Plans `gates` for an n-qubit single-GPU state exactly as sv_apply_circuit (adjoint = 0) or the

@@ -19,7 +19,7 @@ KIND = {"X": 0, "Y": 1, "XLIKE": 2, "Z": 3, "S": 4, "SDG": 5, "T": 6, "TDG": 7, 
 STATUS = {0: "SV_OK", 1: "SV_E_ARG", 2: "SV_E_QUBIT_RANGE", 3: "SV_E_TARGET_CONTROL_OVERLAP",
           4: "SV_E_DUPLICATE_TARGET", 5: "SV_E_PARAM_RANGE", 6: "SV_E_NOT_DIFFERENTIABLE", 7: "SV_E_NOT_UNITARY",
           8: "SV_E_OOM", 9: "SV_E_CUDA", 10: "SV_E_NCCL", 11: "SV_E_POISONED"}
-SV_OPT_TILE_QUBITS, SV_OPT_FUSION, SV_OPT_LOW_QUBITS = 1, 2, 3
+SV_OPT_TILE_QUBITS, SV_OPT_FUSION, SV_OPT_LOW_QUBITS, SV_OPT_DENSE, SV_OPT_KERNEL = 1, 2, 3, 4, 5
 
 
 class SvError(RuntimeError):
@@ -49,7 +49,7 @@ class sv_stats(ctypes.Structure):
 class sv_pass_info(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("low", ctypes.c_int32), ("R", ctypes.c_int32), ("n_ops", ctypes.c_int32),
                 ("n_stages", ctypes.c_int32), ("n_grad", ctypes.c_int32), ("tile_mask", ctypes.c_uint64),
-                ("nondiag_mask", ctypes.c_uint64)]
+                ("nondiag_mask", ctypes.c_uint64), ("n_dense", ctypes.c_int32), ("mat_doubles", ctypes.c_int32)]
 
 
 def _load():

@@ -73,15 +73,17 @@ int upload_plan(sv_state_s* h, const Plan& plan) {
   // one buffer: [ops | stages | mats], each section 64-byte aligned; one H2D copy
   auto al = [](size_t x) { return (x + 63) & ~size_t(63); };
   const size_t ob = plan.ops.size() * sizeof(DevOp), sb = plan.stages.size() * sizeof(StageDesc),
-               mb = plan.mats.size() * sizeof(double);
-  const size_t so = al(ob), mo = so + al(sb), total = mo + al(mb);
+               mb = plan.mats.size() * sizeof(double), rb = plan.rops.size() * sizeof(RegOp);
+  const size_t so = al(ob), mo = so + al(sb), ro = mo + al(mb), total = ro + al(rb);
   if (!h->d_ops.ensure(total + 64)) return fail(SV_E_OOM, "plan buffers");
   h->h_stage.assign(total, 0);
   std::memcpy(h->h_stage.data(), plan.ops.data(), ob);
   std::memcpy(h->h_stage.data() + so, plan.stages.data(), sb);
   std::memcpy(h->h_stage.data() + mo, plan.mats.data(), mb);
+  std::memcpy(h->h_stage.data() + ro, plan.rops.data(), rb);
   h->plan_stages_off = so;
   h->plan_mats_off = mo;
+  h->plan_rops_off = ro;
   cudaError_t e = cudaSuccess;
   if (total) e = cudaMemcpyAsync(h->d_ops.p, h->h_stage.data(), total, cudaMemcpyHostToDevice, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "plan upload");
@@ -98,9 +100,10 @@ int run_plan(sv_state_s* h, const Plan& plan, double* psi, double* lam, double* 
     L.d_ops = static_cast<const DevOp*>(h->d_ops.p);
     L.d_stages = reinterpret_cast<const StageDesc*>(static_cast<const char*>(h->d_ops.p) + h->plan_stages_off);
     L.d_mats = reinterpret_cast<const double*>(static_cast<const char*>(h->d_ops.p) + h->plan_mats_off);
+    L.d_rops = reinterpret_cast<const RegOp*>(static_cast<const char*>(h->d_ops.p) + h->plan_rops_off);
     L.d_partials = d_partials;
     L.nmats = next_mat - pd.mat_begin;
-    L.grid = grid > 0 ? grid : pass_grid(h->n_local, pd.k, lam != nullptr);
+    L.grid = grid > 0 ? grid : plan_grid(plan, h->n_local);
     L.n_local = h->n_local;
     L.rank_bits = 0;
     cudaError_t e = launch_pass(psi, lam, L, h->stream);
@@ -255,6 +258,8 @@ sv_status sv_set_option(sv_handle h, int32_t key, int64_t value) {
       if (value < 0 || value > 8) return fail(SV_E_ARG, "low qubits out of range");
       h->opts.low_qubits = (int)value;
       return SV_OK;
+    case SV_OPT_DENSE: h->opts.dense = value != 0 ? 1 : 0; return SV_OK;
+    case SV_OPT_KERNEL: h->opts.kernel = value != 0 ? 1 : 0; return SV_OK;
     default: return fail(SV_E_ARG, "unknown option");
   }
 }
@@ -393,8 +398,7 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   // 2. lambda = H psi, E partials
   const int pgrid = pauli_grid(h->n_local);
   const size_t ng = G.xs.size();
-  int rk = rev.passes.empty() ? 1 : rev.passes[0].k;
-  const int agrid = pass_grid(h->n_local, rk, true);
+  const int agrid = plan_grid(rev, h->n_local);
   const size_t ns = (size_t)rev.n_grad_slots;
   const size_t part_doubles = ng * pgrid + ns * agrid;
   if (!h->d_partials.ensure(part_doubles * 8 + 8) || !h->d_out.ensure((ng + ns) * 8 + 8)) return fail(SV_E_OOM, "partials");
@@ -476,6 +480,9 @@ extern "C" sv_status sv_plan_info(int32_t n_qubits, const sv_gate* gates, int64_
     r.n_grad = pd.n_grad;
     r.tile_mask = 0;
     for (int p = 0; p < pd.k; ++p) r.tile_mask |= 1ull << pd.tq[p];
+    r.n_dense = 0;
+    for (int si = pd.stage_begin; si < pd.stage_end; ++si) r.n_dense += plan.stages[si].dense;
+    r.mat_doubles = (int32_t)(((i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size()) - pd.mat_begin);
     r.nondiag_mask = 0;
     for (int j = pd.op_begin; j < pd.op_end; ++j) {
       const DevOp& op = plan.ops[j];

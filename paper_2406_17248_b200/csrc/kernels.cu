@@ -370,6 +370,19 @@ int pass_grid(int n_local, int k, bool dual) {
   return (int)(ntiles < want ? ntiles : want);
 }
 
+// One grid for every pass of a plan (the adjoint partials are laid out [slot][grid]): register
+// passes run one persistent, double-buffered CTA per SM; shared-memory passes two or more.
+int plan_grid(const Plan& plan, int n_local) {
+  if (plan.passes.empty()) return 1;
+  const PassDesc& pd = plan.passes[0];
+  if (pd.R > 0) {
+    const int64_t ntiles = 1ll << (n_local - pd.k);
+    const int64_t want = num_sms();
+    return (int)(ntiles < want ? ntiles : want);
+  }
+  return pass_grid(n_local, pd.k, false);
+}
+
 cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStream_t s) {
   const PassDesc& pd = *L.pd;
   if (pd.R > 0) return launch_pass_reg(psi, lam, L, s);

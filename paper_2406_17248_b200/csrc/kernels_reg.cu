@@ -13,6 +13,12 @@
 // (adjoint) variant the same happens for psi and lambda together, and before un-applying a
 // parametrised op each warp reduces its share of Re<lambda|D|psi> (shuffles) into a per-CTA,
 // per-op accumulator: deterministic fixed-order partials, no floating-point atomics.
+//
+// Instruction economy (the pass is FP64-pipe bound once ~10 gates are fused): ops are 32-byte
+// RegOps read with two 16-byte shared loads; the pair/quad loops are fully unrolled over
+// compile-time register indices with a control-free fast path, so the FP64 pipe sees long runs of
+// independent DFMAs; Z-like ops with a = 1 touch only half the amplitudes and CZ-type ops
+// (a = 1, b = -1) are sign flips without FP64 work.
 #include <cstdint>
 
 #include "cx.cuh"
@@ -27,23 +33,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
-
-struct RegArgs {
-  int32_t k, low, nops, nstages, n_outer, nmats, ngrad, grid;
-  int8_t tq[kMaxTileQubits + 3];
-  int8_t oq[64];
-  int64_t ntiles;
-  const DevOp* ops;
-  const double* mats;
-  const StageDesc* stages;
-  double* partials;
-};
-
-// ---------------------------------------------------------------- register-resident op kernels
 
 // Shared-memory load the compiler may not hoist or CSE (keeps 4x4 matrices out of registers).
 __device__ __forceinline__ double2 lds(const double2* p) {
@@ -53,13 +42,64 @@ __device__ __forceinline__ double2 lds(const double2* p) {
   return r;
 }
 
-template <int NR, int RB>
+__device__ __forceinline__ double2 cneg(double2 a) { return make_double2(-a.x, -a.y); }
+
+struct RegArgs {
+  int32_t k, low, nops, nstages, n_outer, nmats, ngrad, grid;
+  int8_t tq[kMaxTileQubits + 3];
+  int8_t oq[64];
+  int64_t ntiles;
+  const RegOp* ops;
+  const double* mats;
+  const StageDesc* stages;
+  double* partials;
+};
+
+// An op held as its raw words; fields are extracted where used (keeps register pressure low).
+struct Op {
+  uint32_t code, w1, w2, w3;
+  uint64_t couter;
+  __device__ __forceinline__ uint32_t type() const { return code & 15u; }
+  __device__ __forceinline__ uint32_t ra() const { return (code >> 4) & 15u; }
+  __device__ __forceinline__ uint32_t rb() const { return (code >> 8) & 15u; }
+  __device__ __forceinline__ uint32_t cj() const { return (code >> 12) & 15u; }
+  __device__ __forceinline__ uint32_t pa() const { return (code >> 16) & 31u; }
+  __device__ __forceinline__ uint32_t pb() const { return (code >> 21) & 31u; }
+  __device__ __forceinline__ uint32_t gen() const { return (code >> 26) & 3u; }
+  __device__ __forceinline__ uint32_t gdiag() const { return (code >> 28) & 1u; }
+  __device__ __forceinline__ uint32_t dfl() const { return code >> 29; }
+  __device__ __forceinline__ uint32_t mat_off() const { return w1 & 0xffffu; }
+  __device__ __forceinline__ uint32_t gen_off() const { return w1 >> 16; }
+  __device__ __forceinline__ uint32_t cthr() const { return w2 & 0xffffu; }
+  __device__ __forceinline__ int32_t grad_local() const { return (int32_t)(int16_t)(w2 >> 16); }
+  __device__ __forceinline__ uint32_t qa() const { return w3 & 0xffu; }
+  __device__ __forceinline__ uint32_t qb() const { return (w3 >> 8) & 0xffu; }
+};
+
+__device__ __forceinline__ Op load_op(const RegOp* p) {
+  const uint4 a = *reinterpret_cast<const uint4*>(p);
+  const uint2 b = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint4*>(p) + 1);
+  Op o;
+  o.code = a.x;
+  o.w1 = a.y;
+  o.w2 = a.z;
+  o.w3 = a.w;
+  o.couter = (uint64_t)b.x | ((uint64_t)b.y << 32);
+  return o;
+}
+
+// ---------------------------------------------------------------- register-resident op kernels
+
+#define SV_CTRL_SKIP(j) \
+  if (CTRL && (((j) & cj) != cj)) continue;
+
+template <int NR, int RB, bool CTRL>
 __device__ __forceinline__ void reg_m1(double2 (&v)[1 << NR], const double2* m, uint32_t cj) {
   const double2 m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
 #pragma unroll
   for (int j = 0; j < (1 << NR); ++j) {
     if (j & (1 << RB)) continue;
-    if ((j & cj) != cj) continue;
+    SV_CTRL_SKIP(j)
     const int j1 = j | (1 << RB);
     const double2 a = v[j], b = v[j1];
     v[j] = cfma(m00, a, cmul(m01, b));
@@ -67,13 +107,13 @@ __device__ __forceinline__ void reg_m1(double2 (&v)[1 << NR], const double2* m, 
   }
 }
 
-template <int NR, int RB>
+template <int NR, int RB, bool CTRL>
 __device__ __forceinline__ void reg_ax1(double2 (&v)[1 << NR], const double2* m, uint32_t cj) {
   const double2 a = m[0], b = m[1];  // X-like [[0,a],[b,0]]: new0 = a old1, new1 = b old0
 #pragma unroll
   for (int j = 0; j < (1 << NR); ++j) {
     if (j & (1 << RB)) continue;
-    if ((j & cj) != cj) continue;
+    SV_CTRL_SKIP(j)
     const int j1 = j | (1 << RB);
     const double2 x0 = v[j], x1 = v[j1];
     v[j] = cmul(a, x1);
@@ -81,12 +121,61 @@ __device__ __forceinline__ void reg_ax1(double2 (&v)[1 << NR], const double2* m,
   }
 }
 
-template <int NR, int RA, int RB>
+// Z-like diag(f0, f1) on register bit RB. dfl bit0: f0 == 1; bit1: f0 == 1 and f1 == -1.
+template <int NR, int RB, bool CTRL>
+__device__ __forceinline__ void reg_d1(double2 (&v)[1 << NR], const double2* m, uint32_t cj, uint32_t dfl) {
+  if (dfl & 2u) {
+#pragma unroll
+    for (int j = 0; j < (1 << NR); ++j) {
+      if (!(j & (1 << RB))) continue;
+      SV_CTRL_SKIP(j)
+      v[j] = cneg(v[j]);
+    }
+  } else if (dfl & 1u) {
+    const double2 f1 = m[1];
+#pragma unroll
+    for (int j = 0; j < (1 << NR); ++j) {
+      if (!(j & (1 << RB))) continue;
+      SV_CTRL_SKIP(j)
+      v[j] = cmul(f1, v[j]);
+    }
+  } else {
+    const double2 f0 = m[0], f1 = m[1];
+#pragma unroll
+    for (int j = 0; j < (1 << NR); ++j) {
+      SV_CTRL_SKIP(j)
+      v[j] = cmul((j & (1 << RB)) ? f1 : f0, v[j]);
+    }
+  }
+}
+
+// Z-like op whose target is a thread or outer bit tb (uniform over the thread's amplitudes).
+template <int NR, bool CTRL>
+__device__ __forceinline__ void reg_d1_uniform(double2 (&v)[1 << NR], const double2* m, uint32_t cj, uint32_t dfl,
+                                               uint32_t tb) {
+  if ((dfl & 1u) && !tb) return;
+  if (dfl & 2u) {
+#pragma unroll
+    for (int j = 0; j < (1 << NR); ++j) {
+      SV_CTRL_SKIP(j)
+      v[j] = cneg(v[j]);
+    }
+    return;
+  }
+  const double2 f = tb ? m[1] : m[0];
+#pragma unroll
+  for (int j = 0; j < (1 << NR); ++j) {
+    SV_CTRL_SKIP(j)
+    v[j] = cmul(f, v[j]);
+  }
+}
+
+template <int NR, int RA, int RB, bool CTRL>
 __device__ __forceinline__ void reg_m2(double2 (&v)[1 << NR], const double2* m, uint32_t cj) {
 #pragma unroll
   for (int j = 0; j < (1 << NR); ++j) {
     if (j & ((1 << RA) | (1 << RB))) continue;
-    if ((j & cj) != cj) continue;
+    SV_CTRL_SKIP(j)
     const int idx[4] = {j, j | (1 << RA), j | (1 << RB), j | (1 << RA) | (1 << RB)};
     double2 x[4];
 #pragma unroll
@@ -101,12 +190,12 @@ __device__ __forceinline__ void reg_m2(double2 (&v)[1 << NR], const double2* m, 
   }
 }
 
-template <int NR, int RA, int RB>
+template <int NR, int RA, int RB, bool CTRL>
 __device__ __forceinline__ void reg_swap(double2 (&v)[1 << NR], uint32_t cj) {
 #pragma unroll
   for (int j = 0; j < (1 << NR); ++j) {
     if (j & ((1 << RA) | (1 << RB))) continue;
-    if ((j & cj) != cj) continue;
+    SV_CTRL_SKIP(j)
     const int a = j | (1 << RA), b = j | (1 << RB);
     const double2 t = v[a];
     v[a] = v[b];
@@ -115,30 +204,30 @@ __device__ __forceinline__ void reg_swap(double2 (&v)[1 << NR], uint32_t cj) {
 }
 
 // Re <w| (Pi_C (x) G) |v> over this thread's amplitudes, G on register bit RB (2x2).
-template <int NR, int RB>
+template <int NR, int RB, bool CTRL>
 __device__ __forceinline__ double reg_ov1(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR], const double2* g,
                                           uint32_t cj) {
   const double2 g00 = g[0], g01 = g[1], g10 = g[2], g11 = g[3];
-  double acc = 0.0;
+  double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
   for (int j = 0; j < (1 << NR); ++j) {
     if (j & (1 << RB)) continue;
-    if ((j & cj) != cj) continue;
+    SV_CTRL_SKIP(j)
     const int j1 = j | (1 << RB);
-    acc += re_conj_mul(w[j], cfma(g00, v[j], cmul(g01, v[j1])));
-    acc += re_conj_mul(w[j1], cfma(g10, v[j], cmul(g11, v[j1])));
+    acc0 += re_conj_mul(w[j], cfma(g00, v[j], cmul(g01, v[j1])));
+    acc1 += re_conj_mul(w[j1], cfma(g10, v[j], cmul(g11, v[j1])));
   }
-  return acc;
+  return acc0 + acc1;
 }
 
-template <int NR, int RA, int RB>
+template <int NR, int RA, int RB, bool CTRL>
 __device__ __forceinline__ double reg_ov2(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR], const double2* g,
                                           uint32_t cj) {
   double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < (1 << NR); ++j) {
     if (j & ((1 << RA) | (1 << RB))) continue;
-    if ((j & cj) != cj) continue;
+    SV_CTRL_SKIP(j)
     const int idx[4] = {j, j | (1 << RA), j | (1 << RB), j | (1 << RA) | (1 << RB)};
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -151,117 +240,73 @@ __device__ __forceinline__ double reg_ov2(const double2 (&v)[1 << NR], const dou
   return acc;
 }
 
-// Dispatch helpers: runtime register index -> compile-time template.
-template <int NR>
-__device__ __forceinline__ void disp_m1(double2 (&v)[1 << NR], int r, const double2* m, uint32_t cj) {
-  switch (r) {
-    case 0: reg_m1<NR, 0>(v, m, cj); break;
-    case 1: reg_m1<NR, 1>(v, m, cj); break;
-    case 2: reg_m1<NR, 2>(v, m, cj); break;
-    default: if constexpr (NR > 3) reg_m1<NR, 3>(v, m, cj); break;
+// ---- runtime register index -> compile-time template dispatch ----
+#define SV_DISP1(NR, r, CALL)                          \
+  switch (r) {                                         \
+    case 0: CALL(0); break;                            \
+    case 1: CALL(1); break;                            \
+    case 2: CALL(2); break;                            \
+    default: if constexpr (NR > 3) { CALL(3); } break; \
   }
-}
-template <int NR>
-__device__ __forceinline__ void disp_ax1(double2 (&v)[1 << NR], int r, const double2* m, uint32_t cj) {
-  switch (r) {
-    case 0: reg_ax1<NR, 0>(v, m, cj); break;
-    case 1: reg_ax1<NR, 1>(v, m, cj); break;
-    case 2: reg_ax1<NR, 2>(v, m, cj); break;
-    default: if constexpr (NR > 3) reg_ax1<NR, 3>(v, m, cj); break;
+#define SV_DISP2(NR, ra, rb, CALL)                       \
+  switch ((ra) * 4 + (rb)) {                             \
+    case 1: CALL(0, 1); break;                           \
+    case 2: CALL(0, 2); break;                           \
+    case 6: CALL(1, 2); break;                           \
+    case 3: if constexpr (NR > 3) { CALL(0, 3); } break; \
+    case 7: if constexpr (NR > 3) { CALL(1, 3); } break; \
+    default: if constexpr (NR > 3) { CALL(2, 3); } break; \
   }
-}
-template <int NR>
-__device__ __forceinline__ void disp_m2(double2 (&v)[1 << NR], int ra, int rb, const double2* m, uint32_t cj) {
-  const int key = ra * 4 + rb;  // ra < rb
-  switch (key) {
-    case 1: reg_m2<NR, 0, 1>(v, m, cj); break;
-    case 2: reg_m2<NR, 0, 2>(v, m, cj); break;
-    case 6: reg_m2<NR, 1, 2>(v, m, cj); break;
-    default:
-      if constexpr (NR > 3) {
-        if (key == 3) reg_m2<NR, 0, 3>(v, m, cj);
-        else if (key == 7) reg_m2<NR, 1, 3>(v, m, cj);
-        else reg_m2<NR, 2, 3>(v, m, cj);
-      }
-      break;
-  }
-}
-template <int NR>
-__device__ __forceinline__ void disp_swap(double2 (&v)[1 << NR], int ra, int rb, uint32_t cj) {
-  const int key = ra * 4 + rb;
-  switch (key) {
-    case 1: reg_swap<NR, 0, 1>(v, cj); break;
-    case 2: reg_swap<NR, 0, 2>(v, cj); break;
-    case 6: reg_swap<NR, 1, 2>(v, cj); break;
-    default:
-      if constexpr (NR > 3) {
-        if (key == 3) reg_swap<NR, 0, 3>(v, cj);
-        else if (key == 7) reg_swap<NR, 1, 3>(v, cj);
-        else reg_swap<NR, 2, 3>(v, cj);
-      }
-      break;
-  }
-}
-template <int NR>
-__device__ __forceinline__ double disp_ov1(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR], int r,
-                                           const double2* g, uint32_t cj) {
-  switch (r) {
-    case 0: return reg_ov1<NR, 0>(v, w, g, cj);
-    case 1: return reg_ov1<NR, 1>(v, w, g, cj);
-    case 2: return reg_ov1<NR, 2>(v, w, g, cj);
-    default: if constexpr (NR > 3) return reg_ov1<NR, 3>(v, w, g, cj); return 0.0;
-  }
-}
-template <int NR>
-__device__ __forceinline__ double disp_ov2(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR], int ra, int rb,
-                                           const double2* g, uint32_t cj) {
-  const int key = ra * 4 + rb;
-  switch (key) {
-    case 1: return reg_ov2<NR, 0, 1>(v, w, g, cj);
-    case 2: return reg_ov2<NR, 0, 2>(v, w, g, cj);
-    case 6: return reg_ov2<NR, 1, 2>(v, w, g, cj);
-    default:
-      if constexpr (NR > 3) {
-        if (key == 3) return reg_ov2<NR, 0, 3>(v, w, g, cj);
-        if (key == 7) return reg_ov2<NR, 1, 3>(v, w, g, cj);
-        return reg_ov2<NR, 2, 3>(v, w, g, cj);
-      }
-      return 0.0;
-  }
-}
 
-// Bit of a target for register index j: register bit (ra >= 0), else thread / outer bit (tb).
-__device__ __forceinline__ uint32_t tbit(int ra, int j, uint32_t tb) { return ra >= 0 ? ((uint32_t)j >> ra) & 1u : tb; }
-
-template <int NR>
-__device__ __forceinline__ void reg_apply(double2 (&v)[1 << NR], const DevOp& o, const double2* m, uint32_t tthr,
-                                          uint64_t base) {
-  const uint32_t cj = o.cj;
-  switch (o.type) {
-    case OP_M1: disp_m1<NR>(v, o.ra, m, cj); break;
-    case OP_AX1: disp_ax1<NR>(v, o.ra, m, cj); break;
-    case OP_M2: disp_m2<NR>(v, o.ra, o.rb, m, cj); break;
-    case OP_SWAP: disp_swap<NR>(v, o.ra, o.rb, cj); break;
+template <int NR, bool CTRL>
+__device__ __forceinline__ void reg_apply_c(double2 (&v)[1 << NR], const Op& o, const double2* m, uint32_t tthr,
+                                            uint64_t base) {
+  const uint32_t cj = o.cj();
+  switch (o.type()) {
+    case OP_M1: {
+#define C1(R) reg_m1<NR, R, CTRL>(v, m, cj)
+      SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      break;
+    }
+    case OP_AX1: {
+#define C1(R) reg_ax1<NR, R, CTRL>(v, m, cj)
+      SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      break;
+    }
+    case OP_M2: {
+#define C2(A, B) reg_m2<NR, A, B, CTRL>(v, m, cj)
+      SV_DISP2(NR, o.ra(), o.rb(), C2)
+#undef C2
+      break;
+    }
+    case OP_SWAP: {
+#define C2(A, B) reg_swap<NR, A, B, CTRL>(v, cj)
+      SV_DISP2(NR, o.ra(), o.rb(), C2)
+#undef C2
+      break;
+    }
     case OP_D1: {
-      const double2 f0 = m[0], f1 = m[1];
-      const uint32_t tb = o.pa >= 0 ? (tthr >> o.pa) & 1u : (uint32_t)((base >> o.qa) & 1ull);
-#pragma unroll
-      for (int j = 0; j < (1 << NR); ++j) {
-        if ((j & cj) != cj) continue;
-        v[j] = cmul(tbit(o.ra, j, tb) ? f1 : f0, v[j]);
+      if (o.ra() != 15u) {
+#define C1(R) reg_d1<NR, R, CTRL>(v, m, cj, o.dfl())
+        SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      } else {
+        const uint32_t tb = o.pa() != 31u ? (tthr >> o.pa()) & 1u : (uint32_t)((base >> o.qa()) & 1ull);
+        reg_d1_uniform<NR, CTRL>(v, m, cj, o.dfl(), tb);
       }
       break;
     }
     case OP_D2: {
-      const double2 f0 = m[0], f1 = m[1], f2 = m[2], f3 = m[3];
-      const uint32_t ta = o.pa >= 0 ? (tthr >> o.pa) & 1u : (uint32_t)((base >> o.qa) & 1ull);
-      const uint32_t tb = o.pb >= 0 ? (tthr >> o.pb) & 1u : (uint32_t)((base >> o.qb) & 1ull);
+      const uint32_t ta = o.pa() != 31u ? (tthr >> o.pa()) & 1u : (uint32_t)((base >> o.qa()) & 1ull);
+      const uint32_t tb = o.pb() != 31u ? (tthr >> o.pb()) & 1u : (uint32_t)((base >> o.qb()) & 1ull);
 #pragma unroll
       for (int j = 0; j < (1 << NR); ++j) {
-        if ((j & cj) != cj) continue;
-        const uint32_t b0 = tbit(o.ra, j, ta), b1 = tbit(o.rb, j, tb);
-        const double2 f = b1 ? (b0 ? f3 : f2) : (b0 ? f1 : f0);
-        v[j] = cmul(f, v[j]);
+        SV_CTRL_SKIP(j)
+        const uint32_t b0 = o.ra() != 15u ? ((uint32_t)j >> o.ra()) & 1u : ta;
+        const uint32_t b1 = o.rb() != 15u ? ((uint32_t)j >> o.rb()) & 1u : tb;
+        v[j] = cmul(lds(m + (b0 | (b1 << 1))), v[j]);
       }
       break;
     }
@@ -269,36 +314,139 @@ __device__ __forceinline__ void reg_apply(double2 (&v)[1 << NR], const DevOp& o,
 }
 
 template <int NR>
-__device__ __forceinline__ double reg_overlap(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR], const DevOp& o,
-                                              const double2* g, uint32_t tthr, uint64_t base) {
-  const uint32_t cj = o.cj;
-  if (o.gen_diag) {
-    const uint32_t ta = o.pa >= 0 ? (tthr >> o.pa) & 1u : (uint32_t)((base >> o.qa) & 1ull);
-    const uint32_t tb = (o.gen_dim == 4) ? (o.pb >= 0 ? (tthr >> o.pb) & 1u : (uint32_t)((base >> o.qb) & 1ull)) : 0u;
+__device__ __forceinline__ void reg_apply(double2 (&v)[1 << NR], const Op& o, const double2* m, uint32_t tthr,
+                                          uint64_t base) {
+  if (o.cj()) reg_apply_c<NR, true>(v, o, m, tthr, base);
+  else reg_apply_c<NR, false>(v, o, m, tthr, base);
+}
+
+template <int NR, bool CTRL>
+__device__ __forceinline__ double reg_overlap_c(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR], const Op& o,
+                                                const double2* g, uint32_t tthr, uint64_t base) {
+  const uint32_t cj = o.cj();
+  if (o.gdiag()) {
+    const uint32_t ta = o.pa() != 31u ? (tthr >> o.pa()) & 1u : (uint32_t)((base >> o.qa()) & 1ull);
+    const uint32_t tb = o.pb() != 31u ? (tthr >> o.pb()) & 1u : (uint32_t)((base >> o.qb()) & 1ull);
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < (1 << NR); ++j) {
-      if ((j & cj) != cj) continue;
-      uint32_t idx = tbit(o.ra, j, ta);
-      if (o.gen_dim == 4) idx |= tbit(o.rb, j, tb) << 1;
+      SV_CTRL_SKIP(j)
+      uint32_t idx = o.ra() != 15u ? ((uint32_t)j >> o.ra()) & 1u : ta;
+      if (o.gen() == 2u) idx |= (o.rb() != 15u ? ((uint32_t)j >> o.rb()) & 1u : tb) << 1;
       acc += re_conj_mul(w[j], cmul(g[idx], v[j]));
     }
     return acc;
   }
-  if (o.gen_dim == 2) return disp_ov1<NR>(v, w, o.ra, g, cj);
-  return disp_ov2<NR>(v, w, o.ra, o.rb, g, cj);
+  double r = 0.0;
+  if (o.gen() == 1u) {
+#define C1(R) r = reg_ov1<NR, R, CTRL>(v, w, g, cj)
+    SV_DISP1(NR, o.ra(), C1)
+#undef C1
+  } else {
+#define C2(A, B) r = reg_ov2<NR, A, B, CTRL>(v, w, g, cj)
+    SV_DISP2(NR, o.ra(), o.rb(), C2)
+#undef C2
+  }
+  return r;
+}
+
+
+// ---------------------------------------------------------------- dense FP64-MMA stage
+//
+// The stage's ops were folded on the host into a 16x16 complex matrix U per variant; with
+// X = [Re; Im] of the tile's 2^(k-4) vectors of 16 amplitudes, Y = [[Ur, -Ui], [Ui, Ur]] X is a
+// real 32 x 32 x 2^(k-4) GEMM, run as mma.sync m8n8k4 f64 (DMMA): per warp 4 N-tiles of 8 vectors,
+// 4 M-tiles x 8 K-tiles. Fragment layouts (PTX m8n8k4 .f64): A[r = lane/4][c = lane%4],
+// B[k = lane%4][n = lane/4], D[r = lane/4][c = 2 (lane%4) + {0,1}].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double lds64(const double* p) {
+  double r;
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(r) : "r"(a));
+  return r;
+}
+
+__device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, const double2* mats2, uint64_t base,
+                                            int warp, int lane, int nw_bits) {
+  uint32_t twarp = 0;
+  for (int b = 0; b < nw_bits; ++b)
+    if ((warp >> b) & 1) twarp |= 1u << S.thrpos[5 + b];
+  uint32_t var = (uint32_t)warp & ((1u << S.m_tile) - 1u);
+  for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
+  const double* U = reinterpret_cast<const double*>(mats2 + S.op_begin + var * 256u);
+  const uint32_t p0 = 1u << S.regpos[0], p1 = 1u << S.regpos[1], p2 = 1u << S.regpos[2], p3 = 1u << S.regpos[3];
+  const uint32_t c0 = 1u << S.thrpos[0], c1 = 1u << S.thrpos[1], c2 = 1u << S.thrpos[2];
+  const uint32_t n0 = 1u << S.thrpos[3], n1 = 1u << S.thrpos[4];
+  // ---- B fragments: amps j = 4 kq + lane%4 of column lane/4 ----
+  const uint32_t lb = (uint32_t)lane;
+  const uint32_t tcolB = ((lb >> 2) & 1u ? c0 : 0u) | ((lb >> 3) & 1u ? c1 : 0u) | ((lb >> 4) & 1u ? c2 : 0u);
+  const uint32_t tjlo = ((lb & 1u) ? p0 : 0u) | ((lb & 2u) ? p1 : 0u);
+  double b[4][8];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const uint32_t tn = twarp | ((nt & 1) ? n0 : 0u) | ((nt & 2) ? n1 : 0u) | tcolB | tjlo;
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      const uint32_t t = tn | ((kq & 1) ? p2 : 0u) | ((kq & 2) ? p3 : 0u);
+      const double2 x = tp[swz(t)];
+      b[nt][kq] = x.x;
+      b[nt][kq + 4] = x.y;
+    }
+  }
+  // ---- D = A B ----
+  double d[4][4][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
+  const int arow = lane >> 2, acol = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+#pragma unroll
+    for (int kt = 0; kt < 8; ++kt) {
+      const int jo = 8 * (mt & 1) + arow, ji = 4 * (kt & 3) + acol;
+      // [[Ur, -Ui], [Ui, Ur]]: re-out rows mt < 2, im-in columns kt >= 4
+      const bool im_out = mt >= 2, im_in = kt >= 4;
+      const double* e = U + 2 * (jo * 16 + ji);
+      double a = lds64(e + ((im_out != im_in) ? 1 : 0));
+      if (!im_out && im_in) a = -a;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma(d[mt][nt][0], d[mt][nt][1], a, b[nt][kt]);
+    }
+  }
+  // ---- stores: amps j = 8 mh + lane/4 of columns 2 (lane%4) + v ----
+  const uint32_t tjs = ((lb >> 2) & 1u ? p0 : 0u) | ((lb >> 3) & 1u ? p1 : 0u) | ((lb >> 4) & 1u ? p2 : 0u);
+  const uint32_t tcs = ((lb & 1u) ? c1 : 0u) | ((lb & 2u) ? c2 : 0u);
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const uint32_t tn = twarp | ((nt & 1) ? n0 : 0u) | ((nt & 2) ? n1 : 0u) | tjs | tcs;
+#pragma unroll
+    for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const uint32_t t = tn | (mh ? p3 : 0u) | (v ? c0 : 0u);
+        tp[swz(t)] = make_double2(d[mh][nt][v], d[mh + 2][nt][v]);
+      }
+  }
 }
 
 // ---------------------------------------------------------------- the pass kernel
 
 template <int NR, bool DUAL>
-__global__ void __launch_bounds__(256, DUAL ? 1 : 2) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam, RegArgs a) {
+__global__ void __launch_bounds__(256, 1) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
+                                                                  RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
   const int nthr = blockDim.x, tid = threadIdx.x, nwarps = nthr >> 5, warp = tid >> 5, lane = tid & 31;
-  double2* tp = reinterpret_cast<double2*>(smem_raw);
-  double2* tl = DUAL ? tp + N : nullptr;
-  DevOp* s_ops = reinterpret_cast<DevOp*>(tp + (DUAL ? 2 * N : N));
+  const uint32_t NB = DUAL ? 2 * N : N;  // doubles2 per buffer (psi [+ lambda])
+  double2* smem_tiles = reinterpret_cast<double2*>(smem_raw);
+  double2* tp = smem_tiles;  // (setup-phase alias; the tile loop rebinds per buffer)
+  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + 2 * NB);
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
   double* s_mats = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
   const int nhi = 1 << (a.k - a.low);
@@ -306,9 +454,9 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : 2) k_pass_reg(double2* __restr
   double* s_acc = reinterpret_cast<double*>(s_hi + nhi);  // [ngrad][nwarps]
 
   {
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(a.ops);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(s_ops);
-    for (int i = tid; i < a.nops * 8; i += nthr) dst[i] = src[i];
+    const uint4* src = reinterpret_cast<const uint4*>(a.ops);
+    uint4* dst = reinterpret_cast<uint4*>(s_ops);
+    for (int i = tid; i < a.nops * 2; i += nthr) dst[i] = src[i];
     const uint64_t* ss = reinterpret_cast<const uint64_t*>(a.stages);
     uint64_t* sd = reinterpret_cast<uint64_t*>(s_st);
     for (int i = tid; i < a.nstages * (int)(sizeof(StageDesc) / 8); i += nthr) sd[i] = ss[i];
@@ -325,54 +473,98 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : 2) k_pass_reg(double2* __restr
   __syncthreads();
   const uint32_t lowmask = (1u << a.low) - 1u;
   const int nthr_bits = a.k - NR;
+  const double2* mats2 = reinterpret_cast<const double2*>(s_mats);
 
-  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+  // Double-buffered tiles: while the stages of tile i run from buffer (i & 1), cp.async streams
+  // tile i + gridDim.x into the other buffer, so HBM reads overlap the FP64 work.
+  auto tile_base = [&](int64_t tile) {
     uint64_t base = 0;
     for (int j = 0; j < a.n_outer; ++j)
       if ((tile >> j) & 1) base |= 1ull << a.oq[j];
-    // ---- load: HBM -> shared (cp.async, coalesced 16-byte) ----
+    return base;
+  };
+  auto issue_load = [&](int64_t tile, int buf) {
+    const uint64_t base = tile_base(tile);
+    double2* dp = tp + (size_t)buf * NB;
     for (uint32_t e = tid; e < N; e += nthr) {
       const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
-      cp_async16(tp + swz(e), psi + gi);
-      if (DUAL) cp_async16(tl + swz(e), lam + gi);
+      cp_async16(dp + swz(e), psi + gi);
+      if (DUAL) cp_async16(dp + N + swz(e), lam + gi);
     }
-    cp_async_wait_all();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if ((int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+    const int cur = it & 1;
+    const uint64_t base = tile_base(tile);
+    const int64_t next = tile + gridDim.x;
+    if (next < a.ntiles) {
+      issue_load(next, cur ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
+    double2* tp = smem_tiles + (size_t)cur * NB;
+    double2* tl = DUAL ? tp + N : nullptr;
     // ---- stages ----
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
+      if constexpr (!DUAL && NR == 4) {
+        if (S.dense) {
+          dense_stage(tp, S, mats2, base, warp, lane, a.k - 9);
+          __syncthreads();
+          continue;
+        }
+      }
       uint32_t tthr = 0;
       for (int b = 0; b < nthr_bits; ++b)
         if ((tid >> b) & 1) tthr |= 1u << S.thrpos[b];
       const uint32_t A = swz(tthr);
+      uint32_t SR[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) SR[r] = swz(1u << S.regpos[r]);
       double2 v[1 << NR];
       double2 w[DUAL ? (1 << NR) : 1];
 #pragma unroll
       for (int j = 0; j < (1 << NR); ++j) {
-        v[j] = tp[A ^ S.swz_reg[j]];
-        if constexpr (DUAL) w[j] = tl[A ^ S.swz_reg[j]];
+        uint32_t ad = A;
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          if ((j >> r) & 1) ad ^= SR[r];
+        v[j] = tp[ad];
+        if constexpr (DUAL) w[j] = tl[ad];
       }
       for (int i = S.op_begin; i < S.op_end; ++i) {
-        const DevOp& o = s_ops[i];
-        const bool ok = ((base & o.couter) == o.couter) && ((tthr & (uint32_t)o.cthr) == (uint32_t)o.cthr);
+        const Op o = load_op(s_ops + i);
+        const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
         if constexpr (DUAL) {
-          if (o.grad_slot >= 0) {
+          if (o.gen()) {
             double part = 0.0;
-            if (ok) part = reg_overlap<NR>(v, w, o, reinterpret_cast<const double2*>(s_mats + o.gen_off), tthr, base);
+            if (ok) {
+              const double2* g = mats2 + o.gen_off();
+              part = o.cj() ? reg_overlap_c<NR, true>(v, w, o, g, tthr, base)
+                          : reg_overlap_c<NR, false>(v, w, o, g, tthr, base);
+            }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-            if (lane == 0) s_acc[o.grad_local * nwarps + warp] += part;
+            if (lane == 0) s_acc[o.grad_local() * nwarps + warp] += part;
           }
         }
         if (!ok) continue;
-        const double2* m = reinterpret_cast<const double2*>(s_mats + o.mat_off);
+        const double2* m = mats2 + o.mat_off();
         reg_apply<NR>(v, o, m, tthr, base);
         if constexpr (DUAL) reg_apply<NR>(w, o, m, tthr, base);
       }
 #pragma unroll
       for (int j = 0; j < (1 << NR); ++j) {
-        tp[A ^ S.swz_reg[j]] = v[j];
-        if constexpr (DUAL) tl[A ^ S.swz_reg[j]] = w[j];
+        uint32_t ad = A;
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          if ((j >> r) & 1) ad ^= SR[r];
+        tp[ad] = v[j];
+        if constexpr (DUAL) tl[ad] = w[j];
       }
       __syncthreads();
     }
@@ -386,18 +578,18 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : 2) k_pass_reg(double2* __restr
   }
   if (DUAL) {
     for (int i = tid; i < a.nops; i += nthr) {
-      const DevOp& o = s_ops[i];
-      if (o.grad_slot < 0) continue;
+      const Op o = load_op(s_ops + i);
+      if (!o.gen()) continue;
       double s = 0.0;
-      for (int wi = 0; wi < nwarps; ++wi) s += s_acc[o.grad_local * nwarps + wi];
-      a.partials[(int64_t)o.grad_slot * a.grid + blockIdx.x] = s;
+      for (int wi = 0; wi < nwarps; ++wi) s += s_acc[o.grad_local() * nwarps + wi];
+      a.partials[(int64_t)s_ops[i].grad_slot * a.grid + blockIdx.x] = s;
     }
   }
 }
 
 size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual) {
-  size_t b = (size_t(16) << k) * (dual ? 2 : 1);
-  b += (size_t)nops * sizeof(DevOp) + (size_t)nstages * sizeof(StageDesc) + 16;
+  size_t b = (size_t(16) << k) * (dual ? 2 : 1) * 2;  // double-buffered
+  b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
   b += (size_t)nmats * 8 + (size_t(8) << (k - low));
   b += dual ? (size_t)ngrad * (nthr / 32) * 8 : 0;
   return b;
@@ -422,7 +614,7 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   for (int q = 0; q < L.n_local; ++q)
     if (!((tmask >> q) & 1ull)) a.oq[a.n_outer++] = (int8_t)q;
   a.ntiles = 1ll << (L.n_local - pd.k);
-  a.ops = L.d_ops + pd.op_begin;
+  a.ops = L.d_rops + pd.op_begin;
   a.mats = L.d_mats + pd.mat_begin;
   a.stages = L.d_stages + pd.stage_begin;
   a.partials = L.d_partials;

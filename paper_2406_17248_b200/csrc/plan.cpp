@@ -12,6 +12,8 @@
 // used here: the qubits on which either acts non-diagonally are disjoint from all qubits of the
 // other (operators block-diagonal on shared qubits commute). Controls act diagonally.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sv.h"
@@ -58,7 +60,7 @@ bool op_is_diag(const DevOp& o) { return o.type == OP_D1 || o.type == OP_D2; }
 // stage. An op joins the current stage if it may legally move ahead of the ops left for later
 // stages (same commutation rule as the pass planner) and its non-diagonal target positions fit
 // the stage's R register positions.
-void plan_stages(Plan* plan, PassDesc* pd, int R) {
+void plan_stages(Plan* plan, PassDesc* pd, int R, int max_var_tile = -1, int max_var_total = -1) {
   const int k = pd->k;
   std::vector<DevOp> ops(plan->ops.begin() + pd->op_begin, plan->ops.begin() + pd->op_end);
   auto phys_masks = [&](const DevOp& o, uint64_t* N, uint64_t* A) {
@@ -79,20 +81,45 @@ void plan_stages(Plan* plan, PassDesc* pd, int R) {
   pd->stage_begin = (int)plan->stages.size();
   int stage_idx = 0;
   while (!pending.empty()) {
-    uint32_t regset = 0;
-    uint64_t bN = 0, bA = 0;
+    uint32_t regset = 0, vt = 0;
+    uint64_t bN = 0, bA = 0, vo = 0;
     std::vector<int> taken, skipped;
     for (int i : pending) {
+      const DevOp& op = ops[i];
       uint64_t N, A;
-      phys_masks(ops[i], &N, &A);
+      phys_masks(op, &N, &A);
       bool ok = !(N & bA) && !(A & bN);
-      const uint32_t pm = pos_mask(ops[i]);
+      const uint32_t pm = pos_mask(op);
+      uint32_t nreg = regset;
       if (ok && (pm & ~regset)) {
-        if (__builtin_popcount(regset | pm) <= R) regset |= pm;
+        if (__builtin_popcount(regset | pm) <= R) nreg = regset | pm;
         else ok = false;
       }
-      if (ok) taken.push_back(i);
+      uint32_t nvt = vt;
+      uint64_t nvo = vo;
+      if (ok && max_var_total >= 0) {
+        // variant bits (dense stages): thread / outer bits read by controls or diagonal factors
+        nvt |= (uint32_t)op.ctile;
+        nvo |= op.couter;
+        if (op_is_diag(op)) {
+          for (int t = 0; t < (op.type == OP_D2 ? 2 : 1); ++t) {
+            const int pos = t ? op.pb : op.pa;
+            if (pos >= 0) nvt |= 1u << pos;
+            else nvo |= 1ull << (t ? op.qb : op.qa);
+          }
+        }
+        nvt &= ~nreg;
+        if (__builtin_popcount(nvt) > max_var_tile || __builtin_popcount(nvt) + __builtin_popcountll(nvo) > max_var_total)
+          ok = false;
+      }
+      if (ok) { taken.push_back(i); regset = nreg; vt = nvt; vo = nvo; }
       else { skipped.push_back(i); bN |= N; bA |= A; }
+    }
+    if (taken.empty()) {
+      // the variant limit admits nothing: take the first pending op (this stage stays sequential)
+      taken.push_back(skipped.front());
+      skipped.erase(skipped.begin());
+      regset = pos_mask(ops[taken[0]]);
     }
     // layout: lanes 0..2 on thread positions with distinct residues mod 3 (conflict-free 16-byte
     // shared-memory phases), then fill the register set, then the remaining thread positions.
@@ -181,6 +208,210 @@ void plan_stages(Plan* plan, PassDesc* pd, int R) {
   // local grad indices
   int gl = 0;
   for (int i = pd->op_begin; i < pd->op_end; ++i) plan->ops[i].grad_local = (int16_t)(plan->ops[i].grad_slot >= 0 ? gl++ : -1);
+}
+
+
+// ---------------------------------------------------------------- dense (FP64-MMA) stages
+
+// FP64 pipe cost per amplitude of an op applied sequentially (DFMA path), for the dense choice.
+int seq_cost(const DevOp& o, const double* m) {
+  switch (o.type) {
+    case OP_M1: return 8;
+    case OP_AX1: return 4;
+    case OP_M2: return 32;
+    case OP_SWAP: return 0;
+    case OP_D2: return 4;
+    case OP_D1:
+      if (m[0] == 1.0 && m[1] == 0.0) return (m[2] == -1.0 && m[3] == 0.0) ? 0 : 2;
+      return 4;
+  }
+  return 0;
+}
+
+// Applies one op to the 16-dim register-space vector u (complex), given the values of the
+// variant bits it reads (tile positions in `tbits`, outer qubits in `obits`). reg_new[p] is the
+// dense register index of tile position p (-1 if p is not a register position).
+void dense_apply(Cx* u, const DevOp& o, const double* m, const int* reg_new, uint32_t tbits, uint64_t obits) {
+  if ((o.cthr & tbits) != o.cthr) return;
+  if ((o.couter & obits) != o.couter) return;
+  uint32_t cj = 0;
+  for (int p = 0; p < 32; ++p)
+    if (((o.ctile >> p) & 1ull) && reg_new[p] >= 0) cj |= 1u << reg_new[p];
+  auto bit_of = [&](int pos, int q, int j) -> uint32_t {
+    if (pos >= 0 && reg_new[pos] >= 0) return ((uint32_t)j >> reg_new[pos]) & 1u;
+    if (pos >= 0) return (tbits >> pos) & 1u;
+    return (uint32_t)((obits >> q) & 1ull);
+  };
+  auto cm = [](Cx a, Cx b) { return Cx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; };
+  auto ca = [](Cx a, Cx b) { return Cx{a.re + b.re, a.im + b.im}; };
+  const Cx* M = reinterpret_cast<const Cx*>(m);
+  switch (o.type) {
+    case OP_M1: case OP_AX1: {
+      const int r = reg_new[o.pa];
+      Cx mm[4];
+      if (o.type == OP_M1) { mm[0] = M[0]; mm[1] = M[1]; mm[2] = M[2]; mm[3] = M[3]; }
+      else { mm[0] = Cx{0, 0}; mm[1] = M[0]; mm[2] = M[1]; mm[3] = Cx{0, 0}; }
+      for (int j = 0; j < 16; ++j) {
+        if ((j >> r) & 1) continue;
+        if (((uint32_t)j & cj) != cj) continue;
+        const int j1 = j | (1 << r);
+        const Cx a = u[j], b = u[j1];
+        u[j] = ca(cm(mm[0], a), cm(mm[1], b));
+        u[j1] = ca(cm(mm[2], a), cm(mm[3], b));
+      }
+      break;
+    }
+    case OP_M2: case OP_SWAP: {
+      const int ra = reg_new[o.pa], rb = reg_new[o.pb];
+      for (int j = 0; j < 16; ++j) {
+        if (((j >> ra) & 1) || ((j >> rb) & 1)) continue;
+        if (((uint32_t)j & cj) != cj) continue;
+        const int idx[4] = {j, j | (1 << ra), j | (1 << rb), j | (1 << ra) | (1 << rb)};
+        Cx x[4], y[4];
+        for (int c = 0; c < 4; ++c) x[c] = u[idx[c]];
+        if (o.type == OP_SWAP) { y[0] = x[0]; y[1] = x[2]; y[2] = x[1]; y[3] = x[3]; }
+        else
+          for (int rr = 0; rr < 4; ++rr) {
+            Cx acc{0, 0};
+            for (int c = 0; c < 4; ++c) acc = ca(acc, cm(M[rr * 4 + c], x[c]));
+            y[rr] = acc;
+          }
+        for (int c = 0; c < 4; ++c) u[idx[c]] = y[c];
+      }
+      break;
+    }
+    case OP_D1:
+      for (int j = 0; j < 16; ++j) {
+        if (((uint32_t)j & cj) != cj) continue;
+        u[j] = cm(M[bit_of(o.pa, o.qa, j)], u[j]);
+      }
+      break;
+    case OP_D2:
+      for (int j = 0; j < 16; ++j) {
+        if (((uint32_t)j & cj) != cj) continue;
+        u[j] = cm(M[bit_of(o.pa, o.qa, j) | (bit_of(o.pb, o.qb, j) << 1)], u[j]);
+      }
+      break;
+  }
+}
+
+// Turns the stages of a forward pass into dense MMA stages where that is cheaper and feasible.
+void densify_stages(Plan* plan, PassDesc* pd, size_t mat_budget_doubles) {
+  const int k = pd->k;
+  const int nw_bits = k - 9;  // warp bits (256 threads at k = 12)
+  if (nw_bits < 0) return;
+  for (int si = pd->stage_begin; si < pd->stage_end; ++si) {
+    StageDesc& S = plan->stages[si];
+    const int ob = pd->op_begin + S.op_begin, oe = pd->op_begin + S.op_end;
+    // cost and variant bits
+    int cost = 0;
+    uint32_t vt = 0;
+    uint64_t vo = 0;
+    uint32_t regmask = 0;
+    for (int r = 0; r < 4; ++r) regmask |= 1u << S.regpos[r];
+    for (int i = ob; i < oe; ++i) {
+      const DevOp& o = plan->ops[i];
+      const double* m = plan->mats.data() + pd->mat_begin + o.mat_off;
+      cost += seq_cost(o, m);
+      vt |= (uint32_t)o.cthr;
+      vo |= o.couter;
+      if (o.type == OP_D1 || o.type == OP_D2) {
+        for (int t = 0; t < (o.type == OP_D2 ? 2 : 1); ++t) {
+          const int pos = t ? o.pb : o.pa;
+          const int q = t ? o.qb : o.qa;
+          if (pos >= 0 && !((regmask >> pos) & 1u)) vt |= 1u << pos;
+          if (pos < 0) vo |= 1ull << q;
+        }
+      }
+    }
+    const int m_tile = __builtin_popcount(vt), m_outer = __builtin_popcountll(vo);
+    if (std::getenv("SV_PLAN_DEBUG"))
+      std::fprintf(stderr, "stage %d: ops %d cost %d m_tile %d m_outer %d\n", si, oe - ob, cost, m_tile, m_outer);
+    if (cost < 20 || m_tile > nw_bits || m_outer > 3 || m_tile + m_outer > 3) continue;
+    const int nvar = 1 << (m_tile + m_outer);
+    const size_t need = (size_t)nvar * 512;
+    const size_t used = plan->mats.size() - pd->mat_begin;
+    if (used + need > mat_budget_doubles) continue;
+    // layout: register order R0..R3 and MMA column bits c0..c2 with conflict-free shared phases
+    std::vector<int> regs = {S.regpos[0], S.regpos[1], S.regpos[2], S.regpos[3]};
+    std::vector<int> free_pos;
+    for (int p = 0; p < k; ++p)
+      if (!((regmask >> p) & 1u) && !((vt >> p) & 1u)) free_pos.push_back(p);
+    int best[5] = {-1, -1, -1, -1, -1};
+    int best_score = -1;
+    auto distinct3 = [](int a, int b, int c) { return (a % 3) != (b % 3) && (a % 3) != (c % 3) && (b % 3) != (c % 3); };
+    for (int r0 = 0; r0 < 4 && best_score < 2; ++r0)
+      for (int r1 = 0; r1 < 4 && best_score < 2; ++r1) {
+        if (r1 == r0) continue;
+        for (size_t a = 0; a < free_pos.size() && best_score < 2; ++a)
+          for (size_t b = 0; b < free_pos.size() && best_score < 2; ++b)
+            for (size_t c = 0; c < free_pos.size() && best_score < 2; ++c) {
+              if (a == b || a == c || b == c) continue;
+              const int sc = (distinct3(regs[r0], regs[r1], free_pos[a]) ? 1 : 0) +
+                             (distinct3(regs[r0], free_pos[b], free_pos[c]) ? 1 : 0);
+              if (sc > best_score) {
+                best_score = sc;
+                best[0] = r0; best[1] = r1; best[2] = (int)a; best[3] = (int)b; best[4] = (int)c;
+              }
+            }
+      }
+    if (best_score < 0 || free_pos.size() < 3) continue;
+    std::vector<int> newreg = {regs[best[0]], regs[best[1]]};
+    for (int r = 0; r < 4; ++r)
+      if (r != best[0] && r != best[1]) newreg.push_back(regs[r]);
+    const int c0 = free_pos[best[2]], c1 = free_pos[best[3]], c2 = free_pos[best[4]];
+    std::vector<int> rest;
+    for (int p = 0; p < k; ++p)
+      if (!((regmask >> p) & 1u) && !((vt >> p) & 1u) && p != c0 && p != c1 && p != c2) rest.push_back(p);
+    // thrpos: c0 c1 c2 | n0 n1 | w (variant positions first)
+    std::vector<int> vlist;
+    for (int p = 0; p < k; ++p)
+      if ((vt >> p) & 1u) vlist.push_back(p);
+    std::vector<int> order = {c0, c1, c2};
+    // n0, n1 from rest (not variant); warp bits: variant first then the remaining rest
+    if (rest.size() < 2) continue;
+    order.push_back(rest[0]);
+    order.push_back(rest[1]);
+    std::vector<int> wl = vlist;
+    for (size_t i = 2; i < rest.size(); ++i) wl.push_back(rest[i]);
+    if ((int)wl.size() != nw_bits) continue;
+    order.insert(order.end(), wl.begin(), wl.end());
+    int reg_new[32];
+    for (int p = 0; p < 32; ++p) reg_new[p] = -1;
+    for (int r = 0; r < 4; ++r) reg_new[newreg[r]] = r;
+    std::vector<int> olist;
+    for (int q = 0; q < 64; ++q)
+      if ((vo >> q) & 1ull) olist.push_back(q);
+    // variant matrices: U_v = G_n ... G_1 in register space (row-major complex 16x16)
+    const size_t off = plan->mats.size() - pd->mat_begin;
+    for (int v = 0; v < nvar; ++v) {
+      uint32_t tbits = 0;
+      for (int b = 0; b < m_tile; ++b)
+        if ((v >> b) & 1) tbits |= 1u << vlist[b];
+      uint64_t obits = 0;
+      for (int b = 0; b < m_outer; ++b)
+        if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
+      Cx U[256];
+      for (int c = 0; c < 16; ++c) {
+        Cx u[16];
+        for (int j = 0; j < 16; ++j) u[j] = Cx{j == c ? 1.0 : 0.0, 0.0};
+        for (int i = ob; i < oe; ++i) {
+          const DevOp& o = plan->ops[i];
+          dense_apply(u, o, plan->mats.data() + pd->mat_begin + o.mat_off, reg_new, tbits, obits);
+        }
+        for (int j = 0; j < 16; ++j) U[j * 16 + c] = u[j];
+      }
+      for (int e = 0; e < 256; ++e) { plan->mats.push_back(U[e].re); plan->mats.push_back(U[e].im); }
+    }
+    S.dense = 1;
+    S.m_tile = (uint8_t)m_tile;
+    S.m_outer = (uint8_t)m_outer;
+    for (int b = 0; b < 3; ++b) S.var_outer[b] = (int8_t)(b < m_outer ? olist[b] : -1);
+    for (int r = 0; r < 4; ++r) S.regpos[r] = (int8_t)newreg[r];
+    for (int b = 0; b < 12; ++b) S.thrpos[b] = (int8_t)(b < (int)order.size() ? order[b] : -1);
+    S.op_begin = (int32_t)(off / 2);
+    S.op_end = 0;
+  }
 }
 
 }  // namespace
@@ -333,7 +564,16 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
     const int R = reverse ? 3 : 4;
     if (o.kernel == 1 && k - R >= 5) {
       pd.R = R;
-      plan_stages(plan, &pd, R);
+      if (!reverse && o.dense) plan_stages(plan, &pd, R, std::max(0, std::min(3, k - 9)), 3);
+      else plan_stages(plan, &pd, R);
+      if (!reverse && o.dense) {
+        // shared-memory budget of the register kernel: 2 tile buffers + ops + stages + hi table
+        const size_t fixed = (size_t(32) << k) + (size_t)(pd.op_end - pd.op_begin) * sizeof(RegOp) +
+                             (size_t)(pd.stage_end - pd.stage_begin) * sizeof(StageDesc) + (size_t(8) << (k - pd.low)) + 64;
+        const size_t limit = 227 * 1024;
+        const size_t budget = fixed < limit ? (limit - fixed) / 8 : 0;
+        densify_stages(plan, &pd, budget);
+      }
     } else {
       pd.R = 0;
       pd.stage_begin = pd.stage_end = (int)plan->stages.size();
@@ -342,6 +582,38 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
         plan->ops[i].grad_local = (int16_t)(plan->ops[i].grad_slot >= 0 ? gl++ : -1);
     }
     plan->passes.push_back(pd);
+  }
+  // compact register-kernel ops
+  plan->rops.assign(plan->ops.size(), RegOp{});
+  for (const PassDesc& pd : plan->passes) {
+    if (pd.R == 0) continue;
+    for (int i = pd.op_begin; i < pd.op_end; ++i) {
+      const DevOp& o = plan->ops[i];
+      RegOp r;
+      std::memset(&r, 0, sizeof(r));
+      const uint32_t ra = o.ra >= 0 ? (uint32_t)o.ra : 15u, rb = o.rb >= 0 ? (uint32_t)o.rb : 15u;
+      const uint32_t pa = o.pa >= 0 ? (uint32_t)o.pa : 31u, pb = o.pb >= 0 ? (uint32_t)o.pb : 31u;
+      const uint32_t gen = o.grad_slot >= 0 ? (o.gen_dim == 4 ? 2u : 1u) : 0u;
+      uint32_t dfl = 0;
+      if (o.type == OP_D1) {
+        const double* m = plan->mats.data() + pd.mat_begin + o.mat_off;
+        if (m[0] == 1.0 && m[1] == 0.0) {
+          dfl |= 1u;
+          if (m[2] == -1.0 && m[3] == 0.0) dfl |= 2u;
+        }
+      }
+      r.code = (uint32_t)o.type | (ra << 4) | (rb << 8) | ((uint32_t)o.cj << 12) | (pa << 16) | (pb << 21) |
+               (gen << 26) | ((o.gen_diag ? 1u : 0u) << 28) | (dfl << 29);
+      r.mat_off = (uint16_t)(o.mat_off / 2);
+      r.gen_off = (uint16_t)(o.gen_off / 2);
+      r.cthr = (uint16_t)o.cthr;
+      r.grad_local = o.grad_local;
+      r.qa = (uint8_t)(o.qa >= 0 ? o.qa : 0);
+      r.qb = (uint8_t)(o.qb >= 0 ? o.qb : 0);
+      r.couter = o.couter;
+      r.grad_slot = o.grad_slot;
+      plan->rops[i] = r;
+    }
   }
 }
 

@@ -33,7 +33,7 @@ struct sv_state_s {
   double* psi = nullptr;
   sv::DevBuf d_ops, d_mats, d_terms, d_partials, d_out;
   std::vector<char> h_stage;
-  size_t plan_stages_off = 0, plan_mats_off = 0;
+  size_t plan_stages_off = 0, plan_mats_off = 0, plan_rops_off = 0;
   sv::PlanOptions opts;
   sv_stats stats{};
   sv::ShardState* shard = nullptr;

@@ -54,18 +54,49 @@ static_assert(sizeof(DevOp) == 64, "DevOp layout");
 // Register-kernel stage: which tile positions the 2^R amplitudes a thread holds in registers span
 // (regpos), and the order of the remaining positions over thread-index bits (thrpos; bits 0..4 =
 // lane). Ops of a stage whose non-diagonal targets are all register positions run from registers.
+//
+// Dense stages (forward passes): all ops of the stage are folded on the host into one 16x16
+// complex matrix per "variant" — the assignment of the thread / outer bits the ops read through
+// controls or diagonal factors — and applied as a real 32x32 GEMM over the tile's 2^(k-4)
+// vectors with FP64 tensor-core MMAs (mma.sync m8n8k4 f64). For dense stages thrpos holds
+// [c0 c1 c2 | n0 n1 | w0 w1 w2 ...]: column-in-MMA bits, N-tile bits, warp bits; the m_tile
+// variant positions are the first warp bits; op_begin is the matrix offset (double2 units).
 struct StageDesc {
   int8_t regpos[4];
   int8_t thrpos[12];
-  int32_t op_begin, op_end;  // range in the pass' op list (pass-relative)
+  int32_t op_begin, op_end;  // range in the pass' op list (pass-relative); dense: op_begin = matrix offset
   uint16_t swz_reg[16];      // swizzled smem offset contribution of register index j (XOR-linear)
+  uint8_t dense;             // 1: dense MMA stage
+  uint8_t m_tile;            // variant bits on warp positions (thrpos[5 .. 5+m_tile))
+  uint8_t m_outer;           // variant bits on outer qubits (var_outer[0 .. m_outer))
+  int8_t var_outer[3];
+  uint16_t pad;
 };
-static_assert(sizeof(StageDesc) == 56, "StageDesc layout");
+static_assert(sizeof(StageDesc) == 64, "StageDesc layout");
 
+
+// Compact op of the register kernel (32 bytes: two 16-byte shared loads per op).
+//   code bits [0,4) type, [4,8) ra (15 = not a register bit), [8,12) rb, [12,16) cj,
+//             [16,21) pa (31 = outside the tile), [21,26) pb, [26,28) generator (0 none, 1 2x2, 2 4x4),
+//             [28] generator diagonal, [29,32) D1 flags (bit0: a == 1, bit1: a == 1 and b == -1)
+struct RegOp {
+  uint32_t code;
+  uint16_t mat_off;    // double2 units, relative to the pass' matrix block
+  uint16_t gen_off;    // double2 units
+  uint16_t cthr;       // control bits on thread positions (tile-position space)
+  int16_t grad_local;  // index among the pass' grad ops, -1 none
+  uint8_t qa, qb;      // physical qubits (outer target bits of diagonal ops)
+  uint16_t pad;
+  uint64_t couter;     // control bits outside the tile (local physical index space)
+  int32_t grad_slot;   // global adjoint slot (-1 none)
+  uint32_t pad2;
+};
+static_assert(sizeof(RegOp) == 32, "RegOp layout");
 
 constexpr int kMaxTileQubits = 13;
 constexpr int kMaxOpsPerPass = 256;
-constexpr int kMaxMatDoublesPerPass = 2048;
+constexpr int kMaxMatDoublesPerPass = 2048;      // sequential ops' matrices per pass
+constexpr int kMaxDenseMatDoublesPerPass = 8192; // dense-stage variant matrices per pass (64 KiB)
 
 struct PassDesc {
   int32_t k;                // tile qubits
@@ -82,6 +113,7 @@ struct PassDesc {
 struct Plan {
   std::vector<PassDesc> passes;
   std::vector<DevOp> ops;
+  std::vector<RegOp> rops;  // compact copy of ops for register passes (same indexing)
   std::vector<double> mats;
   std::vector<StageDesc> stages;
   int n_grad_slots = 0;
@@ -116,6 +148,7 @@ struct PlanOptions {
   int low_qubits = 3;
   bool fusion = true;
   int kernel = 1;        // 1: register-blocked stage kernel where possible, 0: shared-memory kernel
+  int dense = 1;         // 1: dense FP64-MMA stages in forward passes where cheaper, 0: never
 };
 int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual);
 void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOptions& o, bool reverse_for_adjoint,
@@ -128,6 +161,7 @@ struct PassLaunch {
   const DevOp* d_ops;      // device pointer to the plan's ops
   const double* d_mats;    // device pointer to the plan's matrices
   const StageDesc* d_stages;  // device pointer to the plan's stages
+  const RegOp* d_rops;        // device pointer to the plan's compact ops
   double* d_partials;      // [n_slots][grid] adjoint overlap partials (or null)
   int nmats;               // matrix doubles of this pass
   int grid;                // CTAs
@@ -138,6 +172,7 @@ struct PassLaunch {
 cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
 cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
 int pass_grid(int n_local, int k, bool dual);
+int plan_grid(const Plan& plan, int n_local);
 
 cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
 

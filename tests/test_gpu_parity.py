@@ -104,7 +104,8 @@ def test_random_complex_circuits(P, n):
     _assert_amps(_gpu_run(P, n, w.gates, w.params), ref)
 
 
-@pytest.mark.parametrize("opts", [{1: 4}, {1: 7}, {1: 10}, {2: 0}, {3: 0}, {3: 5}, {1: 13}])
+@pytest.mark.parametrize("opts", [{1: 4}, {1: 7}, {1: 10}, {2: 0}, {3: 0}, {3: 5}, {1: 13}, {4: 0}, {5: 0},
+                                  {1: 9}, {1: 11}, {4: 0, 1: 12}])
 def test_plan_options_do_not_change_results(P, opts):
     """Tile width, fusion on/off and the low-qubit granule only change the schedule."""
     n = 16
@@ -113,10 +114,18 @@ def test_plan_options_do_not_change_results(P, opts):
     _assert_amps(_gpu_run(P, n, w.gates, w.params, opts=opts), ref)
 
 
-def test_c4_shape_at_22q(P):
-    """C4's generator (Haar 1q + CZ bricks) at 22 qubits, depth 12."""
+@pytest.mark.parametrize("dense", [1, 0])
+def test_c4_shape_at_22q(P, dense):
+    """C4's generator (Haar 1q + CZ bricks) at 22 qubits, depth 12; dense MMA stages on and off."""
     w = W.random_circuit(22, 12, seed=3040)
-    _assert_amps(_gpu_run(P, 22, w.gates), oracle.apply_circuit(22, w.gates))
+    _assert_amps(_gpu_run(P, 22, w.gates, opts={4: dense}), oracle.apply_circuit(22, w.gates))
+
+
+def test_dense_stages_are_used(P):
+    """The C4 plan folds most register stages into dense FP64-MMA stages (planner introspection)."""
+    w = W.random_circuit(22, 12, seed=3040)
+    plan = P.sv_plan_info(22, w.gates)
+    assert sum(p["n_dense"] for p in plan) > 0.5 * sum(p["n_stages"] for p in plan)
 
 
 def test_mirror_and_norm_at_24q(P):
