@@ -34,6 +34,10 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 36.9  # measured FP64 tensor (DMMA) peak = DMMA+DFMA mixed peak on this pool's B200
+# dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
+# --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
+TRAFFIC_PER_LAUNCH = {}
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
 
@@ -224,6 +228,9 @@ def main():
     passes = st["gate_passes"] // args.steps
     hbm_peak, peak_src = _peaks()
     amps = float(1 << n)
+    plan = P.sv_plan_info(n, ga, w.params)
+    fma_per_amp = sum(p["fma_per_amp"] for p in plan)
+    fp64_flops = 2.0 * fma_per_amp * amps  # algorithmic FP64 work of the executed plan
     # effective SV bytes: what unfused single-gate sweeps would move: 32 B x 2^(n-c) per gate
     eff_bytes = sum(32.0 * amps / (1 << len(g.controls)) for g in w.gates)
     plan_bytes = st["algorithmic_bytes"] / args.steps
@@ -286,10 +293,16 @@ def main():
             "sv_effective_gbs": eff_bytes / (circ_ms / 1e3) / 1e9,
             "plan_hbm_gbs": plan_bytes / (ms_step / 1e3) / 1e9,
             "plan_hbm_frac": plan_bytes / (ms_step / 1e3) / 1e9 / hbm_peak,
-            "roofline": {"bound": "hbm", "kernel": "k_pass<false> (fused forward tile pass)",
-                         "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None,
-                         "algorithmic_bytes_per_launch": pass_bytes, "avg_launch_ms": pass_ms},
+            "roofline": {
+                "bound": "tensor", "kernel": "k_pass_reg<3,false> (fused forward tile pass: FP64 DMMA + DFMA stages)",
+                "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                "peak_source": "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
+                               "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)",
+                "unit": "TFLOP/s", "frac": fp64_flops / passes / (pass_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                "traffic": TRAFFIC_PER_LAUNCH.get(args.config),
+                "algorithmic_flops_per_launch": fp64_flops / passes, "avg_launch_ms": pass_ms,
+                "hbm": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src,
+                        "unit": "GB/s", "frac": achieved / hbm_peak, "algorithmic_bytes_per_launch": pass_bytes}},
             "grad": grad,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -25,6 +25,9 @@ typedef struct {
   uint64_t nondiag_mask;/* qubits on which the pass' ops act non-diagonally (subset of tile_mask) */
   int32_t n_dense;      /* stages executed as dense FP64-MMA stages                              */
   int32_t mat_doubles;  /* matrix data of the pass (doubles)                                     */
+  int32_t fma_per_amp;  /* FP64 fused multiply-adds per amplitude the pass executes (dense stages   */
+                        /* 64 each; sequential ops by class) — the roofline's algorithmic work     */
+  int32_t pad;
 } sv_pass_info;
 
 /* Plans `gates` for an n-qubit single-GPU state exactly as sv_apply_circuit (adjoint = 0) or the

@@ -377,7 +377,11 @@ int plan_grid(const Plan& plan, int n_local) {
   const PassDesc& pd = plan.passes[0];
   if (pd.R > 0) {
     const int64_t ntiles = 1ll << (n_local - pd.k);
-    const int64_t want = num_sms();
+    // forward passes: two CTAs per SM (their phases interleave: one CTA's MMA stage overlaps the
+    // other's shared-memory / HBM phases); adjoint passes: one (register-heavy) CTA per SM
+    bool has_grad = false;
+    for (const PassDesc& p : plan.passes) has_grad |= p.n_grad > 0;
+    const int64_t want = (int64_t)num_sms() * (has_grad ? 1 : 2);
     return (int)(ntiles < want ? ntiles : want);
   }
   return pass_grid(n_local, pd.k, false);

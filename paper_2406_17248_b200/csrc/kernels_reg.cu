@@ -371,74 +371,69 @@ __device__ __forceinline__ double lds64(const double* p) {
   return r;
 }
 
-__device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, const double2* mats2, uint64_t base,
-                                            int warp, int lane, int nw_bits) {
-  uint32_t twarp = 0;
-  for (int b = 0; b < nw_bits; ++b)
-    if ((warp >> b) & 1) twarp |= 1u << S.thrpos[5 + b];
-  uint32_t var = (uint32_t)warp & ((1u << S.m_tile) - 1u);
+__device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, const double2* __restrict__ gmats2,
+                                            uint64_t base, int warp, int lane) {
+  // warp-owned vectors: 2 N-tiles (n0) x 8 MMA columns (c0 c1 c2); all address parts are
+  // host-precomputed swizzled offsets (the swizzle is XOR-linear)
+  uint32_t var = S.warp_var[warp];
   for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
-  const double* U = reinterpret_cast<const double*>(mats2 + S.op_begin + var * 256u);
-  const uint32_t p0 = 1u << S.regpos[0], p1 = 1u << S.regpos[1], p2 = 1u << S.regpos[2], p3 = 1u << S.regpos[3];
-  const uint32_t c0 = 1u << S.thrpos[0], c1 = 1u << S.thrpos[1], c2 = 1u << S.thrpos[2];
-  const uint32_t n0 = 1u << S.thrpos[3], n1 = 1u << S.thrpos[4];
-  // ---- B fragments: amps j = 4 kq + lane%4 of column lane/4 ----
-  const uint32_t lb = (uint32_t)lane;
-  const uint32_t tcolB = ((lb >> 2) & 1u ? c0 : 0u) | ((lb >> 3) & 1u ? c1 : 0u) | ((lb >> 4) & 1u ? c2 : 0u);
-  const uint32_t tjlo = ((lb & 1u) ? p0 : 0u) | ((lb & 2u) ? p1 : 0u);
-  double b[4][8];
+  const double2* U = gmats2 + S.dense_off + var * (16u * 20u);  // global (L1/L2-resident)
+  double2 ue[2][4];
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    const uint32_t tn = twarp | ((nt & 1) ? n0 : 0u) | ((nt & 2) ? n1 : 0u) | tcolB | tjlo;
+  for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+    for (int kh = 0; kh < 4; ++kh) ue[mh][kh] = __ldg(U + (8 * mh + (lane >> 2)) * 20 + 4 * kh + (lane & 3));
+  const uint32_t wsw = S.warp_swz[warp];
+  const uint32_t baseB = wsw ^ S.lane_b[lane];
+  double b[2][8];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int kq = 0; kq < 4; ++kq) {
-      const uint32_t t = tn | ((kq & 1) ? p2 : 0u) | ((kq & 2) ? p3 : 0u);
-      const double2 x = tp[swz(t)];
+      const double2 x = tp[baseB ^ S.swz_reg[nt * 4 + kq]];
       b[nt][kq] = x.x;
       b[nt][kq + 4] = x.y;
     }
-  }
-  // ---- D = A B ----
-  double d[4][4][2];
+  // ---- D = A B, A = [[Ur, -Ui], [Ui, Ur]] ----
+  double d[4][2][2];
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
-  const int arow = lane >> 2, acol = lane & 3;
+    for (int nt = 0; nt < 2; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
+  for (int mh = 0; mh < 2; ++mh) {
 #pragma unroll
-    for (int kt = 0; kt < 8; ++kt) {
-      const int jo = 8 * (mt & 1) + arow, ji = 4 * (kt & 3) + acol;
-      // [[Ur, -Ui], [Ui, Ur]]: re-out rows mt < 2, im-in columns kt >= 4
-      const bool im_out = mt >= 2, im_in = kt >= 4;
-      const double* e = U + 2 * (jo * 16 + ji);
-      double a = lds64(e + ((im_out != im_in) ? 1 : 0));
-      if (!im_out && im_in) a = -a;
+    for (int kh = 0; kh < 4; ++kh) {
+      // one complex entry feeds the four (re/im out) x (re/im in) fragments
+      const double2 e = ue[mh][kh];
+      // consecutive MMAs go to four different accumulators (hides the MMA latency)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) dmma(d[mt][nt][0], d[mt][nt][1], a, b[nt][kt]);
+      for (int nt = 0; nt < 2; ++nt) {
+        dmma(d[mh][nt][0], d[mh][nt][1], e.x, b[nt][kh]);           // Re out += Ur Re in
+        dmma(d[mh + 2][nt][0], d[mh + 2][nt][1], e.y, b[nt][kh]);   // Im out += Ui Re in
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        dmma(d[mh][nt][0], d[mh][nt][1], -e.y, b[nt][kh + 4]);      // Re out -= Ui Im in
+        dmma(d[mh + 2][nt][0], d[mh + 2][nt][1], e.x, b[nt][kh + 4]); // Im out += Ur Im in
+      }
     }
   }
   // ---- stores: amps j = 8 mh + lane/4 of columns 2 (lane%4) + v ----
-  const uint32_t tjs = ((lb >> 2) & 1u ? p0 : 0u) | ((lb >> 3) & 1u ? p1 : 0u) | ((lb >> 4) & 1u ? p2 : 0u);
-  const uint32_t tcs = ((lb & 1u) ? c1 : 0u) | ((lb & 2u) ? c2 : 0u);
+  const uint32_t baseD = wsw ^ S.lane_d[lane];
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    const uint32_t tn = twarp | ((nt & 1) ? n0 : 0u) | ((nt & 2) ? n1 : 0u) | tjs | tcs;
+  for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const uint32_t t = tn | (mh ? p3 : 0u) | (v ? c0 : 0u);
-        tp[swz(t)] = make_double2(d[mh][nt][v], d[mh + 2][nt][v]);
-      }
-  }
+      for (int v = 0; v < 2; ++v)
+        tp[baseD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]] = make_double2(d[mh][nt][v], d[mh + 2][nt][v]);
 }
 
 // ---------------------------------------------------------------- the pass kernel
 
 template <int NR, bool DUAL>
-__global__ void __launch_bounds__(256, 1) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
+__global__ void __launch_bounds__(256, DUAL ? 1 : 2) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
@@ -511,9 +506,9 @@ __global__ void __launch_bounds__(256, 1) k_pass_reg(double2* __restrict__ psi, 
     // ---- stages ----
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
-      if constexpr (!DUAL && NR == 4) {
+      if constexpr (!DUAL) {
         if (S.dense) {
-          dense_stage(tp, S, mats2, base, warp, lane, a.k - 9);
+          dense_stage(tp, S, reinterpret_cast<const double2*>(a.mats), base, warp, lane);
           __syncthreads();
           continue;
         }
@@ -604,7 +599,7 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   a.low = pd.low;
   a.nops = pd.op_end - pd.op_begin;
   a.nstages = pd.stage_end - pd.stage_begin;
-  a.nmats = L.nmats;
+  a.nmats = pd.seq_mats < L.nmats ? pd.seq_mats : L.nmats;  // dense variants stay in global memory
   a.ngrad = pd.n_grad;
   a.grid = L.grid;
   for (int i = 0; i < kMaxTileQubits + 3; ++i) a.tq[i] = pd.tq[i];
@@ -624,7 +619,7 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   static bool attr_set[2] = {false, false};
   if (!attr_set[dual]) {
     cudaError_t e = dual ? cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
-                         : cudaFuncSetAttribute(k_pass_reg<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                         : cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set[dual] = true;
   }
@@ -633,8 +628,8 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
     if (pd.R != 3) return cudaErrorInvalidValue;
     k_pass_reg<3, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
   } else {
-    if (pd.R != 4) return cudaErrorInvalidValue;
-    k_pass_reg<4, false><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
+    if (pd.R != 3) return cudaErrorInvalidValue;
+    k_pass_reg<3, false><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
   }
   return cudaGetLastError();
 }

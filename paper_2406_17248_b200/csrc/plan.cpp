@@ -56,30 +56,76 @@ uint32_t swz(uint32_t t) { return t ^ ((t >> 3 ^ t >> 6 ^ t >> 9 ^ t >> 12) & 7u
 
 bool op_is_diag(const DevOp& o) { return o.type == OP_D1 || o.type == OP_D2; }
 
-// Splits the ops of one pass into register stages (see StageDesc) and reorders them stage by
-// stage. An op joins the current stage if it may legally move ahead of the ops left for later
-// stages (same commutation rule as the pass planner) and its non-diagonal target positions fit
-// the stage's R register positions.
-void plan_stages(Plan* plan, PassDesc* pd, int R, int max_var_tile = -1, int max_var_total = -1) {
-  const int k = pd->k;
-  std::vector<DevOp> ops(plan->ops.begin() + pd->op_begin, plan->ops.begin() + pd->op_end);
-  auto phys_masks = [&](const DevOp& o, uint64_t* N, uint64_t* A) {
-    uint64_t t = (1ull << o.qa) | (o.qb >= 0 ? (1ull << o.qb) : 0ull);
-    uint64_t c = o.couter;
-    for (int p = 0; p < k; ++p)
-      if ((o.ctile >> p) & 1ull) c |= 1ull << pd->tq[p];
-    *N = op_is_diag(o) ? 0ull : t;
-    *A = t | c;
+// ---------------------------------------------------------------- register stages
+
+struct StagePlan {
+  StageDesc sd;
+  std::vector<DevOp> ops;  // in execution order, ra/rb/cj/cthr relative to this stage
+  uint32_t regset = 0;     // register positions
+};
+
+// Commutation masks of an op in physical qubits: N = non-diagonal targets, A = all qubits.
+void phys_masks(const DevOp& o, const PassDesc& pd, uint64_t* N, uint64_t* A) {
+  uint64_t t = (1ull << o.qa) | (o.qb >= 0 ? (1ull << o.qb) : 0ull);
+  uint64_t c = o.couter;
+  for (int p = 0; p < pd.k; ++p)
+    if ((o.ctile >> p) & 1ull) c |= 1ull << pd.tq[p];
+  *N = op_is_diag(o) ? 0ull : t;
+  *A = t | c;
+}
+
+uint32_t pos_mask(const DevOp& o) {
+  if (op_is_diag(o)) return 0u;
+  return (1u << o.pa) | (o.pb >= 0 ? (1u << o.pb) : 0u);
+}
+
+// Sets the register-relative fields of the stage's ops (ra, rb, cj, cthr) for register positions
+// regpos[0..R) and canonicalises two-qubit non-diagonal ops to ra < rb (swapping matrix bits).
+void bind_stage_ops(StagePlan* sp, const int* regpos, int R, int stage_idx, Plan* plan, const PassDesc& pd) {
+  int reg_of[32];
+  for (int p = 0; p < 32; ++p) reg_of[p] = -1;
+  for (int r = 0; r < R; ++r) reg_of[regpos[r]] = r;
+  auto perm = [](int i) { return ((i & 1) << 1) | ((i >> 1) & 1); };
+  auto swap_bits = [&](double* m) {
+    double t[32];
+    for (int r = 0; r < 4; ++r)
+      for (int c = 0; c < 4; ++c) {
+        t[2 * (perm(r) * 4 + perm(c))] = m[2 * (r * 4 + c)];
+        t[2 * (perm(r) * 4 + perm(c)) + 1] = m[2 * (r * 4 + c) + 1];
+      }
+    std::memcpy(m, t, sizeof(t));
   };
-  auto pos_mask = [&](const DevOp& o) -> uint32_t {
-    if (op_is_diag(o)) return 0u;
-    return (1u << o.pa) | (o.pb >= 0 ? (1u << o.pb) : 0u);
-  };
+  for (DevOp& o : sp->ops) {
+    o.stage = (int16_t)stage_idx;
+    o.ra = (int8_t)(o.pa >= 0 ? reg_of[o.pa] : -1);
+    o.rb = (int8_t)(o.pb >= 0 ? reg_of[o.pb] : -1);
+    o.cj = 0;
+    o.cthr = 0;
+    for (int p = 0; p < pd.k; ++p)
+      if ((o.ctile >> p) & 1ull) {
+        if (reg_of[p] >= 0) o.cj |= (uint8_t)(1u << reg_of[p]);
+        else o.cthr |= 1ull << p;
+      }
+    if ((o.type == OP_M2 || o.type == OP_SWAP) && o.ra > o.rb) {
+      std::swap(o.ra, o.rb);
+      std::swap(o.pa, o.pb);
+      std::swap(o.qa, o.qb);
+      if (o.type == OP_M2) swap_bits(plan->mats.data() + pd.mat_begin + o.mat_off);
+      if (o.grad_slot >= 0 && !o.gen_diag && o.gen_dim == 4) swap_bits(plan->mats.data() + pd.mat_begin + o.gen_off);
+    }
+  }
+}
+
+// Greedy split of `ops` (pass order) into register stages of <= R register positions. An op joins
+// the current stage if it may legally move ahead of the ops left for later stages (same
+// commutation rule as the pass planner) and its non-diagonal target positions fit the register
+// set; with max_var_total >= 0 it must also keep the stage's variant bits (thread / outer bits
+// read by controls or diagonal factors, see StageDesc) within the limits.
+std::vector<StagePlan> split_stages(const std::vector<DevOp>& ops, const PassDesc& pd, int R, int max_var_tile,
+                                    int max_var_total) {
+  std::vector<StagePlan> out;
   std::vector<int> pending(ops.size());
   for (size_t i = 0; i < ops.size(); ++i) pending[i] = (int)i;
-  std::vector<DevOp> out;
-  pd->stage_begin = (int)plan->stages.size();
-  int stage_idx = 0;
   while (!pending.empty()) {
     uint32_t regset = 0, vt = 0;
     uint64_t bN = 0, bA = 0, vo = 0;
@@ -87,7 +133,7 @@ void plan_stages(Plan* plan, PassDesc* pd, int R, int max_var_tile = -1, int max
     for (int i : pending) {
       const DevOp& op = ops[i];
       uint64_t N, A;
-      phys_masks(op, &N, &A);
+      phys_masks(op, pd, &N, &A);
       bool ok = !(N & bA) && !(A & bN);
       const uint32_t pm = pos_mask(op);
       uint32_t nreg = regset;
@@ -98,7 +144,6 @@ void plan_stages(Plan* plan, PassDesc* pd, int R, int max_var_tile = -1, int max
       uint32_t nvt = vt;
       uint64_t nvo = vo;
       if (ok && max_var_total >= 0) {
-        // variant bits (dense stages): thread / outer bits read by controls or diagonal factors
         nvt |= (uint32_t)op.ctile;
         nvo |= op.couter;
         if (op_is_diag(op)) {
@@ -115,103 +160,62 @@ void plan_stages(Plan* plan, PassDesc* pd, int R, int max_var_tile = -1, int max
       if (ok) { taken.push_back(i); regset = nreg; vt = nvt; vo = nvo; }
       else { skipped.push_back(i); bN |= N; bA |= A; }
     }
-    if (taken.empty()) {
-      // the variant limit admits nothing: take the first pending op (this stage stays sequential)
+    if (taken.empty()) {  // the variant limit admits nothing: the first pending op goes alone
       taken.push_back(skipped.front());
       skipped.erase(skipped.begin());
       regset = pos_mask(ops[taken[0]]);
     }
-    // layout: lanes 0..2 on thread positions with distinct residues mod 3 (conflict-free 16-byte
-    // shared-memory phases), then fill the register set, then the remaining thread positions.
-    std::vector<int> free_pos;
-    for (int p = 0; p < k; ++p)
-      if (!((regset >> p) & 1u)) free_pos.push_back(p);
-    std::vector<int> lanes;
-    for (int res = 0; res < 3; ++res)
-      for (size_t f = 0; f < free_pos.size(); ++f)
-        if (free_pos[f] % 3 == res && (int)free_pos.size() - 1 >= R - __builtin_popcount(regset)) {
-          lanes.push_back(free_pos[f]);
-          free_pos.erase(free_pos.begin() + f);
-          break;
-        }
-    // fill registers from the highest free positions
-    while (__builtin_popcount(regset) < R && !free_pos.empty()) {
-      regset |= 1u << free_pos.back();
-      free_pos.pop_back();
-    }
-    std::vector<int> thr = lanes;
-    thr.insert(thr.end(), free_pos.begin(), free_pos.end());
-    StageDesc sd;
-    std::memset(&sd, 0, sizeof(sd));
-    int rp[4] = {-1, -1, -1, -1}, nr = 0;
-    int reg_of[32];
-    for (int p = 0; p < 32; ++p) reg_of[p] = -1;
-    for (int p = 0; p < k; ++p)
-      if ((regset >> p) & 1u) { rp[nr] = p; reg_of[p] = nr; ++nr; }
-    for (int r = 0; r < 4; ++r) sd.regpos[r] = (int8_t)rp[r];
-    for (int b = 0; b < 12; ++b) sd.thrpos[b] = (int8_t)(b < (int)thr.size() ? thr[b] : -1);
-    for (int j = 0; j < (1 << R); ++j) {
-      uint32_t dep = 0;
-      for (int r = 0; r < R; ++r)
-        if ((j >> r) & 1) dep |= 1u << rp[r];
-      sd.swz_reg[j] = (uint16_t)swz(dep);
-    }
-    sd.op_begin = (int)out.size();
-    for (int i : taken) {
-      DevOp o = ops[i];
-      o.stage = (int16_t)stage_idx;
-      o.ra = (int8_t)(o.pa >= 0 ? reg_of[o.pa] : -1);
-      o.rb = (int8_t)(o.pb >= 0 ? reg_of[o.pb] : -1);
-      o.cj = 0;
-      o.cthr = 0;
-      for (int p = 0; p < k; ++p)
-        if ((o.ctile >> p) & 1ull) {
-          if (reg_of[p] >= 0) o.cj |= (uint8_t)(1u << reg_of[p]);
-          else o.cthr |= 1ull << p;
-        }
-      // two-qubit non-diagonal ops: canonical register order ra < rb (swap matrix index bits)
-      if ((o.type == OP_M2 || o.type == OP_SWAP) && o.ra > o.rb) {
-        std::swap(o.ra, o.rb);
-        std::swap(o.pa, o.pb);
-        std::swap(o.qa, o.qb);
-        auto perm = [](int i) { return ((i & 1) << 1) | ((i >> 1) & 1); };
-        if (o.type == OP_M2) {
-          double* m = plan->mats.data() + pd->mat_begin + o.mat_off;
-          double t[32];
-          for (int r = 0; r < 4; ++r)
-            for (int c = 0; c < 4; ++c) {
-              t[2 * (perm(r) * 4 + perm(c))] = m[2 * (r * 4 + c)];
-              t[2 * (perm(r) * 4 + perm(c)) + 1] = m[2 * (r * 4 + c) + 1];
-            }
-          std::memcpy(m, t, sizeof(t));
-        }
-        if (o.grad_slot >= 0 && !o.gen_diag && o.gen_dim == 4) {
-          double* g = plan->mats.data() + pd->mat_begin + o.gen_off;
-          double t[32];
-          for (int r = 0; r < 4; ++r)
-            for (int c = 0; c < 4; ++c) {
-              t[2 * (perm(r) * 4 + perm(c))] = g[2 * (r * 4 + c)];
-              t[2 * (perm(r) * 4 + perm(c)) + 1] = g[2 * (r * 4 + c) + 1];
-            }
-          std::memcpy(g, t, sizeof(t));
-        }
-      }
-      out.push_back(o);
-    }
-    sd.op_end = (int)out.size();
-    plan->stages.push_back(sd);
-    ++stage_idx;
+    StagePlan sp;
+    std::memset(&sp.sd, 0, sizeof(sp.sd));
+    sp.regset = regset;
+    for (int i : taken) sp.ops.push_back(ops[i]);
+    out.push_back(std::move(sp));
     pending.swap(skipped);
   }
-  std::copy(out.begin(), out.end(), plan->ops.begin() + pd->op_begin);
-  pd->stage_end = (int)plan->stages.size();
-  // local grad indices
-  int gl = 0;
-  for (int i = pd->op_begin; i < pd->op_end; ++i) plan->ops[i].grad_local = (int16_t)(plan->ops[i].grad_slot >= 0 ? gl++ : -1);
+  return out;
 }
 
+// Layout of a sequential stage: lanes 0..2 on thread positions with distinct residues mod 3
+// (conflict-free 16-byte shared phases), register set filled to R from the highest free
+// positions, then the remaining thread positions.
+void layout_sequential(StagePlan* sp, const PassDesc& pd, int R) {
+  const int k = pd.k;
+  uint32_t regset = sp->regset;
+  std::vector<int> free_pos;
+  for (int p = 0; p < k; ++p)
+    if (!((regset >> p) & 1u)) free_pos.push_back(p);
+  std::vector<int> lanes;
+  for (int res = 0; res < 3; ++res)
+    for (size_t f = 0; f < free_pos.size(); ++f)
+      if (free_pos[f] % 3 == res && (int)free_pos.size() - 1 >= R - __builtin_popcount(regset)) {
+        lanes.push_back(free_pos[f]);
+        free_pos.erase(free_pos.begin() + f);
+        break;
+      }
+  while (__builtin_popcount(regset) < R && !free_pos.empty()) {
+    regset |= 1u << free_pos.back();
+    free_pos.pop_back();
+  }
+  sp->regset = regset;
+  std::vector<int> thr = lanes;
+  thr.insert(thr.end(), free_pos.begin(), free_pos.end());
+  StageDesc& sd = sp->sd;
+  int rp[4] = {-1, -1, -1, -1}, nr = 0;
+  for (int p = 0; p < k; ++p)
+    if ((regset >> p) & 1u) rp[nr++] = p;
+  for (int r = 0; r < 4; ++r) sd.regpos[r] = (int8_t)rp[r];
+  for (int b = 0; b < 12; ++b) sd.thrpos[b] = (int8_t)(b < (int)thr.size() ? thr[b] : -1);
+  for (int j = 0; j < (1 << R); ++j) {
+    uint32_t dep = 0;
+    for (int r = 0; r < R; ++r)
+      if ((j >> r) & 1) dep |= 1u << rp[r];
+    sd.swz_reg[j] = (uint16_t)swz(dep);
+  }
+}
 
 // ---------------------------------------------------------------- dense (FP64-MMA) stages
+
+constexpr int kDenseStride = 20;  // complex entries per row of a stored variant matrix
 
 // FP64 pipe cost per amplitude of an op applied sequentially (DFMA path), for the dense choice.
 int seq_cost(const DevOp& o, const double* m) {
@@ -228,15 +232,18 @@ int seq_cost(const DevOp& o, const double* m) {
   return 0;
 }
 
-// Applies one op to the 16-dim register-space vector u (complex), given the values of the
-// variant bits it reads (tile positions in `tbits`, outer qubits in `obits`). reg_new[p] is the
-// dense register index of tile position p (-1 if p is not a register position).
+// Applies one op to the 16-dim register-space vector u, given the values of the variant bits it
+// reads (tile positions in tbits, outer qubits in obits). reg_new[p]: dense register index of
+// tile position p (-1 if p is not a register position).
 void dense_apply(Cx* u, const DevOp& o, const double* m, const int* reg_new, uint32_t tbits, uint64_t obits) {
-  if ((o.cthr & tbits) != o.cthr) return;
-  if ((o.couter & obits) != o.couter) return;
-  uint32_t cj = 0;
+  uint32_t cj = 0, cthr = 0;
   for (int p = 0; p < 32; ++p)
-    if (((o.ctile >> p) & 1ull) && reg_new[p] >= 0) cj |= 1u << reg_new[p];
+    if ((o.ctile >> p) & 1ull) {
+      if (reg_new[p] >= 0) cj |= 1u << reg_new[p];
+      else cthr |= 1u << p;
+    }
+  if ((cthr & tbits) != cthr) return;
+  if ((o.couter & obits) != o.couter) return;
   auto bit_of = [&](int pos, int q, int j) -> uint32_t {
     if (pos >= 0 && reg_new[pos] >= 0) return ((uint32_t)j >> reg_new[pos]) & 1u;
     if (pos >= 0) return (tbits >> pos) & 1u;
@@ -295,129 +302,188 @@ void dense_apply(Cx* u, const DevOp& o, const double* m, const int* reg_new, uin
   }
 }
 
-// Turns the stages of a forward pass into dense MMA stages where that is cheaper and feasible.
-void densify_stages(Plan* plan, PassDesc* pd, size_t mat_budget_doubles) {
-  const int k = pd->k;
-  const int nw_bits = k - 9;  // warp bits (256 threads at k = 12)
-  if (nw_bits < 0) return;
-  for (int si = pd->stage_begin; si < pd->stage_end; ++si) {
-    StageDesc& S = plan->stages[si];
-    const int ob = pd->op_begin + S.op_begin, oe = pd->op_begin + S.op_end;
-    // cost and variant bits
-    int cost = 0;
-    uint32_t vt = 0;
-    uint64_t vo = 0;
-    uint32_t regmask = 0;
-    for (int r = 0; r < 4; ++r) regmask |= 1u << S.regpos[r];
-    for (int i = ob; i < oe; ++i) {
-      const DevOp& o = plan->ops[i];
-      const double* m = plan->mats.data() + pd->mat_begin + o.mat_off;
-      cost += seq_cost(o, m);
-      vt |= (uint32_t)o.cthr;
-      vo |= o.couter;
-      if (o.type == OP_D1 || o.type == OP_D2) {
-        for (int t = 0; t < (o.type == OP_D2 ? 2 : 1); ++t) {
-          const int pos = t ? o.pb : o.pa;
-          const int q = t ? o.qb : o.qa;
-          if (pos >= 0 && !((regmask >> pos) & 1u)) vt |= 1u << pos;
-          if (pos < 0) vo |= 1ull << q;
-        }
+// Folds a 4-register stage into dense variant matrices (appended to plan->mats) when cheaper than
+// the sequential path and feasible: variant bits <= 3 in total, tile variant bits on warp
+// positions. Returns false (stage untouched) otherwise.
+bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles) {
+  const int k = pd.k;
+  const int nw_bits = k - 8;  // 2^(k-3) threads: 16 vectors of 16 amplitudes per warp
+  if (nw_bits < 1 || __builtin_popcount(sp->regset) != 4) return false;
+  const uint32_t regmask = sp->regset;
+  int cost = 0;
+  uint32_t vt = 0;
+  uint64_t vo = 0;
+  for (const DevOp& o : sp->ops) {
+    cost += seq_cost(o, plan->mats.data() + pd.mat_begin + o.mat_off);
+    vt |= (uint32_t)o.ctile & ~regmask;
+    vo |= o.couter;
+    if (op_is_diag(o))
+      for (int t = 0; t < (o.type == OP_D2 ? 2 : 1); ++t) {
+        const int pos = t ? o.pb : o.pa;
+        if (pos >= 0 && !((regmask >> pos) & 1u)) vt |= 1u << pos;
+        if (pos < 0) vo |= 1ull << (t ? o.qb : o.qa);
       }
-    }
-    const int m_tile = __builtin_popcount(vt), m_outer = __builtin_popcountll(vo);
-    if (std::getenv("SV_PLAN_DEBUG"))
-      std::fprintf(stderr, "stage %d: ops %d cost %d m_tile %d m_outer %d\n", si, oe - ob, cost, m_tile, m_outer);
-    if (cost < 20 || m_tile > nw_bits || m_outer > 3 || m_tile + m_outer > 3) continue;
-    const int nvar = 1 << (m_tile + m_outer);
-    const size_t need = (size_t)nvar * 512;
-    const size_t used = plan->mats.size() - pd->mat_begin;
-    if (used + need > mat_budget_doubles) continue;
-    // layout: register order R0..R3 and MMA column bits c0..c2 with conflict-free shared phases
-    std::vector<int> regs = {S.regpos[0], S.regpos[1], S.regpos[2], S.regpos[3]};
-    std::vector<int> free_pos;
-    for (int p = 0; p < k; ++p)
-      if (!((regmask >> p) & 1u) && !((vt >> p) & 1u)) free_pos.push_back(p);
-    int best[5] = {-1, -1, -1, -1, -1};
-    int best_score = -1;
-    auto distinct3 = [](int a, int b, int c) { return (a % 3) != (b % 3) && (a % 3) != (c % 3) && (b % 3) != (c % 3); };
-    for (int r0 = 0; r0 < 4 && best_score < 2; ++r0)
-      for (int r1 = 0; r1 < 4 && best_score < 2; ++r1) {
-        if (r1 == r0) continue;
-        for (size_t a = 0; a < free_pos.size() && best_score < 2; ++a)
-          for (size_t b = 0; b < free_pos.size() && best_score < 2; ++b)
-            for (size_t c = 0; c < free_pos.size() && best_score < 2; ++c) {
-              if (a == b || a == c || b == c) continue;
-              const int sc = (distinct3(regs[r0], regs[r1], free_pos[a]) ? 1 : 0) +
-                             (distinct3(regs[r0], free_pos[b], free_pos[c]) ? 1 : 0);
-              if (sc > best_score) {
-                best_score = sc;
-                best[0] = r0; best[1] = r1; best[2] = (int)a; best[3] = (int)b; best[4] = (int)c;
-              }
-            }
-      }
-    if (best_score < 0 || free_pos.size() < 3) continue;
-    std::vector<int> newreg = {regs[best[0]], regs[best[1]]};
-    for (int r = 0; r < 4; ++r)
-      if (r != best[0] && r != best[1]) newreg.push_back(regs[r]);
-    const int c0 = free_pos[best[2]], c1 = free_pos[best[3]], c2 = free_pos[best[4]];
-    std::vector<int> rest;
-    for (int p = 0; p < k; ++p)
-      if (!((regmask >> p) & 1u) && !((vt >> p) & 1u) && p != c0 && p != c1 && p != c2) rest.push_back(p);
-    // thrpos: c0 c1 c2 | n0 n1 | w (variant positions first)
-    std::vector<int> vlist;
-    for (int p = 0; p < k; ++p)
-      if ((vt >> p) & 1u) vlist.push_back(p);
-    std::vector<int> order = {c0, c1, c2};
-    // n0, n1 from rest (not variant); warp bits: variant first then the remaining rest
-    if (rest.size() < 2) continue;
-    order.push_back(rest[0]);
-    order.push_back(rest[1]);
-    std::vector<int> wl = vlist;
-    for (size_t i = 2; i < rest.size(); ++i) wl.push_back(rest[i]);
-    if ((int)wl.size() != nw_bits) continue;
-    order.insert(order.end(), wl.begin(), wl.end());
-    int reg_new[32];
-    for (int p = 0; p < 32; ++p) reg_new[p] = -1;
-    for (int r = 0; r < 4; ++r) reg_new[newreg[r]] = r;
-    std::vector<int> olist;
-    for (int q = 0; q < 64; ++q)
-      if ((vo >> q) & 1ull) olist.push_back(q);
-    // variant matrices: U_v = G_n ... G_1 in register space (row-major complex 16x16)
-    const size_t off = plan->mats.size() - pd->mat_begin;
-    for (int v = 0; v < nvar; ++v) {
-      uint32_t tbits = 0;
-      for (int b = 0; b < m_tile; ++b)
-        if ((v >> b) & 1) tbits |= 1u << vlist[b];
-      uint64_t obits = 0;
-      for (int b = 0; b < m_outer; ++b)
-        if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
-      Cx U[256];
-      for (int c = 0; c < 16; ++c) {
-        Cx u[16];
-        for (int j = 0; j < 16; ++j) u[j] = Cx{j == c ? 1.0 : 0.0, 0.0};
-        for (int i = ob; i < oe; ++i) {
-          const DevOp& o = plan->ops[i];
-          dense_apply(u, o, plan->mats.data() + pd->mat_begin + o.mat_off, reg_new, tbits, obits);
-        }
-        for (int j = 0; j < 16; ++j) U[j * 16 + c] = u[j];
-      }
-      for (int e = 0; e < 256; ++e) { plan->mats.push_back(U[e].re); plan->mats.push_back(U[e].im); }
-    }
-    S.dense = 1;
-    S.m_tile = (uint8_t)m_tile;
-    S.m_outer = (uint8_t)m_outer;
-    for (int b = 0; b < 3; ++b) S.var_outer[b] = (int8_t)(b < m_outer ? olist[b] : -1);
-    for (int r = 0; r < 4; ++r) S.regpos[r] = (int8_t)newreg[r];
-    for (int b = 0; b < 12; ++b) S.thrpos[b] = (int8_t)(b < (int)order.size() ? order[b] : -1);
-    S.op_begin = (int32_t)(off / 2);
-    S.op_end = 0;
   }
+  const int m_tile = __builtin_popcount(vt), m_outer = __builtin_popcountll(vo);
+  if (std::getenv("SV_PLAN_DEBUG"))
+    std::fprintf(stderr, "stage: ops %d cost %d m_tile %d m_outer %d\n", (int)sp->ops.size(), cost, m_tile, m_outer);
+  if (cost < 20 || m_tile > nw_bits || m_tile + m_outer > 3) return false;
+  const int nvar = 1 << (m_tile + m_outer);
+  const size_t per = 2 * 16 * kDenseStride;
+  const size_t used = plan->mats.size() - pd.mat_begin;
+  if (used + (size_t)nvar * per > mat_budget_doubles) return false;
+  // layout: R0, R1 and column bits c0, c1, c2 such that {R0, R1, c0} and {R0, c1, c2} have
+  // distinct residues mod 3 (conflict-free B loads and D stores)
+  int regs[4], nr = 0;
+  for (int p = 0; p < k; ++p)
+    if ((regmask >> p) & 1u) regs[nr++] = p;
+  std::vector<int> free_pos;
+  for (int p = 0; p < k; ++p)
+    if (!((regmask >> p) & 1u) && !((vt >> p) & 1u)) free_pos.push_back(p);
+  if (free_pos.size() < 4) return false;
+  auto d3 = [](int a, int b, int c) { return (a % 3) != (b % 3) && (a % 3) != (c % 3) && (b % 3) != (c % 3); };
+  int best[5] = {0, 1, 0, 1, 2}, best_score = -1;
+  for (int r0 = 0; r0 < 4 && best_score < 2; ++r0)
+    for (int r1 = 0; r1 < 4 && best_score < 2; ++r1) {
+      if (r1 == r0) continue;
+      for (size_t a = 0; a < free_pos.size() && best_score < 2; ++a)
+        for (size_t b = 0; b < free_pos.size() && best_score < 2; ++b)
+          for (size_t c = 0; c < free_pos.size() && best_score < 2; ++c) {
+            if (a == b || a == c || b == c) continue;
+            const int sc = (d3(regs[r0], regs[r1], free_pos[a]) ? 1 : 0) + (d3(regs[r0], free_pos[b], free_pos[c]) ? 1 : 0);
+            if (sc > best_score) { best_score = sc; best[0] = r0; best[1] = r1; best[2] = (int)a; best[3] = (int)b; best[4] = (int)c; }
+          }
+    }
+  int newreg[4] = {regs[best[0]], regs[best[1]], -1, -1};
+  for (int r = 0, w = 2; r < 4; ++r)
+    if (r != best[0] && r != best[1]) newreg[w++] = regs[r];
+  const int c0 = free_pos[best[2]], c1 = free_pos[best[3]], c2 = free_pos[best[4]];
+  std::vector<int> rest;
+  for (int p : free_pos)
+    if (p != c0 && p != c1 && p != c2) rest.push_back(p);
+  std::vector<int> vlist;
+  for (int p = 0; p < k; ++p)
+    if ((vt >> p) & 1u) vlist.push_back(p);
+  // thrpos: c0 c1 c2 | n0 | warp bits (variant positions first)
+  std::vector<int> order = {c0, c1, c2, rest[0]};
+  std::vector<int> wl = vlist;
+  for (size_t i = 1; i < rest.size(); ++i) wl.push_back(rest[i]);
+  if ((int)wl.size() != nw_bits) return false;
+  order.insert(order.end(), wl.begin(), wl.end());
+  int reg_new[32];
+  for (int p = 0; p < 32; ++p) reg_new[p] = -1;
+  for (int r = 0; r < 4; ++r) reg_new[newreg[r]] = r;
+  std::vector<int> olist;
+  for (int q = 0; q < 64; ++q)
+    if ((vo >> q) & 1ull) olist.push_back(q);
+  // variant matrices U_v = G_n ... G_1 (register space), row stride kDenseStride
+  const size_t off = plan->mats.size() - pd.mat_begin;
+  for (int v = 0; v < nvar; ++v) {
+    uint32_t tbits = 0;
+    for (int b = 0; b < m_tile; ++b)
+      if ((v >> b) & 1) tbits |= 1u << vlist[b];
+    uint64_t obits = 0;
+    for (int b = 0; b < m_outer; ++b)
+      if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
+    Cx U[256];
+    for (int c = 0; c < 16; ++c) {
+      Cx u[16];
+      for (int j = 0; j < 16; ++j) u[j] = Cx{j == c ? 1.0 : 0.0, 0.0};
+      for (const DevOp& o : sp->ops) dense_apply(u, o, plan->mats.data() + pd.mat_begin + o.mat_off, reg_new, tbits, obits);
+      for (int j = 0; j < 16; ++j) U[j * 16 + c] = u[j];
+    }
+    for (int j = 0; j < 16; ++j)
+      for (int c = 0; c < kDenseStride; ++c) {
+        const Cx e = c < 16 ? U[j * 16 + c] : Cx{0, 0};
+        plan->mats.push_back(e.re);
+        plan->mats.push_back(e.im);
+      }
+  }
+  StageDesc& S = sp->sd;
+  std::memset(&S, 0, sizeof(S));
+  S.dense = 1;
+  S.m_tile = (uint8_t)m_tile;
+  S.m_outer = (uint8_t)m_outer;
+  for (int b = 0; b < 3; ++b) S.var_outer[b] = (int8_t)(b < m_outer ? olist[b] : -1);
+  for (int r = 0; r < 4; ++r) S.regpos[r] = (int8_t)newreg[r];
+  for (int b = 0; b < 12; ++b) S.thrpos[b] = (int8_t)(b < (int)order.size() ? order[b] : -1);
+  S.dense_off = (uint16_t)(off / 2);
+  const uint32_t p2 = 1u << newreg[2], p3 = 1u << newreg[3], n0 = 1u << order[3], bc0 = 1u << c0;
+  const uint32_t p0 = 1u << newreg[0], p1 = 1u << newreg[1], bc1 = 1u << c1, bc2 = 1u << c2;
+  for (int w = 0; w < 8; ++w) {
+    uint32_t tw = 0;
+    for (int b = 0; b < nw_bits; ++b)
+      if ((w >> b) & 1) tw |= 1u << order[4 + b];
+    S.warp_swz[w] = (uint16_t)swz(tw);
+    S.warp_var[w] = (uint8_t)(w & ((1 << m_tile) - 1));
+  }
+  for (int l = 0; l < 32; ++l) {
+    const uint32_t lb = (uint32_t)l;
+    S.lane_b[l] = (uint16_t)swz(((lb >> 2) & 1u ? bc0 : 0u) | ((lb >> 3) & 1u ? bc1 : 0u) | ((lb >> 4) & 1u ? bc2 : 0u) |
+                                ((lb & 1u) ? p0 : 0u) | ((lb & 2u) ? p1 : 0u));
+    S.lane_d[l] = (uint16_t)swz(((lb >> 2) & 1u ? p0 : 0u) | ((lb >> 3) & 1u ? p1 : 0u) | ((lb >> 4) & 1u ? p2 : 0u) |
+                                ((lb & 1u) ? bc1 : 0u) | ((lb & 2u) ? bc2 : 0u));
+  }
+  for (int nt = 0; nt < 2; ++nt)
+    for (int kq = 0; kq < 4; ++kq)
+      S.swz_reg[nt * 4 + kq] = (uint16_t)swz((nt ? n0 : 0u) | ((kq & 1) ? p2 : 0u) | ((kq & 2) ? p3 : 0u));
+  for (int nt = 0; nt < 2; ++nt)
+    for (int mh = 0; mh < 2; ++mh)
+      for (int v = 0; v < 2; ++v)
+        S.swz_reg[8 + nt * 4 + mh * 2 + v] = (uint16_t)swz((nt ? n0 : 0u) | (mh ? p3 : 0u) | (v ? bc0 : 0u));
+  return true;
+}
+
+// Plans the register stages of pass `pd` (ops already emitted in pass order) and rewrites the
+// pass' op range in stage order.
+void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense) {
+  const int k = pd->k;
+  std::vector<DevOp> pops(plan->ops.begin() + pd->op_begin, plan->ops.begin() + pd->op_end);
+  std::vector<StagePlan> final_stages;
+  auto add_sequential = [&](std::vector<StagePlan> sub) {
+    for (StagePlan& sp : sub) {
+      layout_sequential(&sp, *pd, pd->R);
+      final_stages.push_back(std::move(sp));
+    }
+  };
+  pd->seq_mats = (int32_t)(plan->mats.size() - pd->mat_begin);
+  if (forward && dense && k >= 9) {
+    const size_t budget = size_t(1) << 22;  // variant matrices live in global memory (L2-resident)
+    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(3, k - 8), 3);
+    for (StagePlan& sp : st4) {
+      if (make_dense(&sp, *pd, plan, budget)) final_stages.push_back(std::move(sp));
+      else add_sequential(split_stages(sp.ops, *pd, pd->R, -1, -1));
+    }
+  } else {
+    add_sequential(split_stages(pops, *pd, pd->R, -1, -1));
+  }
+  // write back in stage order
+  pd->stage_begin = (int)plan->stages.size();
+  int pos = 0;
+  for (size_t si = 0; si < final_stages.size(); ++si) {
+    StagePlan& sp = final_stages[si];
+    if (!sp.sd.dense) {
+      int rp[4];
+      for (int r = 0; r < 4; ++r) rp[r] = sp.sd.regpos[r];
+      bind_stage_ops(&sp, rp, pd->R, (int)si, plan, *pd);
+    } else {
+      for (DevOp& o : sp.ops) o.stage = (int16_t)si;
+    }
+    sp.sd.op_begin = pos;
+    for (const DevOp& o : sp.ops) plan->ops[pd->op_begin + pos++] = o;
+    sp.sd.op_end = pos;
+    plan->stages.push_back(sp.sd);
+  }
+  pd->stage_end = (int)plan->stages.size();
+  int gl = 0;
+  for (int i = pd->op_begin; i < pd->op_end; ++i)
+    plan->ops[i].grad_local = (int16_t)(plan->ops[i].grad_slot >= 0 ? gl++ : -1);
 }
 
 }  // namespace
 
 int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual) {
-  int kmax = dual ? 11 : 12;
+  int kmax = 11;  // 2^11-amplitude tiles: 256 threads, two double-buffered CTAs per SM
   if (o.tile_qubits > 0) kmax = std::min(o.tile_qubits, kMaxTileQubits);
   kmax = std::max(kmax, std::min(n_local, 2));  // a two-qubit gate must fit a tile
   if (n_local <= kmax) return n_local;
@@ -561,21 +627,12 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
       plan->ops.push_back(op);
     }
     pd.op_end = (int)plan->ops.size();
-    const int R = reverse ? 3 : 4;
-    if (o.kernel == 1 && k - R >= 5) {
-      pd.R = R;
-      if (!reverse && o.dense) plan_stages(plan, &pd, R, std::max(0, std::min(3, k - 9)), 3);
-      else plan_stages(plan, &pd, R);
-      if (!reverse && o.dense) {
-        // shared-memory budget of the register kernel: 2 tile buffers + ops + stages + hi table
-        const size_t fixed = (size_t(32) << k) + (size_t)(pd.op_end - pd.op_begin) * sizeof(RegOp) +
-                             (size_t)(pd.stage_end - pd.stage_begin) * sizeof(StageDesc) + (size_t(8) << (k - pd.low)) + 64;
-        const size_t limit = 227 * 1024;
-        const size_t budget = fixed < limit ? (limit - fixed) / 8 : 0;
-        densify_stages(plan, &pd, budget);
-      }
+    if (o.kernel == 1 && k - 3 >= 5) {
+      pd.R = 3;
+      plan_pass_stages(plan, &pd, !reverse, o.dense != 0);
     } else {
       pd.R = 0;
+      pd.seq_mats = (int32_t)(plan->mats.size() - pd.mat_begin);
       pd.stage_begin = pd.stage_end = (int)plan->stages.size();
       int gl = 0;
       for (int i = pd.op_begin; i < pd.op_end; ++i)
@@ -615,6 +672,22 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
       plan->rops[i] = r;
     }
   }
+}
+
+int pass_fma_per_amp(const Plan& plan, size_t i) {
+  const PassDesc& pd = plan.passes[i];
+  int f = 0;
+  if (pd.R > 0) {
+    for (int si = pd.stage_begin; si < pd.stage_end; ++si) {
+      const StageDesc& S = plan.stages[si];
+      if (S.dense) { f += 64; continue; }
+      for (int j = pd.op_begin + S.op_begin; j < pd.op_begin + S.op_end; ++j)
+        f += seq_cost(plan.ops[j], plan.mats.data() + pd.mat_begin + plan.ops[j].mat_off);
+    }
+  } else {
+    for (int j = pd.op_begin; j < pd.op_end; ++j) f += seq_cost(plan.ops[j], plan.mats.data() + pd.mat_begin + plan.ops[j].mat_off);
+  }
+  return f;
 }
 
 }  // namespace sv

@@ -59,20 +59,26 @@ static_assert(sizeof(DevOp) == 64, "DevOp layout");
 // complex matrix per "variant" — the assignment of the thread / outer bits the ops read through
 // controls or diagonal factors — and applied as a real 32x32 GEMM over the tile's 2^(k-4)
 // vectors with FP64 tensor-core MMAs (mma.sync m8n8k4 f64). For dense stages thrpos holds
-// [c0 c1 c2 | n0 n1 | w0 w1 w2 ...]: column-in-MMA bits, N-tile bits, warp bits; the m_tile
-// variant positions are the first warp bits; op_begin is the matrix offset (double2 units).
+// [c0 c1 c2 | n0 | w0 w1 ...]: column-in-MMA bits, N-tile bit, warp bits; the m_tile variant
+// positions are the first warp bits; swz_reg[0..8) are the swizzled offsets of the B-fragment
+// loads (n, kq), swz_reg[8..16) those of the D-fragment stores (n, mh, v). Variant matrices are
+// row-major 16 x 16 complex with a row stride of 20 entries (bank-conflict-free A fragments).
 struct StageDesc {
   int8_t regpos[4];
   int8_t thrpos[12];
   int32_t op_begin, op_end;  // range in the pass' op list (pass-relative); dense: op_begin = matrix offset
   uint16_t swz_reg[16];      // swizzled smem offset contribution of register index j (XOR-linear)
   uint8_t dense;             // 1: dense MMA stage
-  uint8_t m_tile;            // variant bits on warp positions (thrpos[5 .. 5+m_tile))
+  uint8_t m_tile;            // variant bits on warp positions (thrpos[4 .. 4+m_tile))
   uint8_t m_outer;           // variant bits on outer qubits (var_outer[0 .. m_outer))
   int8_t var_outer[3];
-  uint16_t pad;
+  uint16_t dense_off;        // dense: first variant matrix (double2 units in the pass' matrix block)
+  uint16_t warp_swz[8];      // dense: swz(tile-position bits of warp w)
+  uint8_t warp_var[8];       // dense: tile-variant index of warp w
+  uint16_t lane_b[32];       // dense: swz(lane part of the B-fragment load address)
+  uint16_t lane_d[32];       // dense: swz(lane part of the D-fragment store address)
 };
-static_assert(sizeof(StageDesc) == 64, "StageDesc layout");
+static_assert(sizeof(StageDesc) == 216, "StageDesc layout");
 
 
 // Compact op of the register kernel (32 bytes: two 16-byte shared loads per op).
@@ -106,6 +112,8 @@ struct PassDesc {
   int32_t mat_begin;        // base offset of this pass' matrices in the plan's matrix array
   int32_t n_grad;           // grad ops in this pass (adjoint)
   int32_t R;                // register qubits per thread (0: shared-memory kernel)
+  int32_t seq_mats;         // matrix doubles the kernel stages in shared memory (ops' matrices);
+                            // dense-stage variant matrices follow in global memory (read via L1/L2)
   int32_t stage_begin, stage_end;  // range in the plan's stage array
 };
 
@@ -153,6 +161,8 @@ struct PlanOptions {
 int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual);
 void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOptions& o, bool reverse_for_adjoint,
                 Plan* plan);
+// FP64 FMAs per amplitude of pass i of a plan (dense stages 64, sequential ops by class).
+int pass_fma_per_amp(const Plan& plan, size_t i);
 
 // ---------------------------------------------------------------------------------------------
 // Kernel launchers (kernels.cu).

@@ -44,8 +44,8 @@ def test_plan_invariants(n, adjoint):
 def test_fusion_reduces_passes_for_c4():
     w = W.config("C4")
     fused = P.sv_plan_info(w.n, w.gates)
-    assert len(fused) <= 60, len(fused)          # 1780 gates in a few dozen HBM passes
-    assert all(p["k"] == 12 and p["low"] >= 3 for p in fused)
+    assert len(fused) <= 70, len(fused)          # 1780 gates in a few dozen HBM passes
+    assert all(p["k"] == 11 and p["low"] >= 3 for p in fused)
     assert sum(p["n_dense"] for p in fused) > 0.5 * sum(p["n_stages"] for p in fused)
 
 
