@@ -37,7 +37,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_TFLOPS = 36.9  # measured FP64 tensor (DMMA) peak = DMMA+DFMA mixed peak on this pool's B200
 # dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
 # --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
-TRAFFIC_PER_LAUNCH = {}
+TRAFFIC_PER_LAUNCH = {"C4": (17.183848 + 17.122593) * 1e9}  # profiles/r01_ncu_pass30_full.txt
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
 
@@ -101,7 +101,7 @@ def _ham_terms(ham):
     return len(ham)
 
 
-def cpu_oracle_sample(config: str, seconds_target: float = 15.0):
+def cpu_oracle_sample(config: str, seconds_target: float = 20.0):
     """The oracle as it stands, timed on the host cores on a bounded sample of the workload:
     the first G gates of the config's circuit at full width (n=30 for C4), G chosen to take about
     `seconds_target` seconds. Returns (gates/s, cores, sample description)."""

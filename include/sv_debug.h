@@ -38,6 +38,27 @@ sv_status sv_plan_info(int32_t n_qubits, const sv_gate* gates, int64_t n_gates, 
                        int32_t n_params, int32_t adjoint, int32_t tile_qubits, int32_t fusion, sv_pass_info* out,
                        int64_t cap, int64_t* n_passes);
 
+/* One step of a sharded schedule: kind 0 = segment of n_gates local gates (written to the
+ * local_gates output in order), kind 1 = swap of physical qubit positions gpos (global, >= n_local)
+ * and lpos (local): ranks r and r ^ 2^(gpos - n_local) exchange the halves of their shards whose
+ * local bit lpos differs from their own bit (gpos - n_local). */
+typedef struct {
+  int32_t kind;
+  int32_t gpos, lpos;
+  int32_t n_gates;
+} sv_shard_step;
+
+/* Host-only: the schedule sv_apply_circuit would run on a `world`-way sharded state starting from
+ * the identity layout, as seen by shard `rank`: segments of gates rewritten for that shard (global
+ * controls resolved, diagonal factors on global qubits folded) with explicit matrices (MAT1 /
+ * MAT2 kinds; mats: 32 doubles per gate, gate.mat points into local_mats), and swaps. final_perm
+ * (n entries) receives the logical -> physical layout at the end. Used by the world-size-2 gloo
+ * tests of the sharding logic on CPU. */
+sv_status sv_shard_plan(int32_t n_qubits, int32_t world, int32_t rank, const sv_gate* gates, int64_t n_gates,
+                        const double* params, int32_t n_params, sv_shard_step* steps, int64_t cap_steps,
+                        int64_t* n_steps, sv_gate* local_gates, double* local_mats, int64_t cap_gates,
+                        int64_t* n_local_gates, int32_t* final_perm);
+
 #ifdef __cplusplus
 }
 #endif

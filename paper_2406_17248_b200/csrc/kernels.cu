@@ -269,6 +269,31 @@ __global__ void __launch_bounds__(kThreads) k_pass(double2* __restrict__ psi, do
   }
 }
 
+
+// ---- sharding helpers: global <-> local qubit swaps ----
+// a[y0 | 2^l] <-> b[y0] for every y0 with bit l clear (virtual shards on one device).
+__global__ void k_swap_halves(double2* __restrict__ a, double2* __restrict__ b, int nl, int l) {
+  const int64_t half = 1ll << (nl - 1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < half; i += stride) {
+    const uint64_t y0 = insert_zero64((uint64_t)i, l);
+    const uint64_t y1 = y0 | (1ull << l);
+    const double2 t = a[y1];
+    a[y1] = b[y0];
+    b[y0] = t;
+  }
+}
+// dst[i] = src[insert(off + i, l, h)] for i < count (pack == 1), or the reverse (pack == 0).
+__global__ void k_pack_half(double2* __restrict__ shard, double2* __restrict__ buf, int l, int h, int64_t off,
+                            int64_t count, int pack) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint64_t y = insert_zero64((uint64_t)(off + i), l) | ((uint64_t)h << l);
+    if (pack) buf[i] = shard[y];
+    else shard[y] = buf[i];
+  }
+}
+
 __global__ void k_init(double2* psi, int64_t n, bool one) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -450,6 +475,27 @@ cudaError_t launch_pauli_group(const double* psi, double* lam, bool lam_accumula
 cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out, cudaStream_t s) {
   if (n_slots <= 0) return cudaSuccess;
   k_reduce_slots<<<n_slots, kThreads, 0, s>>>(d_partials, per_slot, d_out);
+  return cudaGetLastError();
+}
+
+static int elementwise_grid(int64_t n) {
+  int64_t blocks = (n + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  return (int)(blocks < 1 ? 1 : blocks);
+}
+
+cudaError_t launch_swap_halves(double* a, double* b, int nl, int l, cudaStream_t s) {
+  k_swap_halves<<<elementwise_grid(1ll << (nl - 1)), kThreads, 0, s>>>(reinterpret_cast<double2*>(a),
+                                                                        reinterpret_cast<double2*>(b), nl, l);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_half(double* shard, double* buf, int l, int h, int64_t off, int64_t count, bool pack,
+                             cudaStream_t s) {
+  k_pack_half<<<elementwise_grid(count), kThreads, 0, s>>>(reinterpret_cast<double2*>(shard),
+                                                             reinterpret_cast<double2*>(buf), l, h, off, count,
+                                                             pack ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -185,6 +185,11 @@ int pass_grid(int n_local, int k, bool dual);
 int plan_grid(const Plan& plan, int n_local);
 
 cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
+// Sharding: swap halves of two virtual shards (a[y0|2^l] <-> b[y0]); pack / unpack the half of a
+// shard with local bit l == h (elements off .. off+count of that half) to / from a buffer.
+cudaError_t launch_swap_halves(double* a, double* b, int nl, int l, cudaStream_t s);
+cudaError_t launch_pack_half(double* shard, double* buf, int l, int h, int64_t off, int64_t count, bool pack,
+                             cudaStream_t s);
 
 // Pauli groups (kernels.cu): terms sharing one x-mask.
 struct PauliGroupDev {
