@@ -53,6 +53,11 @@ class sv_pass_info(ctypes.Structure):
                 ("fma_per_amp", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
+class sv_shard_step(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("gpos", ctypes.c_int32), ("lpos", ctypes.c_int32),
+                ("n_gates", ctypes.c_int32)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} not built: run `python build.py` (or __graft_entry__.build()); "
@@ -81,6 +86,8 @@ def _load():
                                      ctypes.POINTER(f64), P],
         "sv_get_stats": [H, ctypes.POINTER(sv_stats)],
         "sv_reset_stats": [H],
+        "sv_shard_plan": [i32, i32, i32, ctypes.POINTER(sv_gate), i64, P, i32, ctypes.POINTER(sv_shard_step), i64,
+                          ctypes.POINTER(i64), ctypes.POINTER(sv_gate), P, i64, ctypes.POINTER(i64), P],
         "sv_plan_info": [i32, ctypes.POINTER(sv_gate), i64, P, i32, i32, i32, i32, ctypes.POINTER(sv_pass_info), i64,
                          ctypes.POINTER(i64)],
     }
@@ -285,6 +292,39 @@ def sv_plan_info(n_qubits: int, gates, params=None, adjoint: bool = False, tile_
     _check(lib.sv_plan_info(n_qubits, ga.arr, ga.n, _ptr(p), np_, int(adjoint), tile_qubits, int(fusion), out, cap,
                             ctypes.byref(npass)))
     return [{f: getattr(out[i], f) for f, _ in sv_pass_info._fields_} for i in range(min(npass.value, cap))]
+
+
+def sv_shard_plan(n_qubits: int, world: int, rank: int, gates, params=None):
+    """Host-only sharded schedule for `rank` (include/sv_debug.h): returns (steps, perm) where
+    steps are ("swap", gpos, lpos) or ("segment", [(matrix, targets, controls_mask), ...])."""
+    ga = gates if isinstance(gates, GateArray) else GateArray(gates)
+    p, np_ = _params(params)
+    cap_s, cap_g = 4 * ga.n + 16, 4 * ga.n + 16
+    steps = (sv_shard_step * cap_s)()
+    lg = (sv_gate * cap_g)()
+    mats = np.zeros(32 * cap_g)
+    ns, ng = ctypes.c_int64(), ctypes.c_int64()
+    perm = np.zeros(n_qubits, dtype=np.int32)
+    _check(lib.sv_shard_plan(n_qubits, world, rank, ga.arr, ga.n, _ptr(p), np_, steps, cap_s, ctypes.byref(ns), lg,
+                             _ptr(mats), cap_g, ctypes.byref(ng), _ptr(perm)))
+    out = []
+    gi = 0
+    for i in range(ns.value):
+        st = steps[i]
+        if st.kind == 1:
+            out.append(("swap", st.gpos, st.lpos))
+            continue
+        seg = []
+        for _ in range(st.n_gates):
+            g = lg[gi]
+            d = 2 if g.kind == KIND["MAT1"] else 4
+            m = mats[32 * gi: 32 * gi + 2 * d * d]
+            mat = (m[0::2] + 1j * m[1::2]).reshape(d, d)
+            targets = [g.targets[0]] + ([g.targets[1]] if d == 4 else [])
+            seg.append((mat, targets, int(g.controls)))
+            gi += 1
+        out.append(("segment", seg))
+    return out, [int(x) for x in perm]
 
 
 class StateVector:

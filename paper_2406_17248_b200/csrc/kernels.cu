@@ -355,6 +355,38 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
   if (threadIdx.x == 0) partials[blockIdx.x] = acc;
 }
 
+
+// Cross-shard Pauli group (sharding, x-mask wider than a shard): E partials of
+// sum_i conj(psi[i]) C(i) partner[i ^ xl], C(i) = sum_j c_j (-1)^{popc((i ^ xl) & z_j)}; the
+// partner's rank-bit signs are folded into c_j by the host. lam (optional) += C(i) partner[i ^ xl].
+__global__ void __launch_bounds__(kThreads) k_pauli_cross(const double2* __restrict__ psi,
+                                                          const double2* __restrict__ partner, double2* __restrict__ lam,
+                                                          int n, uint64_t xl, const uint64_t* __restrict__ z,
+                                                          const double2* __restrict__ c, int nterms,
+                                                          double* __restrict__ partials) {
+  __shared__ uint64_t s_z[256];
+  __shared__ double2 s_c[256];
+  __shared__ double s_red[kThreads / 32];
+  for (int i = threadIdx.x; i < nterms; i += blockDim.x) { s_z[i] = z[i]; s_c[i] = c[i]; }
+  __syncthreads();
+  const int64_t N = 1ll << n, stride = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+    const uint64_t ip = (uint64_t)i ^ xl;
+    double2 C = make_double2(0.0, 0.0);
+    for (int j = 0; j < nterms; ++j) {
+      const double sg = (__popcll(ip & s_z[j]) & 1) ? -1.0 : 1.0;
+      C.x = fma(sg, s_c[j].x, C.x);
+      C.y = fma(sg, s_c[j].y, C.y);
+    }
+    const double2 w = cmul(C, partner[ip]);
+    acc += re_conj_mul(psi[i], w);
+    if (lam) { double2 l = lam[i]; l.x += w.x; l.y += w.y; lam[i] = l; }
+  }
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
 // out[s] = sum_{j < per} partials[s*per + j], fixed order (strided per-thread sums, then a fixed tree).
 __global__ void __launch_bounds__(kThreads) k_reduce_slots(const double* __restrict__ partials, int per,
                                                            double* __restrict__ out) {
@@ -496,6 +528,15 @@ cudaError_t launch_pack_half(double* shard, double* buf, int l, int h, int64_t o
   k_pack_half<<<elementwise_grid(count), kThreads, 0, s>>>(reinterpret_cast<double2*>(shard),
                                                              reinterpret_cast<double2*>(buf), l, h, off, count,
                                                              pack ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int n_local, uint64_t xl,
+                               const uint64_t* d_z, const double* d_c, int nterms, double* d_partials, int grid,
+                               cudaStream_t s) {
+  k_pauli_cross<<<grid, kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<const double2*>(partner),
+                                          reinterpret_cast<double2*>(lam), n_local, xl, d_z,
+                                          reinterpret_cast<const double2*>(d_c), nterms, d_partials);
   return cudaGetLastError();
 }
 

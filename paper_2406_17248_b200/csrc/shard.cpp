@@ -453,20 +453,22 @@ static int sharded_groups(sv_state_s* h, const PauliGroups& G, std::vector<int>&
       int L = -1;
       for (int c = nl - 1; c >= 0; --c)
         if (!((xp >> c) & 1ull)) { L = c; break; }
-      if (L < 0) return fail(SV_E_ARG, "Pauli x-mask wider than a shard");
+      if (L < 0) break;  // X/Y support wider than a shard: cross-shard evaluation below
       int rc = swap_qubits(h, swap_vecs, Gpos, L);
       if (rc) return rc;
       do_swap_perm(perm, Gpos, L);
       if (swaps) swaps->push_back({Gpos, L});
       xp = permute_mask(G.xs[gi], perm);
     }
+    const uint64_t xg = xp >> nl;
     for (size_t a = 0; a < S.ranks.size(); ++a) {
       const uint64_t r = (uint64_t)S.ranks[a];
       std::vector<uint64_t> z;
       std::vector<double> c;
+      const uint64_t rsig = xg ? (r ^ xg) : r;  // cross-shard: signs of the partner's rank bits
       for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
         const uint64_t zp = permute_mask(G.z[t], perm);
-        const double sgn = (__builtin_popcountll((zp >> nl) & r) & 1) ? -1.0 : 1.0;
+        const double sgn = (__builtin_popcountll((zp >> nl) & rsig) & 1) ? -1.0 : 1.0;
         z.push_back(zp & lmask);
         c.push_back(sgn * G.c[2 * t]);
         c.push_back(sgn * G.c[2 * t + 1]);
@@ -479,10 +481,30 @@ static int sharded_groups(sv_state_s* h, const PauliGroups& G, std::vector<int>&
       cudaError_t e = cudaMemcpyAsync(h->d_terms.p, h->h_stage.data(), h->h_stage.size(), cudaMemcpyHostToDevice, h->stream);
       if (e != cudaSuccess) return cuda_fail(h, e, "terms");
       double* dp = static_cast<double*>(h->d_partials.p);
-      e = launch_pauli_group(psi[a], lam.empty() ? nullptr : lam[a], true, nl, xp,
-                             static_cast<const uint64_t*>(h->d_terms.p),
-                             reinterpret_cast<const double*>(static_cast<const char*>(h->d_terms.p) + zb), (int)z.size(), dp,
-                             grid, h->stream);
+      const uint64_t* dz = static_cast<const uint64_t*>(h->d_terms.p);
+      const double* dc = reinterpret_cast<const double*>(static_cast<const char*>(h->d_terms.p) + zb);
+      if (xg == 0) {
+        e = launch_pauli_group(psi[a], lam.empty() ? nullptr : lam[a], true, nl, xp, dz, dc, (int)z.size(), dp, grid,
+                               h->stream);
+      } else {
+        // partner shard r ^ xg: another virtual shard, or a full copy fetched over NCCL
+        const double* partner = nullptr;
+        if (S.virt) {
+          partner = psi[(size_t)(r ^ xg)];
+        } else {
+          const int peer = (int)(r ^ xg);
+          if (!S.recvb.ensure(size_t(16) << nl)) return fail(SV_E_OOM, "partner shard buffer");
+          ncclResult_t nr = ncclGroupStart();
+          if (nr == ncclSuccess) nr = ncclSend(psi[a], (size_t(2) << nl), ncclDouble, peer, S.comm, h->stream);
+          if (nr == ncclSuccess) nr = ncclRecv(S.recvb.p, (size_t(2) << nl), ncclDouble, peer, S.comm, h->stream);
+          ncclResult_t ne = ncclGroupEnd();
+          if (nr != ncclSuccess) return nccl_fail(h, nr, "partner exchange");
+          if (ne != ncclSuccess) return nccl_fail(h, ne, "partner exchange");
+          partner = static_cast<const double*>(S.recvb.p);
+        }
+        e = launch_pauli_cross(psi[a], partner, lam.empty() ? nullptr : lam[a], nl, xp & lmask, dz, dc, (int)z.size(), dp,
+                               grid, h->stream);
+      }
       if (e == cudaSuccess) e = launch_reduce_slots(dp, 1, grid, static_cast<double*>(h->d_out.p), h->stream);
       double v = 0;
       if (e == cudaSuccess) e = cudaMemcpyAsync(&v, h->d_out.p, 8, cudaMemcpyDeviceToHost, h->stream);
@@ -534,7 +556,7 @@ int shard_expectation_with_grad(sv_state_s* h, const std::vector<BoundGate>& bg,
   // 2. lambda = H psi, E (x-masks swapped local on psi first)
   double E = 0.0;
   std::vector<std::pair<int, int>> hswaps;
-  int rc = sharded_groups(h, G, perm, {psi}, psi, lam, &E, &hswaps);
+  int rc = sharded_groups(h, G, perm, {psi, lam}, psi, lam, &E, &hswaps);  // lambda follows every swap
   if (rc) return rc;
   // 3. undo the Hamiltonian swaps on (psi, lambda), then the forward schedule backwards
   for (auto it = hswaps.rbegin(); it != hswaps.rend(); ++it) {

@@ -200,6 +200,9 @@ cudaError_t launch_pauli_group(const double* psi, double* lam, bool lam_accumula
                                const uint64_t* d_z, const double* d_c /* complex coeff pairs */, int nterms,
                                double* d_partials, int grid, cudaStream_t s);
 int pauli_grid(int n_local);
+cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int n_local, uint64_t xl,
+                               const uint64_t* d_z, const double* d_c, int nterms, double* d_partials, int grid,
+                               cudaStream_t s);
 cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out,
                                 cudaStream_t s);
 
