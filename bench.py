@@ -14,8 +14,10 @@ C-ABI with host buffers, clocks during the timed region.
 --impl reference: the CPU oracle (oracle/, test infrastructure) timed on the host cores on a
 bounded sample of the same workload (the tier's reference arm).
 
-Multi-GPU (torchrun, N>1): replicas only for now — every rank runs the same 1-GPU step on its own
-GPU (no collective); scaling "weak". See DESIGN.md §Multi-GPU.
+Multi-GPU (torchrun, N>1): the state is sharded over the N GPUs by its top log2(N) qubits (NCCL
+exchanges over NVLink, all-reduced expectation). Weak scaling: n = 30 + log2(N) qubits (2^30
+amplitudes per GPU), value in 30q-equivalent gates/s (gates x 2^(n-30) / s). `--virtual-shards P`
+runs the same sharded executor with P shards on one GPU. See DESIGN.md §7.
 """
 from __future__ import annotations
 
@@ -161,6 +163,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
+    ap.add_argument("--virtual-shards", type=int, default=0,
+                    help="run the sharded path with P virtual shards on one GPU (tests the N>1 executor)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-grad", action="store_true")
     args = ap.parse_args()
@@ -169,6 +173,7 @@ def main():
 
     import torch
     import paper_2406_17248_b200 as P
+    import paper_2406_17248_b200.dist as PD
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -179,11 +184,27 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    w = W.config(args.config)
-    n = w.n
+    shards = world if world > 1 else max(1, args.virtual_shards)
+    if shards > 1:
+        # weak scaling (BASELINE configs[4] shape): C4's generator at
+        # n = 30 + log2(P) qubits, 2^30 amplitudes (16 GiB) per GPU, + 50-term JW H
+        g = shards.bit_length() - 1
+        n = 30 + g
+        w = W.random_circuit(n, 40, seed=3440)
+        w.ham = W.jw_hamiltonian(n, 50, 3440)
+        workload = f"C5w: {n}q random circuit depth 40 (Haar 1q + CZ bricks) + 50-term JW H, sharded over {shards}"
+    else:
+        w = W.config(args.config)
+        n = w.n
+        workload = args.config
     ga = P.GateArray(w.gates)
     pa = P.PauliArray(w.ham)
-    sv = P.StateVector(n)
+    if world > 1:
+        sv = PD.create_sharded(n)
+    elif shards > 1:
+        sv = P.StateVector(n, handle=P.sv_create_virtual_shards(n, shards))
+    else:
+        sv = P.StateVector(n)
     stream = torch.cuda.Stream()  # a real stream object: its handle is passed to the library
     torch.cuda.set_stream(stream)
     P.sv_set_stream(sv.h, stream.cuda_stream)
@@ -193,8 +214,7 @@ def main():
         P.sv_apply_circuit(sv.h, ga, w.params)
         return P.sv_expectation(sv.h, pa)
 
-    # warm-up (also builds the plan caches inside the library's allocator)
-    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist:
@@ -205,6 +225,8 @@ def main():
     evc1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         ev0.record(stream)
         E = None
         for i in range(args.steps):
@@ -215,33 +237,55 @@ def main():
             E = P.sv_expectation(sv.h, pa)
         ev1.record(stream)
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
     circ_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(evc0, evc1)]))
     st = P.sv_get_stats(sv.h)
     if dist:
-        t = torch.tensor([ms_total], device="cuda")
+        t = torch.tensor([ms_total, circ_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total, circ_ms = float(t[0].item()), float(t[1].item())
     ms_step = ms_total / args.steps
     n_gates = len(w.gates)
-    value = world * n_gates / (ms_step / 1e3)
-    passes = st["gate_passes"] // args.steps
+    amps_total = float(1 << n)
+    # 30q-equivalent gates/s: gates x (state size / 2^30) per second (= plain gates/s at N = 1)
+    value = n_gates * (amps_total / float(1 << 30)) / (ms_step / 1e3)
+    passes = st["gate_passes"] // args.steps // (1 if world > 1 else shards)
     hbm_peak, peak_src = _peaks()
-    amps = float(1 << n)
-    plan = P.sv_plan_info(n, ga, w.params)
-    fma_per_amp = sum(p["fma_per_amp"] for p in plan)
-    fp64_flops = 2.0 * fma_per_amp * amps  # algorithmic FP64 work of the executed plan
-    # effective SV bytes: what unfused single-gate sweeps would move: 32 B x 2^(n-c) per gate
-    eff_bytes = sum(32.0 * amps / (1 << len(g.controls)) for g in w.gates)
-    plan_bytes = st["algorithmic_bytes"] / args.steps
+    amps = amps_total / shards  # per GPU shard
     pass_ms = circ_ms / max(passes, 1)
     pass_bytes = 32.0 * amps
     achieved = pass_bytes / (pass_ms / 1e3) / 1e9
+    plan_bytes = st["algorithmic_bytes"] / args.steps / (1 if world > 1 else shards)
+    eff_bytes = sum(32.0 * amps_total / (1 << len(g.controls)) for g in w.gates)
+    roof = None
+    if shards == 1:
+        plan = P.sv_plan_info(n, ga, w.params)
+        fma_per_amp = sum(p["fma_per_amp"] for p in plan)
+        fp64_flops = 2.0 * fma_per_amp * amps  # algorithmic FP64 work of the executed plan
+        roof = {
+            "bound": "tensor", "kernel": "k_pass_reg<3,false> (fused forward tile pass: FP64 DMMA + DFMA stages)",
+            "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+            "peak_source": "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
+                           "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)",
+            "unit": "TFLOP/s", "frac": fp64_flops / passes / (pass_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+            "traffic": TRAFFIC_PER_LAUNCH.get(args.config),
+            "algorithmic_flops_per_launch": fp64_flops / passes, "avg_launch_ms": pass_ms,
+            "hbm": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src,
+                    "unit": "GB/s", "frac": achieved / hbm_peak, "algorithmic_bytes_per_launch": pass_bytes}}
+    else:
+        roof = {"bound": "hbm", "kernel": "k_pass_reg<3,false> on each shard", "achieved": achieved,
+                "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": None, "algorithmic_bytes_per_launch": pass_bytes, "avg_launch_ms": pass_ms,
+                "exchanges_per_step": st["exchanges"] / args.steps / (1 if world > 1 else 1)}
     clocks = clk.summary()
 
-    # e2e: same step through the public C-ABI with host inputs (gate / term arrays marshalled from
-    # host memory every step; plan upload H2D and the expectation D2H inside the timed region)
+    # e2e: the same step through the public C ABI with host inputs (gate / term arrays marshalled
+    # from host memory every step; plan upload H2D and the expectation D2H inside the timed region)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         ga_h = P.GateArray(w.gates)
@@ -251,28 +295,31 @@ def main():
         P.sv_expectation(sv.h, pa_h)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
     h2d = ga.nbytes + pa.nbytes + w.params.nbytes
-    e2e = {"value": world * n_gates / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": 8}
+    e2e = {"value": n_gates * (amps_total / float(1 << 30)) / e2e_s, "unit": "gates/s (30q-equivalent)",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8}
 
     grad = None
-    if not args.no_grad and args.config == "C4" and rank == 0:
+    if not args.no_grad and args.config == "C4" and shards == 1:
         wg = W.config("C4g")
         gag, pag = P.GateArray(wg.gates), P.PauliArray(wg.ham)
-        svg = sv  # same handle: psi0 = |0>
         sv.reset()
-        P.sv_expectation_with_grad(svg.h, gag, wg.params, pag)  # warm-up
+        P.sv_expectation_with_grad(sv.h, gag, wg.params, pag)  # warm-up
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         reps = 2
         for _ in range(reps):
-            Eg, gg = P.sv_expectation_with_grad(svg.h, gag, wg.params, pag)
+            Eg, gg = P.sv_expectation_with_grad(sv.h, gag, wg.params, pag)
         dtg = (time.perf_counter() - t0) / reps
         grad = {"workload": "C4g: 30q HEA 2 layers RY/RZ + CNOT ladder, 120 params, 50-term JW H",
                 "grad_evals_per_s": 1.0 / dtg, "ms_per_eval": 1e3 * dtg, "E": Eg}
 
     cpu = None
-    if not args.no_cpu_baseline and rank == 0 and world == 1:
+    if not args.no_cpu_baseline and rank == 0 and world == 1 and shards == 1:
         try:
             v, cores, sample = cpu_oracle_sample(args.config)
             cpu = {"value": v, "unit": "gates/s", "cores": cores, "kind": "oracle", "sample": sample}
@@ -283,26 +330,20 @@ def main():
     if rank == 0:
         line = {
             "metric": "gates/sec (30q random circuit C4 evolution + 50-term <H>), SV GB/s, grad evals/sec",
-            "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "value": value, "unit": "gates/s" if shards == 1 else "gates/s (30q-equivalent: gates x 2^(n-30))",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128 (f64)", "data": "synthetic",
-            "config": {"workload": args.config, "n_qubits": n, "gates": n_gates, "ham_terms": len(w.ham),
-                       "state_bytes": int(16 * amps), "l2": "inputs (16 GiB state) larger than L2; no flush",
-                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+            "config": {"workload": workload, "n_qubits": n, "gates": n_gates, "ham_terms": len(w.ham),
+                       "state_bytes": int(16 * amps_total), "shards": shards,
+                       "l2": "inputs (16 GiB per GPU) larger than L2; no flush",
+                       "parallelism": (f"state sharded over {world} GPUs (NCCL)" if world > 1 else
+                                       f"{shards} virtual shards on 1 GPU" if shards > 1 else "1 GPU")},
             "circuit_ms": circ_ms, "passes_per_circuit": passes, "E": E,
             "sv_effective_gbs": eff_bytes / (circ_ms / 1e3) / 1e9,
             "plan_hbm_gbs": plan_bytes / (ms_step / 1e3) / 1e9,
             "plan_hbm_frac": plan_bytes / (ms_step / 1e3) / 1e9 / hbm_peak,
-            "roofline": {
-                "bound": "tensor", "kernel": "k_pass_reg<3,false> (fused forward tile pass: FP64 DMMA + DFMA stages)",
-                "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
-                "peak_source": "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
-                               "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)",
-                "unit": "TFLOP/s", "frac": fp64_flops / passes / (pass_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
-                "traffic": TRAFFIC_PER_LAUNCH.get(args.config),
-                "algorithmic_flops_per_launch": fp64_flops / passes, "avg_launch_ms": pass_ms,
-                "hbm": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src,
-                        "unit": "GB/s", "frac": achieved / hbm_peak, "algorithmic_bytes_per_launch": pass_bytes}},
+            "roofline": roof,
             "grad": grad,
             "cpu_baseline": cpu,
             "e2e": e2e,

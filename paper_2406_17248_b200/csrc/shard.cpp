@@ -76,37 +76,63 @@ void do_swap_perm(std::vector<int>& perm, int G, int L) {
   }
 }
 
-// Splits a circuit into local segments and global<->local swaps, updating perm.
+// Splits a circuit into local segments and global<->local swaps, updating perm. Each segment takes
+// every pending gate that is local (non-diagonal targets on local positions) and may legally move
+// ahead of the gates left behind (same commutation rule as the pass planner), so a swap is only
+// issued when nothing else can run; the swapped-out local qubit is the one whose next
+// non-diagonal use lies furthest ahead (Belady).
 std::vector<Step> schedule(const std::vector<BoundGate>& gates, std::vector<int>& perm, int nl) {
   std::vector<Step> steps;
-  Step seg;
-  auto flush = [&]() {
-    if (!seg.gates.empty()) { steps.push_back(std::move(seg)); seg = Step(); }
-  };
-  for (const BoundGate& g : gates) {
-    BoundGate p = to_physical(g, perm);
-    if (nondiag(p)) {
-      for (int t = 0; t < 2; ++t) {
-        const int pos = t == 0 ? p.t0 : p.t1;
-        if (pos < nl) continue;
-        flush();
-        // local partner: the highest local position that is not a target of this gate (the top
-        // local bit keeps the exchanged half contiguous)
-        int L = -1;
-        for (int c = nl - 1; c >= 0; --c)
-          if (c != p.t0 && c != p.t1) { L = c; break; }
-        Step sw;
-        sw.kind = 1;
-        sw.gpos = pos;
-        sw.lpos = L;
-        steps.push_back(sw);
-        do_swap_perm(perm, pos, L);
-        p = to_physical(g, perm);
+  std::vector<int> pending(gates.size());
+  for (size_t i = 0; i < gates.size(); ++i) pending[i] = (int)i;
+  auto tmask = [](const BoundGate& g) { return (1ull << g.t0) | (g.t1 >= 0 ? (1ull << g.t1) : 0ull); };
+  while (!pending.empty()) {
+    Step seg;
+    std::vector<int> skipped;
+    uint64_t bN = 0, bA = 0;  // logical qubits
+    for (int gi : pending) {
+      const BoundGate& g = gates[(size_t)gi];
+      const uint64_t N = nondiag(g) ? tmask(g) : 0ull;
+      const uint64_t A = tmask(g) | g.controls;
+      bool ok = !(N & bA) && !(A & bN);
+      if (ok && N) {
+        const BoundGate p = to_physical(g, perm);
+        ok = p.t0 < nl && (p.t1 < 0 || p.t1 < nl);
       }
+      if (ok) seg.gates.push_back(to_physical(g, perm));
+      else { skipped.push_back(gi); bN |= N; bA |= A; }
     }
-    seg.gates.push_back(p);
+    if (!seg.gates.empty()) steps.push_back(std::move(seg));
+    pending.swap(skipped);
+    if (pending.empty()) break;
+    // the first pending gate is blocked only by global non-diagonal targets: swap them in
+    const BoundGate& g = gates[(size_t)pending[0]];
+    for (int t = 0; t < 2; ++t) {
+      const int q = t == 0 ? g.t0 : g.t1;
+      if (q < 0 || perm[(size_t)q] < nl) continue;
+      const int G = perm[(size_t)q];
+      int L = -1, best = -1;
+      for (int c = nl - 1; c >= 0; --c) {
+        const BoundGate p = to_physical(g, perm);
+        if (c == p.t0 || c == p.t1) continue;
+        int lq = -1;
+        for (size_t x = 0; x < perm.size(); ++x)
+          if (perm[x] == c) lq = (int)x;
+        int next = (int)pending.size();  // first pending gate using lq non-diagonally
+        for (size_t k = 0; k < pending.size(); ++k) {
+          const BoundGate& h = gates[(size_t)pending[k]];
+          if (nondiag(h) && ((tmask(h) >> lq) & 1ull)) { next = (int)k; break; }
+        }
+        if (next > best) { best = next; L = c; }
+      }
+      Step sw;
+      sw.kind = 1;
+      sw.gpos = G;
+      sw.lpos = L;
+      steps.push_back(sw);
+      do_swap_perm(perm, G, L);
+    }
   }
-  flush();
   return steps;
 }
 
