@@ -3,6 +3,7 @@
 // Every numerical step runs in kernels.cu; this file only validates, binds (gates.cpp), plans
 // (plan.cpp), uploads plan data and launches. Sharding (sv_create_sharded / virtual shards) lives
 // in shard.cpp.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -67,40 +68,77 @@ int bind_circuit(sv_state_s* h, const sv_gate* gates, int64_t n_gates, const dou
   return SV_OK;
 }
 
-// Uploads a plan's ops and matrices (stream-ordered: the copy runs after earlier kernels that read
-// the same buffers).
-int upload_plan(sv_state_s* h, const Plan& plan) {
-  // one buffer: [ops | stages | mats], each section 64-byte aligned; one H2D copy
+static uint64_t fnv1a(const void* data, size_t n, uint64_t h) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; ++i) { h ^= p[i]; h *= 1099511628211ull; }
+  return h;
+}
+
+void release_plan_cache(sv_state_s* h) {
+  for (CachedPlan* c : h->plan_cache) { c->buf.release(); delete c; }
+  h->plan_cache.clear();
+}
+
+int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, const CachedPlan** out) {
+  const int kCacheEntries = 8;
+  uint64_t key = 1469598103934665603ull;
+  key = fnv1a(gates.data(), gates.size() * sizeof(BoundGate), key);
+  const int meta[8] = {h->n_local, reverse ? 1 : 0, h->opts.tile_qubits, h->opts.low_qubits, h->opts.fusion ? 1 : 0,
+                       h->opts.kernel, h->opts.dense, (int)gates.size()};
+  key = fnv1a(meta, sizeof(meta), key);
+  for (CachedPlan* c : h->plan_cache)
+    if (c->key == key) {
+      c->stamp = ++h->plan_clock;
+      *out = c;
+      return SV_OK;
+    }
+  CachedPlan* c = nullptr;
+  if ((int)h->plan_cache.size() < kCacheEntries) {
+    c = new CachedPlan();
+    h->plan_cache.push_back(c);
+  } else {
+    c = *std::min_element(h->plan_cache.begin(), h->plan_cache.end(),
+                          [](const CachedPlan* x, const CachedPlan* y) { return x->stamp < y->stamp; });
+  }
+  c->key = 0;
+  build_plan(gates, h->n_local, h->opts, reverse, &c->plan);
+  // one buffer: [ops | stages | mats | rops], each section 64-byte aligned; one H2D copy
+  const Plan& plan = c->plan;
   auto al = [](size_t x) { return (x + 63) & ~size_t(63); };
   const size_t ob = plan.ops.size() * sizeof(DevOp), sb = plan.stages.size() * sizeof(StageDesc),
                mb = plan.mats.size() * sizeof(double), rb = plan.rops.size() * sizeof(RegOp);
   const size_t so = al(ob), mo = so + al(sb), ro = mo + al(mb), total = ro + al(rb);
-  if (!h->d_ops.ensure(total + 64)) return fail(SV_E_OOM, "plan buffers");
+  if (!c->buf.ensure(total + 64)) return fail(SV_E_OOM, "plan buffers");
   h->h_stage.assign(total, 0);
   std::memcpy(h->h_stage.data(), plan.ops.data(), ob);
   std::memcpy(h->h_stage.data() + so, plan.stages.data(), sb);
   std::memcpy(h->h_stage.data() + mo, plan.mats.data(), mb);
   std::memcpy(h->h_stage.data() + ro, plan.rops.data(), rb);
-  h->plan_stages_off = so;
-  h->plan_mats_off = mo;
-  h->plan_rops_off = ro;
+  c->so = so;
+  c->mo = mo;
+  c->ro = ro;
   cudaError_t e = cudaSuccess;
-  if (total) e = cudaMemcpyAsync(h->d_ops.p, h->h_stage.data(), total, cudaMemcpyHostToDevice, h->stream);
+  if (total) e = cudaMemcpyAsync(c->buf.p, h->h_stage.data(), total, cudaMemcpyHostToDevice, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "plan upload");
+  c->key = key;
+  c->stamp = ++h->plan_clock;
+  *out = c;
   return SV_OK;
 }
 
 // Runs all passes of a plan on psi (and lam for the adjoint plan).
-int run_plan(sv_state_s* h, const Plan& plan, double* psi, double* lam, double* d_partials, int grid) {
+int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, double* d_partials, int grid) {
+  const Plan& plan = cp.plan;
+  const char* base = static_cast<const char*>(cp.buf.p);
   for (size_t i = 0; i < plan.passes.size(); ++i) {
     const PassDesc& pd = plan.passes[i];
     const int next_mat = (i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size();
     PassLaunch L;
     L.pd = &pd;
-    L.d_ops = static_cast<const DevOp*>(h->d_ops.p);
-    L.d_stages = reinterpret_cast<const StageDesc*>(static_cast<const char*>(h->d_ops.p) + h->plan_stages_off);
-    L.d_mats = reinterpret_cast<const double*>(static_cast<const char*>(h->d_ops.p) + h->plan_mats_off);
-    L.d_rops = reinterpret_cast<const RegOp*>(static_cast<const char*>(h->d_ops.p) + h->plan_rops_off);
+    L.d_ops = reinterpret_cast<const DevOp*>(base);
+    L.d_stages = reinterpret_cast<const StageDesc*>(base + cp.so);
+    L.d_mats = reinterpret_cast<const double*>(base + cp.mo);
+    L.d_rops = reinterpret_cast<const RegOp*>(base + cp.ro);
     L.d_partials = d_partials;
     L.nmats = next_mat - pd.mat_begin;
     L.grid = grid > 0 ? grid : plan_grid(plan, h->n_local);
@@ -123,11 +161,10 @@ int run_plan(sv_state_s* h, const Plan& plan, double* psi, double* lam, double* 
 
 int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg) {
   if (bg.empty()) return SV_OK;
-  Plan plan;
-  build_plan(bg, h->n_local, h->opts, false, &plan);
-  int rc = upload_plan(h, plan);
+  const CachedPlan* cp = nullptr;
+  int rc = get_plan(h, bg, false, &cp);
   if (rc != SV_OK) return rc;
-  rc = run_plan(h, plan, h->psi, nullptr, nullptr, 0);
+  rc = run_plan(h, *cp, h->psi, nullptr, nullptr, 0);
   if (rc != SV_OK) return rc;
   h->stats.gates_applied += (int64_t)bg.size();
   return SV_OK;
@@ -229,6 +266,7 @@ sv_status sv_destroy(sv_handle h) {
   h->state.release();
   h->work_psi.release();
   h->work_lam.release();
+  release_plan_cache(h);
   h->d_ops.release();
   h->d_mats.release();
   h->d_terms.release();
@@ -387,13 +425,15 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   if (e != cudaSuccess) return cuda_fail(h, e, "copy psi0");
   h->stats.algorithmic_bytes += 2.0 * (double)bytes;
   // 1. forward
-  Plan fwd, rev;
-  build_plan(bg, h->n_local, h->opts, false, &fwd);
-  build_plan(bg, h->n_local, h->opts, true, &rev);
-  rc = upload_plan(h, fwd);
+  const CachedPlan* fwdp = nullptr;
+  const CachedPlan* revp = nullptr;
+  rc = get_plan(h, bg, false, &fwdp);
   if (rc) return rc;
-  rc = run_plan(h, fwd, psi, nullptr, nullptr, 0);
+  rc = run_plan(h, *fwdp, psi, nullptr, nullptr, 0);
   if (rc) return rc;
+  rc = get_plan(h, bg, true, &revp);
+  if (rc) return rc;
+  const Plan& rev = revp->plan;
   h->stats.gates_applied += (int64_t)bg.size();
   // 2. lambda = H psi, E partials
   const int pgrid = pauli_grid(h->n_local);
@@ -412,9 +452,7 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   }
   // 3. reverse sweep over (psi, lambda)
   if (!rev.passes.empty()) {
-    rc = upload_plan(h, rev);
-    if (rc) return rc;
-    rc = run_plan(h, rev, psi, lam, dp + ng * pgrid, agrid);
+    rc = run_plan(h, *revp, psi, lam, dp + ng * pgrid, agrid);
     if (rc) return rc;
   }
   // 4. reductions

@@ -216,6 +216,14 @@ void layout_sequential(StagePlan* sp, const PassDesc& pd, int R) {
 // ---------------------------------------------------------------- dense (FP64-MMA) stages
 
 constexpr int kDenseStride = 20;  // complex entries per row of a stored variant matrix
+// Dense-stage policy (tunable by environment for A/B runs): minimum sequential FP64 cost
+// (FMA/amp) worth a 64 FMA/amp dense stage, and the maximum number of variant bits.
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+const int g_dense_min_cost = env_int("SV_DENSE_MIN_COST", 20);
+const int g_dense_max_var = env_int("SV_DENSE_MAX_VAR", 6);
 
 // FP64 pipe cost per amplitude of an op applied sequentially (DFMA path), for the dense choice.
 int seq_cost(const DevOp& o, const double* m) {
@@ -308,8 +316,8 @@ void dense_apply(Cx* u, const DevOp& o, const double* m, const int* reg_new, uin
 bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles) {
   const int k = pd.k;
   const int nw_bits = k - 8;  // 2^(k-3) threads: 16 vectors of 16 amplitudes per warp
-  if (nw_bits < 1 || __builtin_popcount(sp->regset) != 4) return false;
-  const uint32_t regmask = sp->regset;
+  if (nw_bits < 1 || __builtin_popcount(sp->regset) > 4) return false;
+  uint32_t regmask = sp->regset;
   int cost = 0;
   uint32_t vt = 0;
   uint64_t vo = 0;
@@ -324,10 +332,14 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
         if (pos < 0) vo |= 1ull << (t ? o.qb : o.qa);
       }
   }
+  // pad the register set to 4 positions with non-variant positions (identity on them)
+  for (int p = k - 1; p >= 0 && __builtin_popcount(regmask) < 4; --p)
+    if (!((regmask >> p) & 1u) && !((vt >> p) & 1u)) regmask |= 1u << p;
+  if (__builtin_popcount(regmask) != 4) return false;
   const int m_tile = __builtin_popcount(vt), m_outer = __builtin_popcountll(vo);
   if (std::getenv("SV_PLAN_DEBUG"))
     std::fprintf(stderr, "stage: ops %d cost %d m_tile %d m_outer %d\n", (int)sp->ops.size(), cost, m_tile, m_outer);
-  if (cost < 20 || m_tile > nw_bits || m_tile + m_outer > 3) return false;
+  if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > g_dense_max_var) return false;
   const int nvar = 1 << (m_tile + m_outer);
   const size_t per = 2 * 16 * kDenseStride;
   const size_t used = plan->mats.size() - pd.mat_begin;
@@ -404,10 +416,10 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
   S.dense = 1;
   S.m_tile = (uint8_t)m_tile;
   S.m_outer = (uint8_t)m_outer;
-  for (int b = 0; b < 3; ++b) S.var_outer[b] = (int8_t)(b < m_outer ? olist[b] : -1);
+  for (int b = 0; b < 8; ++b) S.var_outer[b] = (int8_t)(b < m_outer ? olist[b] : -1);
   for (int r = 0; r < 4; ++r) S.regpos[r] = (int8_t)newreg[r];
   for (int b = 0; b < 12; ++b) S.thrpos[b] = (int8_t)(b < (int)order.size() ? order[b] : -1);
-  S.dense_off = (uint16_t)(off / 2);
+  S.dense_off = (uint32_t)(off / 2);
   const uint32_t p2 = 1u << newreg[2], p3 = 1u << newreg[3], n0 = 1u << order[3], bc0 = 1u << c0;
   const uint32_t p0 = 1u << newreg[0], p1 = 1u << newreg[1], bc1 = 1u << c1, bc2 = 1u << c2;
   for (int w = 0; w < 8; ++w) {
@@ -449,7 +461,7 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense) {
   pd->seq_mats = (int32_t)(plan->mats.size() - pd->mat_begin);
   if (forward && dense && k >= 9) {
     const size_t budget = size_t(1) << 22;  // variant matrices live in global memory (L2-resident)
-    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(3, k - 8), 3);
+    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(3, k - 8), g_dense_max_var);
     for (StagePlan& sp : st4) {
       if (make_dense(&sp, *pd, plan, budget)) final_stages.push_back(std::move(sp));
       else add_sequential(split_stages(sp.ops, *pd, pd->R, -1, -1));

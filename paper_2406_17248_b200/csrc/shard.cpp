@@ -300,11 +300,10 @@ int run_segment(sv_state_s* h, const std::vector<BoundGate>& phys, const std::ve
   for (size_t a = 0; a < S.ranks.size(); ++a) {
     std::vector<BoundGate> loc = localize(phys, h->n_local, (uint64_t)S.ranks[a]);
     if (loc.empty()) continue;
-    Plan plan;
-    build_plan(loc, h->n_local, h->opts, false, &plan);
-    int rc = upload_plan(h, plan);
+    const CachedPlan* cp = nullptr;
+    int rc = get_plan(h, loc, false, &cp);
     if (rc) return rc;
-    rc = run_plan(h, plan, vec[a], nullptr, nullptr, 0);
+    rc = run_plan(h, *cp, vec[a], nullptr, nullptr, 0);
     if (rc) return rc;
   }
   return SV_OK;
@@ -599,14 +598,14 @@ int shard_expectation_with_grad(sv_state_s* h, const std::vector<BoundGate>& bg,
     for (size_t a = 0; a < S.ranks.size(); ++a) {
       std::vector<BoundGate> loc = localize(it->gates, nl, (uint64_t)S.ranks[a]);
       if (loc.empty()) continue;
-      Plan rev;
-      build_plan(loc, nl, h->opts, true, &rev);
+      const CachedPlan* revp = nullptr;
+      rc = get_plan(h, loc, true, &revp);
+      if (rc) return rc;
+      const Plan& rev = revp->plan;
       const int agrid = plan_grid(rev, nl);
       const size_t ns = (size_t)rev.n_grad_slots;
       if (!h->d_partials.ensure(ns * agrid * 8 + 8) || !h->d_out.ensure(ns * 8 + 8)) return fail(SV_E_OOM, "partials");
-      rc = upload_plan(h, rev);
-      if (rc) return rc;
-      rc = run_plan(h, rev, psi[a], lam[a], static_cast<double*>(h->d_partials.p), agrid);
+      rc = run_plan(h, *revp, psi[a], lam[a], static_cast<double*>(h->d_partials.p), agrid);
       if (rc) return rc;
       if (ns) {
         std::vector<double> hv(ns);

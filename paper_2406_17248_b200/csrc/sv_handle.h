@@ -19,6 +19,17 @@ struct DevBuf {
 
 struct ShardState;  // shard.cpp
 
+// A built plan and its device copy ([ops | stages | mats | rops], one upload). Plans are cached
+// per handle by a hash of the bound gates and the options, so re-applying the same circuit (a
+// benchmark loop, a repeated evaluation) skips planning and the upload.
+struct CachedPlan {
+  uint64_t key = 0;
+  uint64_t stamp = 0;
+  Plan plan;
+  DevBuf buf;
+  size_t so = 0, mo = 0, ro = 0;
+};
+
 }  // namespace sv
 
 struct sv_state_s {
@@ -33,7 +44,8 @@ struct sv_state_s {
   double* psi = nullptr;
   sv::DevBuf d_ops, d_mats, d_terms, d_partials, d_out;
   std::vector<char> h_stage;
-  size_t plan_stages_off = 0, plan_mats_off = 0, plan_rops_off = 0;
+  std::vector<sv::CachedPlan*> plan_cache;  // owned, LRU (small)
+  uint64_t plan_clock = 0;
   sv::PlanOptions opts;
   sv_stats stats{};
   sv::ShardState* shard = nullptr;
@@ -44,8 +56,10 @@ namespace sv {
 int fail(int code, const std::string& msg);
 int cuda_fail(sv_state_s* h, cudaError_t e, const char* where);
 int check_handle(sv_state_s* h);
-int upload_plan(sv_state_s* h, const Plan& plan);
-int run_plan(sv_state_s* h, const Plan& plan, double* psi, double* lam, double* d_partials, int grid);
+// Returns the (cached or freshly built and uploaded) plan of `gates` (local physical qubits).
+int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, const CachedPlan** out);
+int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, double* d_partials, int grid);
+void release_plan_cache(sv_state_s* h);
 int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg);
 
 struct PauliGroups {

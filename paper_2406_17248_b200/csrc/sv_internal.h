@@ -71,14 +71,15 @@ struct StageDesc {
   uint8_t dense;             // 1: dense MMA stage
   uint8_t m_tile;            // variant bits on warp positions (thrpos[4 .. 4+m_tile))
   uint8_t m_outer;           // variant bits on outer qubits (var_outer[0 .. m_outer))
-  int8_t var_outer[3];
-  uint16_t dense_off;        // dense: first variant matrix (double2 units in the pass' matrix block)
+  uint8_t pad0;
+  int8_t var_outer[8];
+  uint32_t dense_off;        // dense: first variant matrix (double2 units in the pass' matrix block)
   uint16_t warp_swz[8];      // dense: swz(tile-position bits of warp w)
   uint8_t warp_var[8];       // dense: tile-variant index of warp w
   uint16_t lane_b[32];       // dense: swz(lane part of the B-fragment load address)
   uint16_t lane_d[32];       // dense: swz(lane part of the D-fragment store address)
 };
-static_assert(sizeof(StageDesc) == 216, "StageDesc layout");
+static_assert(sizeof(StageDesc) == 224, "StageDesc layout");
 
 
 // Compact op of the register kernel (32 bytes: two 16-byte shared loads per op).
