@@ -204,25 +204,120 @@ int group_terms(sv_state_s* h, const sv_pauli* terms, int64_t n_terms, PauliGrou
 
 // Launches one Pauli-group pass per group over psi; lam (optional) receives H psi.
 // Writes per-CTA partials of group g to d_partials[g * grid ...].
-int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid) {
-  const size_t zb = (G.z.size() * 8 + 15) & ~size_t(15), cb = G.c.size() * 8;  // complex coeffs 16-B aligned
+int pauli_k(int n_local) { return std::min(n_local, 12); }
+
+// Tiled evaluation of all Pauli groups: groups whose x-masks fit together in one 2^k tile (low
+// qubits + the x bits) share one pass (k_pauli_tile). Writes one partial slot (grid doubles) per
+// pass; *nslots receives the pass count. lam (optional) receives H psi.
+int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
+               int* nslots) {
+  const int nl = h->n_local;
+  const int k = pauli_k(nl);
+  const int L = std::min(3, k);
+  const uint64_t lowmask = (1ull << L) - 1;
+  std::vector<int> order(G.xs.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    return __builtin_popcountll(G.xs[x]) > __builtin_popcountll(G.xs[y]);
+  });
+  std::vector<PauliPassDesc> passes;
+  std::vector<uint64_t> z_all;
+  std::vector<double> c_all;
+  std::vector<int> remaining, wide;  // wide: x-mask does not fit a tile -> per-group pair kernel
+  for (int gi : order) {
+    if (__builtin_popcountll(lowmask | G.xs[gi]) <= k) remaining.push_back(gi);
+    else wide.push_back(gi);
+  }
+  while (!remaining.empty()) {
+    PauliPassDesc pp;
+    std::memset(&pp, 0, sizeof(pp));
+    uint64_t T = lowmask;
+    std::vector<int> taken, rest;
+    int nterms = 0;
+    for (int gi : remaining) {
+      const int nt = G.end[gi] - G.begin[gi];
+      if ((int)taken.size() < 32 && __builtin_popcountll(T | G.xs[gi]) <= k && nterms + nt <= 1024) {
+        T |= G.xs[gi];
+        taken.push_back(gi);
+        nterms += nt;
+      } else {
+        rest.push_back(gi);
+      }
+    }
+    for (int q = 0; q < nl && __builtin_popcountll(T) < k; ++q) T |= 1ull << q;
+    pp.k = k;
+    int low = 0;
+    while (low < k && ((T >> low) & 1ull)) ++low;
+    pp.low = low;
+    int pos_of[64];
+    for (int q = 0, p = 0; q < nl; ++q)
+      if ((T >> q) & 1ull) { pp.tq[p] = (int8_t)q; pos_of[q] = p++; }
+    pp.term_base = (int)z_all.size();
+    for (int gi : taken) {
+      const int g = pp.ngroups++;
+      pp.xphys[g] = G.xs[gi];
+      uint32_t xt = 0;
+      for (int q = 0; q < nl; ++q)
+        if ((G.xs[gi] >> q) & 1ull) xt |= 1u << pos_of[q];
+      pp.xtile[g] = xt;
+      pp.tbeg[g] = (int)z_all.size() - pp.term_base;
+      for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
+        z_all.push_back(G.z[t]);
+        c_all.push_back(G.c[2 * t]);
+        c_all.push_back(G.c[2 * t + 1]);
+      }
+      pp.tend[g] = (int)z_all.size() - pp.term_base;
+    }
+    pp.nterms = (int)z_all.size() - pp.term_base;
+    passes.push_back(pp);
+    remaining.swap(rest);
+  }
+  // wide groups' terms follow the passes' terms
+  std::vector<int> wide_base;
+  for (int gi : wide) {
+    wide_base.push_back((int)z_all.size());
+    for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
+      z_all.push_back(G.z[t]);
+      c_all.push_back(G.c[2 * t]);
+      c_all.push_back(G.c[2 * t + 1]);
+    }
+  }
+  const size_t zb = (z_all.size() * 8 + 15) & ~size_t(15), cb = c_all.size() * 8;
   if (!h->d_terms.ensure(zb + cb + 16)) return fail(SV_E_OOM, "term buffers");
-  h->h_stage.resize(zb + cb + 16);
-  std::memcpy(h->h_stage.data(), G.z.data(), G.z.size() * 8);
-  std::memcpy(h->h_stage.data() + zb, G.c.data(), cb);
+  h->h_stage.assign(zb + cb + 16, 0);
+  std::memcpy(h->h_stage.data(), z_all.data(), z_all.size() * 8);
+  std::memcpy(h->h_stage.data() + zb, c_all.data(), cb);
   cudaError_t e = cudaMemcpyAsync(h->d_terms.p, h->h_stage.data(), zb + cb, cudaMemcpyHostToDevice, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "term upload");
   const uint64_t* dz = static_cast<const uint64_t*>(h->d_terms.p);
   const double* dc = reinterpret_cast<const double*>(static_cast<const char*>(h->d_terms.p) + zb);
-  const double amps = (double)(1ull << h->n_local);
-  for (size_t gi = 0; gi < G.xs.size(); ++gi) {
-    e = launch_pauli_group(psi, lam, gi > 0, h->n_local, G.xs[gi], dz + G.begin[gi], dc + 2 * G.begin[gi],
-                           G.end[gi] - G.begin[gi], d_partials + gi * (size_t)grid, grid, h->stream);
-    if (e != cudaSuccess) return cuda_fail(h, e, "pauli group launch");
+  const double amps = (double)(1ull << nl);
+  int slot = 0;
+  for (size_t p = 0; p < passes.size(); ++p, ++slot) {
+    const int mode = lam == nullptr ? 0 : (slot == 0 ? 1 : 2);
+    e = launch_pauli_tile(psi, lam, mode, nl, passes[p], dz, dc, d_partials + (size_t)slot * grid, grid, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "pauli pass launch");
     h->stats.kernel_launches += 1;
     h->stats.expectation_passes += 1;
-    h->stats.algorithmic_bytes += (lam == nullptr ? 16.0 : (gi == 0 ? 32.0 : 48.0)) * amps;
+    h->stats.algorithmic_bytes += (mode == 0 ? 16.0 : (mode == 1 ? 32.0 : 48.0)) * amps;
   }
+  for (size_t w = 0; w < wide.size(); ++w, ++slot) {
+    const int gi = wide[w];
+    const int nt = G.end[gi] - G.begin[gi];
+    // the pair kernel writes lambda when it is the first launch, else accumulates
+    e = launch_pauli_group(psi, lam, slot > 0, nl, G.xs[gi], dz + wide_base[w], dc + 2 * wide_base[w], nt,
+                           d_partials + (size_t)slot * grid, std::min(grid, pauli_grid(nl)), h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "pauli group launch");
+    if (pauli_grid(nl) < grid) {  // zero the unused tail of this slot (fixed-width reduction)
+      e = cudaMemsetAsync(d_partials + (size_t)slot * grid + pauli_grid(nl), 0, (size_t)(grid - pauli_grid(nl)) * 8,
+                          h->stream);
+      if (e != cudaSuccess) return cuda_fail(h, e, "partials");
+    }
+    h->stats.kernel_launches += 1;
+    h->stats.expectation_passes += 1;
+    h->stats.algorithmic_bytes += (lam == nullptr ? 16.0 : (slot == 0 ? 32.0 : 48.0)) * amps;
+  }
+  *nslots = slot;
   return SV_OK;
 }
 
@@ -385,17 +480,19 @@ sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, do
   if (h->world > 1) return shard_expectation(h, G, out_value);
   *out_value = 0.0;
   if (G.xs.empty()) return SV_OK;
-  const int grid = pauli_grid(h->n_local);
+  const int grid = pauli_tile_grid(h->n_local, pauli_k(h->n_local));
   const size_t ng = G.xs.size();
   if (!h->d_partials.ensure(ng * grid * 8) || !h->d_out.ensure(ng * 8)) return fail(SV_E_OOM, "partials");
   double* dp = static_cast<double*>(h->d_partials.p);
-  rc = run_groups(h, G, h->psi, nullptr, dp, grid);
+  int nslots = 0;
+  rc = run_groups(h, G, h->psi, nullptr, dp, grid, &nslots);
   if (rc) return rc;
-  cudaError_t e = launch_reduce_slots(dp, (int)ng, grid, static_cast<double*>(h->d_out.p), h->stream);
+  const size_t ns_e = (size_t)nslots;
+  cudaError_t e = launch_reduce_slots(dp, (int)ns_e, grid, static_cast<double*>(h->d_out.p), h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "reduce");
   h->stats.kernel_launches += 1;
-  std::vector<double> gv(ng);
-  e = cudaMemcpyAsync(gv.data(), h->d_out.p, ng * 8, cudaMemcpyDeviceToHost, h->stream);
+  std::vector<double> gv(ns_e);
+  e = cudaMemcpyAsync(gv.data(), h->d_out.p, ns_e * 8, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "expectation");
   double E = 0.0;
@@ -436,18 +533,19 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   const Plan& rev = revp->plan;
   h->stats.gates_applied += (int64_t)bg.size();
   // 2. lambda = H psi, E partials
-  const int pgrid = pauli_grid(h->n_local);
+  const int pgrid = pauli_tile_grid(h->n_local, pauli_k(h->n_local));
   const size_t ng = G.xs.size();
   const int agrid = plan_grid(rev, h->n_local);
   const size_t ns = (size_t)rev.n_grad_slots;
   const size_t part_doubles = ng * pgrid + ns * agrid;
   if (!h->d_partials.ensure(part_doubles * 8 + 8) || !h->d_out.ensure((ng + ns) * 8 + 8)) return fail(SV_E_OOM, "partials");
   double* dp = static_cast<double*>(h->d_partials.p);
+  int nslots = 0;
   if (ng == 0) {
     e = cudaMemsetAsync(lam, 0, bytes, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "zero lambda");
   } else {
-    rc = run_groups(h, G, psi, lam, dp, pgrid);
+    rc = run_groups(h, G, psi, lam, dp, pgrid, &nslots);
     if (rc) return rc;
   }
   // 3. reverse sweep over (psi, lambda)
@@ -457,7 +555,7 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   }
   // 4. reductions
   double* dout = static_cast<double*>(h->d_out.p);
-  e = launch_reduce_slots(dp, (int)ng, pgrid, dout, h->stream);
+  e = launch_reduce_slots(dp, nslots, pgrid, dout, h->stream);
   if (e == cudaSuccess && ns) e = launch_reduce_slots(dp + ng * pgrid, (int)ns, agrid, dout + ng, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "reduce");
   h->stats.kernel_launches += (ng ? 1 : 0) + (ns ? 1 : 0);
@@ -468,7 +566,7 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
     if (e != cudaSuccess) return cuda_fail(h, e, "gradient readback");
   }
   double E = 0.0;
-  for (size_t g = 0; g < ng; ++g) E += hv[g];
+  for (int g = 0; g < nslots; ++g) E += hv[(size_t)g];
   *out_value = E;
   for (int32_t p = 0; p < n_params; ++p) out_grad[p] = 0.0;
   // chain rule, in reverse-sweep slot order (fixed): g[p] += coeff_k * 2 Re d_k

@@ -15,6 +15,7 @@
 // Gate classes follow the paper (§3.1): X-like (anti-diagonal, "swap with scaling"),
 // Z-like (diagonal, "no pairing"), general 2x2 pairs, two-qubit quads.
 #include <cstdint>
+#include <cstring>
 
 #include "cx.cuh"
 #include "sv_internal.h"
@@ -387,6 +388,75 @@ __global__ void __launch_bounds__(kThreads) k_pauli_cross(const double2* __restr
   if (threadIdx.x == 0) partials[blockIdx.x] = acc;
 }
 
+
+// ---- tiled multi-group Pauli pass (a4 / a5) ----
+// One CTA loads a tile of 2^k amplitudes whose qubit set contains the x-masks of up to 32 Pauli
+// groups; every element evaluates all those groups from the on-chip tile: one HBM read of psi (and
+// one write / read-modify-write of lambda) for many groups instead of one pass per group.
+struct PauliTileArgs {
+  int32_t k, low, n_outer, ngroups, nterms, mode;  // mode 0: E only, 1: lam = H psi, 2: lam += H psi
+  int8_t tq[16];
+  int8_t oq[64];
+  int64_t ntiles;
+  uint64_t xphys[32];
+  uint32_t xtile[32];
+  int32_t tbeg[32], tend[32];
+  const uint64_t* z;
+  const double2* c;
+  double* partials;
+};
+
+__global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restrict__ psi, double2* __restrict__ lam,
+                                                         PauliTileArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t N = 1u << a.k;
+  double2* tp = reinterpret_cast<double2*>(smem_raw);
+  double2* s_c = tp + N;
+  uint64_t* s_z = reinterpret_cast<uint64_t*>(s_c + a.nterms);
+  const int nhi = 1 << (a.k - a.low);
+  uint64_t* s_hi = s_z + a.nterms;
+  __shared__ double s_red[kThreads / 32];
+  for (int i = threadIdx.x; i < a.nterms; i += blockDim.x) { s_z[i] = a.z[i]; s_c[i] = a.c[i]; }
+  for (int h = threadIdx.x; h < nhi; h += blockDim.x) {
+    uint64_t off = 0;
+    for (int b = 0; b < a.k - a.low; ++b)
+      if ((h >> b) & 1) off |= 1ull << a.tq[a.low + b];
+    s_hi[h] = off;
+  }
+  const uint32_t lowmask = (1u << a.low) - 1u;
+  double acc = 0.0;
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    uint64_t base = 0;
+    for (int j = 0; j < a.n_outer; ++j)
+      if ((tile >> j) & 1) base |= 1ull << a.oq[j];
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) tp[e] = psi[base | (e & lowmask) | s_hi[e >> a.low]];
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+      const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
+      const double2 v = tp[e];
+      double2 l = make_double2(0.0, 0.0);
+      for (int g = 0; g < a.ngroups; ++g) {
+        const uint64_t ip = gi ^ a.xphys[g];
+        double2 C = make_double2(0.0, 0.0);
+        for (int t = a.tbeg[g]; t < a.tend[g]; ++t) {
+          const double sg = (__popcll(ip & s_z[t]) & 1) ? -1.0 : 1.0;
+          C.x = fma(sg, s_c[t].x, C.x);
+          C.y = fma(sg, s_c[t].y, C.y);
+        }
+        const double2 w = cmul(C, tp[e ^ a.xtile[g]]);
+        l.x += w.x;
+        l.y += w.y;
+      }
+      acc += re_conj_mul(v, l);
+      if (a.mode == 1) lam[gi] = l;
+      else if (a.mode == 2) { double2 o = lam[gi]; o.x += l.x; o.y += l.y; lam[gi] = o; }
+    }
+  }
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) a.partials[blockIdx.x] = acc;
+}
+
 // out[s] = sum_{j < per} partials[s*per + j], fixed order (strided per-thread sums, then a fixed tree).
 __global__ void __launch_bounds__(kThreads) k_reduce_slots(const double* __restrict__ partials, int per,
                                                            double* __restrict__ out) {
@@ -537,6 +607,48 @@ cudaError_t launch_pauli_cross(const double* psi, const double* partner, double*
   k_pauli_cross<<<grid, kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<const double2*>(partner),
                                           reinterpret_cast<double2*>(lam), n_local, xl, d_z,
                                           reinterpret_cast<const double2*>(d_c), nterms, d_partials);
+  return cudaGetLastError();
+}
+
+int pauli_tile_grid(int n_local, int k) {
+  const int64_t ntiles = 1ll << (n_local - k);
+  const int64_t want = (int64_t)num_sms() * 3;
+  return (int)(ntiles < want ? ntiles : want);
+}
+
+cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_local, const PauliPassDesc& pp,
+                              const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s) {
+  PauliTileArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.k = pp.k;
+  a.low = pp.low;
+  a.ngroups = pp.ngroups;
+  a.nterms = pp.nterms;
+  a.mode = mode;
+  for (int i = 0; i < 16; ++i) a.tq[i] = pp.tq[i];
+  uint64_t tmask = 0;
+  for (int p = 0; p < pp.k; ++p) tmask |= 1ull << pp.tq[p];
+  a.n_outer = 0;
+  for (int q = 0; q < n_local; ++q)
+    if (!((tmask >> q) & 1ull)) a.oq[a.n_outer++] = (int8_t)q;
+  a.ntiles = 1ll << (n_local - pp.k);
+  for (int g = 0; g < pp.ngroups; ++g) {
+    a.xphys[g] = pp.xphys[g];
+    a.xtile[g] = pp.xtile[g];
+    a.tbeg[g] = pp.tbeg[g];
+    a.tend[g] = pp.tend[g];
+  }
+  a.z = d_z + pp.term_base;
+  a.c = reinterpret_cast<const double2*>(d_c) + pp.term_base;
+  a.partials = d_partials;
+  const size_t smem = (size_t(16) << pp.k) + (size_t)pp.nterms * 24 + (size_t(8) << (pp.k - pp.low));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_pauli_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_pauli_tile<<<grid, kThreads, smem, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<double2*>(lam), a);
   return cudaGetLastError();
 }
 

@@ -68,7 +68,9 @@ struct PauliGroups {
   std::vector<uint64_t> z;
   std::vector<double> c;              // complex coefficients c_t * i^{popc(x&z)} (re, im)
 };
-int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid);
+int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
+               int* nslots);
+int pauli_k(int n_local);
 
 // shard.cpp
 void destroy_sharding(sv_state_s* h);

@@ -201,6 +201,18 @@ cudaError_t launch_pauli_group(const double* psi, double* lam, bool lam_accumula
                                const uint64_t* d_z, const double* d_c /* complex coeff pairs */, int nterms,
                                double* d_partials, int grid, cudaStream_t s);
 int pauli_grid(int n_local);
+// A tiled multi-group Pauli pass: tile positions tq (physical qubits), groups with x-masks inside
+// the tile; term arrays (z, complex c) of its groups are contiguous from term_base.
+struct PauliPassDesc {
+  int32_t k, low, ngroups, nterms, term_base;
+  int8_t tq[16];
+  uint64_t xphys[32];
+  uint32_t xtile[32];
+  int32_t tbeg[32], tend[32];  // relative to term_base
+};
+int pauli_tile_grid(int n_local, int k);
+cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_local, const PauliPassDesc& pp,
+                              const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s);
 cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int n_local, uint64_t xl,
                                const uint64_t* d_z, const double* d_c, int nterms, double* d_partials, int grid,
                                cudaStream_t s);
