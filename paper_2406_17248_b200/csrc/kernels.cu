@@ -408,15 +408,31 @@ struct PauliTileArgs {
 
 __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restrict__ psi, double2* __restrict__ lam,
                                                          PauliTileArgs a) {
+  // Per tile the rank / outer-bit part of every term's sign is folded into its coefficient; per
+  // element only the tile bits remain: sign_t(e) = (-1)^{popc(e & zt_t)} with zt_t the term's Z
+  // support in tile-position space. Loops run term-outer / element-inner (EPT elements per thread
+  // in registers) so each term's data is read once per thread per tile and the element updates are
+  // independent (ILP).
+  constexpr int EPT = 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
-  double2* tp = reinterpret_cast<double2*>(smem_raw);
-  double2* s_c = tp + N;
-  uint64_t* s_z = reinterpret_cast<uint64_t*>(s_c + a.nterms);
+  double2* tile_buf = reinterpret_cast<double2*>(smem_raw);  // two tiles
+  double2* s_c = tile_buf + 2 * N;                         // folded coefficients (per tile)
+  uint64_t* s_z = reinterpret_cast<uint64_t*>(s_c + a.nterms);  // physical Z masks
+  uint32_t* s_zt = reinterpret_cast<uint32_t*>(s_z + a.nterms); // tile-position Z masks
   const int nhi = 1 << (a.k - a.low);
-  uint64_t* s_hi = s_z + a.nterms;
+  uint64_t* s_hi = reinterpret_cast<uint64_t*>(s_zt + ((a.nterms + 1) & ~1));
   __shared__ double s_red[kThreads / 32];
-  for (int i = threadIdx.x; i < a.nterms; i += blockDim.x) { s_z[i] = a.z[i]; s_c[i] = a.c[i]; }
+  uint64_t tmask = 0;
+  for (int p = 0; p < a.k; ++p) tmask |= 1ull << a.tq[p];
+  for (int i = threadIdx.x; i < a.nterms; i += blockDim.x) {
+    const uint64_t z = a.z[i];
+    s_z[i] = z;
+    uint32_t zt = 0;
+    for (int p = 0; p < a.k; ++p)
+      if ((z >> a.tq[p]) & 1ull) zt |= 1u << p;
+    s_zt[i] = zt;
+  }
   for (int h = threadIdx.x; h < nhi; h += blockDim.x) {
     uint64_t off = 0;
     for (int b = 0; b < a.k - a.low; ++b)
@@ -424,33 +440,105 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
     s_hi[h] = off;
   }
   const uint32_t lowmask = (1u << a.low) - 1u;
+  const int per_thread = (int)(N / blockDim.x);  // == EPT for 2^12-amplitude tiles, else smaller
   double acc = 0.0;
-  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+  // double-buffered tiles: cp.async streams tile i + gridDim.x while tile i is evaluated
+  auto tile_base = [&](int64_t tile) {
     uint64_t base = 0;
     for (int j = 0; j < a.n_outer; ++j)
       if ((tile >> j) & 1) base |= 1ull << a.oq[j];
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) tp[e] = psi[base | (e & lowmask) | s_hi[e >> a.low]];
-    __syncthreads();
+    return base;
+  };
+  auto issue = [&](int64_t tile, double2* dst) {
+    const uint64_t base = tile_base(tile);
     for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
-      const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
-      const double2 v = tp[e];
-      double2 l = make_double2(0.0, 0.0);
-      for (int g = 0; g < a.ngroups; ++g) {
-        const uint64_t ip = gi ^ a.xphys[g];
-        double2 C = make_double2(0.0, 0.0);
-        for (int t = a.tbeg[g]; t < a.tend[g]; ++t) {
-          const double sg = (__popcll(ip & s_z[t]) & 1) ? -1.0 : 1.0;
-          C.x = fma(sg, s_c[t].x, C.x);
-          C.y = fma(sg, s_c[t].y, C.y);
-        }
-        const double2 w = cmul(C, tp[e ^ a.xtile[g]]);
-        l.x += w.x;
-        l.y += w.y;
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(psi + (base | (e & lowmask) | s_hi[e >> a.low]))
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  __syncthreads();
+  if ((int64_t)blockIdx.x < a.ntiles) issue(blockIdx.x, tile_buf);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+    const uint64_t base = tile_base(tile);
+    double2* tp = tile_buf + (size_t)(it & 1) * N;
+    __syncthreads();  // the other buffer's previous tile is fully consumed
+    const int64_t next = tile + gridDim.x;
+    const bool more = next < a.ntiles;
+    if (more) issue(next, tile_buf + (size_t)((it + 1) & 1) * N);
+    // fold (-1)^{popc((base ^ x) & z)} (outer part) and (-1)^{popc(xt & zt)} into the coefficients
+    for (int g = 0; g < a.ngroups; ++g)
+      for (int t = a.tbeg[g] + (int)threadIdx.x; t < a.tend[g]; t += blockDim.x) {
+        const uint64_t z = s_z[t];
+        const int par = (__popcll(base & z & ~tmask) + __popc(a.xtile[g] & s_zt[t])) & 1;
+        const double2 c = a.c[t];
+        s_c[t] = par ? make_double2(-c.x, -c.y) : c;
       }
-      acc += re_conj_mul(v, l);
-      if (a.mode == 1) lam[gi] = l;
-      else if (a.mode == 2) { double2 o = lam[gi]; o.x += l.x; o.y += l.y; lam[gi] = o; }
+    if (more) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    if (per_thread == EPT) {
+      double2 l[EPT];
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) l[j] = make_double2(0.0, 0.0);
+      for (int g = 0; g < a.ngroups; ++g) {
+        double2 C[EPT];
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) C[j] = make_double2(0.0, 0.0);
+        for (int t = a.tbeg[g]; t < a.tend[g]; ++t) {
+          const uint32_t zt = s_zt[t];
+          const double2 c = s_c[t];
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) {
+            const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
+            const bool neg = __popc(e & zt) & 1;
+            C[j].x += neg ? -c.x : c.x;
+            C[j].y += neg ? -c.y : c.y;
+          }
+        }
+        const uint32_t xt = a.xtile[g];
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
+          const double2 w = cmul(C[j], tp[e ^ xt]);
+          l[j].x += w.x;
+          l[j].y += w.y;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
+        acc += re_conj_mul(tp[e], l[j]);
+        if (a.mode != 0) {
+          const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
+          if (a.mode == 1) lam[gi] = l[j];
+          else { double2 o = lam[gi]; o.x += l[j].x; o.y += l[j].y; lam[gi] = o; }
+        }
+      }
+    } else {
+      for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+        double2 l = make_double2(0.0, 0.0);
+        for (int g = 0; g < a.ngroups; ++g) {
+          double2 C = make_double2(0.0, 0.0);
+          for (int t = a.tbeg[g]; t < a.tend[g]; ++t) {
+            const bool neg = __popc(e & s_zt[t]) & 1;
+            const double2 c = s_c[t];
+            C.x += neg ? -c.x : c.x;
+            C.y += neg ? -c.y : c.y;
+          }
+          const double2 w = cmul(C, tp[e ^ a.xtile[g]]);
+          l.x += w.x;
+          l.y += w.y;
+        }
+        acc += re_conj_mul(tp[e], l);
+        if (a.mode != 0) {
+          const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
+          if (a.mode == 1) lam[gi] = l;
+          else { double2 o = lam[gi]; o.x += l.x; o.y += l.y; lam[gi] = o; }
+        }
+      }
     }
   }
   acc = block_sum(acc, s_red);
@@ -612,7 +700,7 @@ cudaError_t launch_pauli_cross(const double* psi, const double* partner, double*
 
 int pauli_tile_grid(int n_local, int k) {
   const int64_t ntiles = 1ll << (n_local - k);
-  const int64_t want = (int64_t)num_sms() * 3;
+  const int64_t want = (int64_t)num_sms();
   return (int)(ntiles < want ? ntiles : want);
 }
 
@@ -641,7 +729,7 @@ cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_lo
   a.z = d_z + pp.term_base;
   a.c = reinterpret_cast<const double2*>(d_c) + pp.term_base;
   a.partials = d_partials;
-  const size_t smem = (size_t(16) << pp.k) + (size_t)pp.nterms * 24 + (size_t(8) << (pp.k - pp.low));
+  const size_t smem = (size_t(32) << pp.k) + (size_t)pp.nterms * 28 + 8 + (size_t(8) << (pp.k - pp.low));
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_pauli_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
