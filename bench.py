@@ -157,6 +157,54 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+GRAD_CONFIGS = ("C1", "C2", "C3", "C3dc", "C4g")
+
+
+def run_grad_config(args, P, torch):
+    """Gradient-evaluation throughput of BASELINE configs C1-C3 (and C4g): value = expectation +
+    full adjoint gradient evaluations per second through the C ABI (host call included). C1 runs in
+    batch mode (one launch of 4096 parameter rows: NEXT-1)."""
+    w = W.config(args.config)
+    ga, pa = P.GateArray(w.gates), P.PauliArray(w.ham)
+    sv = P.StateVector(w.n)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    P.sv_set_stream(sv.h, stream.cuda_stream)
+    rows = None
+    if args.config == "C1":
+        rows = np.random.default_rng(1).uniform(-np.pi, np.pi, (4096, len(w.params)))
+
+    def step():
+        if rows is not None:
+            return P.sv_expectation_with_grad_batch(sv.h, ga, rows, pa)
+        return P.sv_expectation_with_grad(sv.h, ga, w.params, pa)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    P.sv_reset_stats(sv.h)
+    with ClockSampler(0) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            out = step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+    st = P.sv_get_stats(sv.h)
+    evals = rows.shape[0] if rows is not None else 1
+    line = {"metric": "expectation + adjoint-gradient evaluations per second", "value": evals / dt,
+            "unit": "grad evals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic", "config": {"workload": args.config, "n_qubits": w.n, "gates": len(w.gates),
+                                            "params": len(w.params), "ham_terms": len(w.ham),
+                                            "rows_per_step": evals},
+            "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
+            "e2e": {"value": evals / dt, "unit": "grad evals/s (host call incl.)",
+                    "h2d_bytes_per_step": int(ga.nbytes + pa.nbytes + (rows.nbytes if rows is not None else w.params.nbytes)),
+                    "d2h_bytes_per_step": int(8 * evals * (1 + len(w.params)))}}
+    print(json.dumps(line), flush=True)
+    sv.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -175,6 +223,9 @@ def main():
     import torch
     import paper_2406_17248_b200 as P
     import paper_2406_17248_b200.dist as PD
+
+    if args.config in GRAD_CONFIGS:
+        return run_grad_config(args, P, torch)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

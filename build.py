@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_2406_17248_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsv.so")
-SOURCES = ["api.cpp", "gates.cpp", "plan.cpp", "shard.cpp", "kernels.cu", "kernels_reg.cu"]
+SOURCES = ["api.cpp", "gates.cpp", "plan.cpp", "shard.cpp", "kernels.cu", "kernels_reg.cu", "kernels_batch.cu"]
 HEADERS = ["sv_internal.h", "sv_handle.h", "cx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

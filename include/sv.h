@@ -177,6 +177,25 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
                                    int32_t n_params, const sv_pauli* terms, int64_t n_terms,
                                    double* out_value, double* out_grad);
 
+/* Batch mode (NEXT-1; "Gradient calculation in batch mode", Fig. 1): n_rows
+ * parameter rows params[r * n_params + p]; out_values[r] = E(row r), out_grads[r * n_params + p] =
+ * dE/dparams[p] at row r. Every row starts from the handle's current state, which is unchanged.
+ * For states of <= 11 local qubits all rows run in ONE launch (one CTA per row, state and adjoint
+ * vector in shared memory); larger states loop over rows with sv_expectation_with_grad.
+ * Validation and errors as sv_expectation_with_grad. Synchronous. */
+sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params,
+                                         int32_t n_params, int32_t n_rows, const sv_pauli* terms, int64_t n_terms,
+                                         double* out_values, double* out_grads);
+
+/* Sampling measurement (NEXT-2; "Sampling Measurement", Fig. 1): draws `shots`
+ * basis states from |psi_i|^2 by inverse CDF and writes, per shot, the measured bits of
+ * qubits[0..n_measured) (bit j of out[s] = value of qubits[j]). Draw s uses the uniform
+ * u_s = (splitmix64(seed + s) >> 11) * 2^-53 (counter-based, reproducible from (seed, s)); draws
+ * are resolved in sorted order, results returned in shot order. The state is unchanged.
+ * Single-GPU handles; synchronous. */
+sv_status sv_sample(sv_handle h, const int32_t* qubits, int32_t n_measured, int64_t shots, uint64_t seed,
+                    uint64_t* out);
+
 sv_status sv_get_stats(sv_handle h, sv_stats* out);
 sv_status sv_reset_stats(sv_handle h);
 

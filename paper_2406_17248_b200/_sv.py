@@ -85,6 +85,9 @@ def _load():
         "sv_expectation_with_grad": [H, ctypes.POINTER(sv_gate), i64, P, i32, ctypes.POINTER(sv_pauli), i64,
                                      ctypes.POINTER(f64), P],
         "sv_get_stats": [H, ctypes.POINTER(sv_stats)],
+        "sv_expectation_with_grad_batch": [H, ctypes.POINTER(sv_gate), i64, P, i32, i32, ctypes.POINTER(sv_pauli), i64,
+                                           P, P],
+        "sv_sample": [H, P, i32, i64, ctypes.c_uint64, P],
         "sv_reset_stats": [H],
         "sv_shard_plan": [i32, i32, i32, ctypes.POINTER(sv_gate), i64, P, i32, ctypes.POINTER(sv_shard_step), i64,
                           ctypes.POINTER(i64), ctypes.POINTER(sv_gate), P, i64, ctypes.POINTER(i64), P],
@@ -271,6 +274,27 @@ def sv_expectation_with_grad(h, gates, params, ham) -> Tuple[float, np.ndarray]:
     return out.value, grad[:np_]
 
 
+def sv_expectation_with_grad_batch(h, gates, params_rows, ham) -> Tuple[np.ndarray, np.ndarray]:
+    """Batch mode: params_rows [B, P]; returns (E [B], grad [B, P])."""
+    ga = gates if isinstance(gates, GateArray) else GateArray(gates)
+    pa = ham if isinstance(ham, PauliArray) else PauliArray(ham)
+    rows = np.ascontiguousarray(np.atleast_2d(np.asarray(params_rows, dtype=np.float64)))
+    B, Pn = rows.shape
+    ev = np.zeros(B)
+    gv = np.zeros((B, max(Pn, 1)))
+    _check(lib.sv_expectation_with_grad_batch(h, ga.arr, ga.n, _ptr(rows) if Pn else None, Pn, B, pa.arr, pa.n,
+                                              _ptr(ev), _ptr(gv)))
+    return ev, gv[:, :Pn]
+
+
+def sv_sample(h, qubits, shots: int, seed: int = 0) -> np.ndarray:
+    """Sampling measurement: shots outcomes over `qubits` (bit j = qubits[j])."""
+    q = np.ascontiguousarray(qubits, dtype=np.int32)
+    out = np.zeros(max(shots, 1), dtype=np.uint64)
+    _check(lib.sv_sample(h, _ptr(q), int(q.size), int(shots), ctypes.c_uint64(seed), _ptr(out)))
+    return out[:shots]
+
+
 def sv_get_stats(h) -> dict:
     s = sv_stats()
     _check(lib.sv_get_stats(h, ctypes.byref(s)))
@@ -371,3 +395,9 @@ class StateVector:
 
     def stats(self):
         return sv_get_stats(self.h)
+
+    def expectation_with_grad_batch(self, gates, params_rows, ham):
+        return sv_expectation_with_grad_batch(self.h, gates, params_rows, ham)
+
+    def sample(self, qubits, shots, seed=0):
+        return sv_sample(self.h, qubits, shots, seed)

@@ -631,3 +631,202 @@ extern "C" sv_status sv_plan_info(int32_t n_qubits, const sv_gate* gates, int64_
   }
   return SV_OK;
 }
+
+extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* gates, int64_t n_gates,
+                                                    const double* params, int32_t n_params, int32_t n_rows,
+                                                    const sv_pauli* terms, int64_t n_terms, double* out_values,
+                                                    double* out_grads) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (n_rows < 0 || !out_values || (n_rows > 0 && n_params > 0 && (!params || !out_grads)))
+    return fail(SV_E_ARG, "bad batch arguments");
+  if (n_rows == 0) return SV_OK;
+  if (h->world > 1 || h->n_local > kBatchMaxQubits) {
+    for (int32_t r = 0; r < n_rows; ++r) {
+      rc = sv_expectation_with_grad(h, gates, n_gates, params ? params + (size_t)r * n_params : nullptr, n_params, terms,
+                                    n_terms, out_values + r, out_grads ? out_grads + (size_t)r * n_params : nullptr);
+      if (rc) return rc;
+    }
+    return SV_OK;
+  }
+  // bind every row (validates every row; the structure is row-independent)
+  std::vector<std::vector<BoundGate>> rows((size_t)n_rows);
+  for (int32_t r = 0; r < n_rows; ++r) {
+    rc = bind_circuit(h, gates, n_gates, params ? params + (size_t)r * n_params : nullptr, n_params, true, &rows[(size_t)r]);
+    if (rc) return fail(rc, std::string("row ") + std::to_string(r) + ": " + g_last_error);
+  }
+  PauliGroups G;
+  rc = group_terms(h, terms, n_terms, &G);
+  if (rc) return rc;
+  // ops, full matrices per row, generators
+  const std::vector<BoundGate>& g0 = rows[0];
+  std::vector<BatchOp> ops(g0.size());
+  std::vector<Cx> gens;
+  int mo = 0;
+  auto full = [](const BoundGate& b, Cx* m) -> int {
+    const Cx z{0, 0}, one{1, 0};
+    switch (b.cls) {
+      case GC_XLIKE: m[0] = z; m[1] = b.m[0]; m[2] = b.m[1]; m[3] = z; return 2;
+      case GC_ZLIKE: m[0] = b.m[0]; m[1] = z; m[2] = z; m[3] = b.m[1]; return 2;
+      case GC_GEN1: for (int e = 0; e < 4; ++e) m[e] = b.m[e]; return 2;
+      case GC_GEN2: for (int e = 0; e < 16; ++e) m[e] = b.m[e]; return 4;
+      case GC_DIAG2: for (int e = 0; e < 16; ++e) m[e] = z; for (int j = 0; j < 4; ++j) m[j * 5] = b.m[j]; return 4;
+      case GC_SWAP: for (int e = 0; e < 16; ++e) m[e] = z; m[0] = one; m[6] = one; m[9] = one; m[15] = one; return 4;
+    }
+    return 0;
+  };
+  for (size_t k = 0; k < g0.size(); ++k) {
+    const BoundGate& b = g0[k];
+    BatchOp& o = ops[k];
+    std::memset(&o, 0, sizeof(o));
+    Cx m[16];
+    o.dim = full(b, m);
+    o.t0 = b.t0;
+    o.t1 = b.t1 >= 0 ? b.t1 : 0;
+    o.cmask = b.controls;
+    o.param = b.param;
+    o.coeff = b.coeff;
+    o.mat_off = mo;
+    mo += o.dim * o.dim;
+    o.gen_off = (int)gens.size();
+    if (b.param >= 0) {
+      // full generator matrix of the gate's dimension (diagonal gens expanded)
+      if (b.gen_dim == o.dim) for (int e = 0; e < o.dim * o.dim; ++e) gens.push_back(b.gen[e]);
+      else return fail(SV_E_ARG, "generator dimension mismatch");
+    }
+  }
+  const int64_t stride = mo;
+  std::vector<Cx> mats((size_t)stride * n_rows);
+  for (int32_t r = 0; r < n_rows; ++r)
+    for (size_t k = 0; k < g0.size(); ++k) full(rows[(size_t)r][k], mats.data() + (size_t)r * stride + ops[k].mat_off);
+  std::vector<uint64_t> xs, zs;
+  std::vector<double> cs;
+  for (size_t gi = 0; gi < G.xs.size(); ++gi)
+    for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
+      xs.push_back(G.xs[gi]);
+      zs.push_back(G.z[t]);
+      cs.push_back(G.c[2 * t]);
+      cs.push_back(G.c[2 * t + 1]);
+    }
+  // one upload: [ops | gens | mats | x | z | c]
+  auto al = [](size_t v) { return (v + 63) & ~size_t(63); };
+  const size_t b_ops = ops.size() * sizeof(BatchOp), b_gen = gens.size() * 16, b_mat = mats.size() * 16,
+               b_x = xs.size() * 8, b_c = cs.size() * 8;
+  const size_t o_gen = al(b_ops), o_mat = o_gen + al(b_gen), o_x = o_mat + al(b_mat), o_z = o_x + al(b_x),
+               o_c = o_z + al(b_x), total = o_c + al(b_c) + 64;
+  if (!h->d_terms.ensure(total)) return fail(SV_E_OOM, "batch buffers");
+  const size_t nout = (size_t)n_rows * (1 + (size_t)std::max(n_params, 0));
+  if (!h->d_out.ensure(nout * 8 + 8)) return fail(SV_E_OOM, "batch outputs");
+  h->h_stage.assign(total, 0);
+  char* hs = h->h_stage.data();
+  std::memcpy(hs, ops.data(), b_ops);
+  std::memcpy(hs + o_gen, gens.data(), b_gen);
+  std::memcpy(hs + o_mat, mats.data(), b_mat);
+  std::memcpy(hs + o_x, xs.data(), b_x);
+  std::memcpy(hs + o_z, zs.data(), b_x);
+  std::memcpy(hs + o_c, cs.data(), b_c);
+  cudaError_t e = cudaMemcpyAsync(h->d_terms.p, hs, total, cudaMemcpyHostToDevice, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "batch upload");
+  const char* db = static_cast<const char*>(h->d_terms.p);
+  double* dout = static_cast<double*>(h->d_out.p);
+  BatchArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.ops = reinterpret_cast<const BatchOp*>(db);
+  a.nops = (int)ops.size();
+  a.nterms = (int)xs.size();
+  a.nparams = std::max(n_params, 0);
+  a.gens = reinterpret_cast<const double*>(db + o_gen);
+  a.mats = reinterpret_cast<const double*>(db + o_mat);
+  a.row_stride = stride;
+  a.x = reinterpret_cast<const uint64_t*>(db + o_x);
+  a.z = reinterpret_cast<const uint64_t*>(db + o_z);
+  a.c = reinterpret_cast<const double*>(db + o_c);
+  a.out_e = dout;
+  a.out_g = dout + n_rows;
+  e = launch_batch_grad(h->psi, h->n_local, a, n_rows, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "batch launch");
+  h->stats.kernel_launches += 1;
+  std::vector<double> hv(nout);
+  e = cudaMemcpyAsync(hv.data(), dout, nout * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "batch readback");
+  for (int32_t r = 0; r < n_rows; ++r) out_values[r] = hv[(size_t)r];
+  if (n_params > 0)
+    for (size_t i = 0; i < (size_t)n_rows * n_params; ++i) out_grads[i] = hv[(size_t)n_rows + i];
+  h->stats.gates_applied += (int64_t)n_rows * n_gates;
+  return SV_OK;
+}
+
+static inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+extern "C" sv_status sv_sample(sv_handle h, const int32_t* qubits, int32_t n_measured, int64_t shots, uint64_t seed,
+                               uint64_t* out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (shots < 0 || n_measured < 0 || n_measured > 64 || (shots > 0 && !out) || (n_measured > 0 && !qubits))
+    return fail(SV_E_ARG, "bad sampling arguments");
+  if (h->world > 1) return fail(SV_E_ARG, "sampling is single-GPU in this version");
+  for (int j = 0; j < n_measured; ++j)
+    if (qubits[j] < 0 || qubits[j] >= h->n) return fail(SV_E_QUBIT_RANGE, "measured qubit out of range");
+  if (shots == 0) return SV_OK;
+  const int n = h->n_local;
+  const int bl = std::min(n, 16);
+  const int64_t nb = int64_t(1) << (n - bl);
+  if (!h->d_partials.ensure((size_t)nb * 8 + 8)) return fail(SV_E_OOM, "block masses");
+  cudaError_t e = launch_block_prob(h->psi, n, bl, static_cast<double*>(h->d_partials.p), h->stream);
+  std::vector<double> mass((size_t)nb);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(mass.data(), h->d_partials.p, nb * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "block masses");
+  h->stats.kernel_launches += 1;
+  std::vector<double> pref((size_t)nb + 1, 0.0);
+  for (int64_t b = 0; b < nb; ++b) pref[(size_t)b + 1] = pref[(size_t)b] + mass[(size_t)b];
+  const double total = pref[(size_t)nb];
+  // sorted draws (target mass = u * total), shot order remembered
+  std::vector<std::pair<double, int64_t>> draws((size_t)shots);
+  for (int64_t s = 0; s < shots; ++s)
+    draws[(size_t)s] = {(double)(splitmix64(seed + (uint64_t)s) >> 11) * 0x1.0p-53 * total, s};
+  std::sort(draws.begin(), draws.end());
+  std::vector<int64_t> blk, beg;
+  std::vector<double> target((size_t)shots);
+  int64_t b = 0;
+  for (int64_t i = 0; i < shots; ++i) {
+    const double u = draws[(size_t)i].first;
+    while (b < nb - 1 && pref[(size_t)b + 1] < u) ++b;
+    if (blk.empty() || blk.back() != b) { blk.push_back(b); beg.push_back(i); }
+    target[(size_t)i] = u - pref[(size_t)b];
+  }
+  beg.push_back(shots);
+  const size_t nblk = blk.size();
+  auto al = [](size_t v) { return (v + 63) & ~size_t(63); };
+  const size_t o_beg = al(nblk * 8), o_t = o_beg + al((nblk + 1) * 8), o_out = o_t + al((size_t)shots * 8),
+               total_b = o_out + (size_t)shots * 8 + 64;
+  if (!h->d_terms.ensure(total_b)) return fail(SV_E_OOM, "sampling buffers");
+  h->h_stage.assign(o_out, 0);
+  std::memcpy(h->h_stage.data(), blk.data(), nblk * 8);
+  std::memcpy(h->h_stage.data() + o_beg, beg.data(), (nblk + 1) * 8);
+  std::memcpy(h->h_stage.data() + o_t, target.data(), (size_t)shots * 8);
+  char* db = static_cast<char*>(h->d_terms.p);
+  e = cudaMemcpyAsync(db, h->h_stage.data(), o_out, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess)
+    e = launch_sample_blocks(h->psi, bl, (int)nblk, reinterpret_cast<const int64_t*>(db),
+                             reinterpret_cast<const int64_t*>(db + o_beg), reinterpret_cast<const double*>(db + o_t),
+                             reinterpret_cast<int64_t*>(db + o_out), h->stream);
+  std::vector<int64_t> idx((size_t)shots);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(idx.data(), db + o_out, (size_t)shots * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "sampling");
+  h->stats.kernel_launches += 1;
+  for (int64_t i = 0; i < shots; ++i) {
+    const uint64_t x = (uint64_t)idx[(size_t)i];
+    uint64_t o = 0;
+    for (int j = 0; j < n_measured; ++j) o |= ((x >> qubits[j]) & 1ull) << j;
+    out[draws[(size_t)i].second] = o;
+  }
+  return SV_OK;
+}

@@ -545,6 +545,66 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
   if (threadIdx.x == 0) a.partials[blockIdx.x] = acc;
 }
 
+
+// ---- sampling (NEXT-2: "Sampling Measurement", Fig. 1) ----
+// Stage 1: probability mass of each block of 2^bl amplitudes (fixed-order block reduction).
+__global__ void __launch_bounds__(kThreads) k_block_prob(const double2* __restrict__ psi, int bl, double* __restrict__ out) {
+  __shared__ double s_red[kThreads / 32];
+  const int64_t b0 = (int64_t)blockIdx.x << bl, B = 1ll << bl;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const double2 v = psi[b0 + i];
+    acc = fma(v.x, v.x, fma(v.y, v.y, acc));
+  }
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+// Stage 2: one CTA per block holding draws: inclusive prefix of |psi|^2 over the block in chunks of
+// blockDim amplitudes; draw r (target mass u_r - block start, sorted) resolves to the first index
+// whose prefix reaches it.
+__global__ void __launch_bounds__(kThreads) k_sample_block(const double2* __restrict__ psi, int bl,
+                                                           const int64_t* __restrict__ blk, const int64_t* __restrict__ beg,
+                                                           const double* __restrict__ target, int64_t* __restrict__ out) {
+  __shared__ double s_scan[kThreads];
+  __shared__ double s_carry;
+  const int64_t b = blk[blockIdx.x], r0 = beg[blockIdx.x], r1 = beg[blockIdx.x + 1];
+  const int64_t b0 = b << bl, B = 1ll << bl;
+  if (threadIdx.x == 0) s_carry = 0.0;
+  int64_t r = r0;  // next unresolved draw (uniform across the block)
+  __syncthreads();
+  for (int64_t off = 0; off < B && r < r1; off += blockDim.x) {
+    double pv = 0.0;
+    if (off + threadIdx.x < B) {
+      const double2 v = psi[b0 + off + threadIdx.x];
+      pv = fma(v.x, v.x, v.y * v.y);
+    }
+    s_scan[threadIdx.x] = pv;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // sequential inclusive scan of the chunk (fixed order, exact reproducibility)
+      double c = s_carry;
+      for (int i = 0; i < (int)blockDim.x; ++i) { c += s_scan[i]; s_scan[i] = c; }
+      s_carry = c;
+    }
+    __syncthreads();
+    // resolve draws whose target falls in this chunk
+    if (threadIdx.x == 0) {
+      while (r < r1 && target[r] <= s_scan[blockDim.x - 1]) {
+        int lo = 0, hi = (int)blockDim.x - 1;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_scan[mid] >= target[r]) hi = mid; else lo = mid + 1; }
+        out[r] = b0 + off + lo;
+        ++r;
+      }
+      s_scan[0] = (double)r;  // broadcast progress
+    }
+    __syncthreads();
+    r = (int64_t)s_scan[0];
+    __syncthreads();
+  }
+  // numerical tail (target beyond the block's accumulated mass by rounding): last index
+  if (threadIdx.x == 0)
+    for (; r < r1; ++r) out[r] = b0 + B - 1;
+}
+
 // out[s] = sum_{j < per} partials[s*per + j], fixed order (strided per-thread sums, then a fixed tree).
 __global__ void __launch_bounds__(kThreads) k_reduce_slots(const double* __restrict__ partials, int per,
                                                            double* __restrict__ out) {
@@ -737,6 +797,18 @@ cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_lo
     attr = true;
   }
   k_pauli_tile<<<grid, kThreads, smem, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<double2*>(lam), a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_prob(const double* psi, int n_local, int bl, double* out, cudaStream_t s) {
+  k_block_prob<<<(unsigned)(1ll << (n_local - bl)), kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), bl, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_blocks(const double* psi, int bl, int nblk, const int64_t* blk, const int64_t* beg,
+                                 const double* target, int64_t* out, cudaStream_t s) {
+  if (nblk <= 0) return cudaSuccess;
+  k_sample_block<<<nblk, kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), bl, blk, beg, target, out);
   return cudaGetLastError();
 }
 

@@ -219,4 +219,33 @@ cudaError_t launch_pauli_cross(const double* psi, const double* partner, double*
 cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out,
                                 cudaStream_t s);
 
+// Batch mode (kernels_batch.cu): one CTA per parameter row, whole state in shared memory.
+struct BatchOp {
+  int32_t dim;        // 2 (one target) or 4 (two targets, matrix index bit j <-> t_j)
+  int32_t t0, t1;
+  int32_t param;      // -1: no gradient slot
+  double coeff;       // chain-rule coefficient
+  uint64_t cmask;     // controls
+  int32_t mat_off;    // double2 offset of the full matrix in the row's block
+  int32_t gen_off;    // double2 offset of the generator D (row-independent)
+};
+struct BatchArgs {
+  const BatchOp* ops;
+  int32_t nops, nterms, nparams, pad;
+  const double* mats;   // [rows][row_stride double2]
+  int64_t row_stride;   // double2 per row
+  const double* gens;
+  const uint64_t* x;
+  const uint64_t* z;
+  const double* c;      // complex coefficients incl. i^{popc(x&z)}
+  double* out_e;        // [rows]
+  double* out_g;        // [rows][nparams]
+};
+constexpr int kBatchMaxQubits = 11;
+// Sampling (kernels.cu): block masses, then per-block inverse-CDF resolution of sorted draws.
+cudaError_t launch_block_prob(const double* psi, int n_local, int bl, double* out, cudaStream_t s);
+cudaError_t launch_sample_blocks(const double* psi, int bl, int nblk, const int64_t* blk, const int64_t* beg,
+                                 const double* target, int64_t* out, cudaStream_t s);
+cudaError_t launch_batch_grad(const double* psi0, int n, const BatchArgs& a, int rows, cudaStream_t s);
+
 }  // namespace sv

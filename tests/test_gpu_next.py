@@ -1,0 +1,95 @@
+"""NEXT-1 batch-mode gradients and NEXT-2 sampling vs the CPU oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+E_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2406_17248_b200 as P
+    return P
+
+
+def test_batch_c1_closed_form(P):
+    """C1 at 256 parameter rows in one launch: E = cos t0 cos t1, g = (-sin t0 cos t1, -cos t0 sin t1, 0, 0)."""
+    w = W.c1_ghz_rx()
+    rows = np.random.default_rng(1).uniform(-np.pi, np.pi, (256, 4))
+    sv = P.StateVector(4)
+    E, G = sv.expectation_with_grad_batch(w.gates, rows, w.ham)
+    sv.close()
+    np.testing.assert_allclose(E, np.cos(rows[:, 0]) * np.cos(rows[:, 1]), atol=E_TOL)
+    ref = np.stack([-np.sin(rows[:, 0]) * np.cos(rows[:, 1]), -np.cos(rows[:, 0]) * np.sin(rows[:, 1]),
+                    np.zeros(256), np.zeros(256)], 1)
+    np.testing.assert_allclose(G, ref, atol=E_TOL)
+
+
+@pytest.mark.parametrize("n", [3, 7, 11, 13])
+def test_batch_random_tasks(P, n):
+    """Rows of a random controlled circuit (one-launch kernel for n <= 11, row loop above)."""
+    w = W.random_complex(n, 5, seed=n, n_params=4, extra_kinds=("PS", "MAT1", "MAT2", "SWAP"))
+    ham = W.random_hamiltonian(n, 8, seed=n)
+    rows = np.random.default_rng(n).uniform(-3, 3, (6, 4))
+    psi0 = W.random_state(n, n)
+    sv = P.StateVector(n)
+    sv.set_state(psi0)
+    E, G = sv.expectation_with_grad_batch(w.gates, rows, ham)
+    for r in range(rows.shape[0]):
+        E0, g0 = oracle.adjoint_grad(n, w.gates, rows[r], ham, psi0)
+        assert abs(E[r] - E0) < E_TOL
+        np.testing.assert_allclose(G[r], g0, atol=E_TOL, rtol=0)
+    assert np.max(np.abs(sv.get_state() - psi0)) == 0.0  # state unchanged
+    sv.close()
+
+
+def _splitmix64(x):
+    m = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & m
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+    return x ^ (x >> 31)
+
+
+def _reference_samples(psi, qubits, shots, seed):
+    """Inverse CDF of the oracle's |psi|^2 with the documented counter-based uniforms."""
+    p = np.abs(psi) ** 2
+    cdf = np.cumsum(p)
+    u = np.array([(_splitmix64(seed + s) >> 11) * 2.0 ** -53 for s in range(shots)]) * cdf[-1]
+    idx = np.minimum(np.searchsorted(cdf, u, side="left"), p.size - 1)
+    out = np.zeros(shots, dtype=np.uint64)
+    for j, q in enumerate(qubits):
+        out |= ((idx >> q) & 1).astype(np.uint64) << np.uint64(j)
+    return out
+
+
+@pytest.mark.parametrize("n", [1, 5, 12, 18])
+def test_sampling_matches_inverse_cdf(P, n):
+    w = W.random_complex(n, 4, seed=100 + n)
+    psi = oracle.apply_circuit(n, w.gates)
+    sv = P.StateVector(n)
+    sv.apply_circuit(w.gates)
+    qubits = list(range(n))[::-1][: min(n, 7)]
+    got = sv.sample(qubits, 4000, seed=n)
+    ref = _reference_samples(psi, qubits, 4000, n)
+    assert np.mean(got == ref) > 0.999  # equal up to prefix-rounding ties at bin edges
+    again = sv.sample(qubits, 4000, seed=n)
+    assert np.array_equal(got, again)  # deterministic under the seed
+    sv.close()
+
+
+def test_sampling_spec_examples(P):
+    """|0> -> all 0; |+> -> binomial within 5 sigma; Bell -> only 00 and 11."""
+    sv = P.StateVector(3)
+    assert np.all(sv.sample([0], 100, seed=1) == 0)
+    sv.apply_circuit([W.Gate("H", (0,))])
+    ones = int(np.sum(sv.sample([0], 100000, seed=2)))
+    assert abs(ones - 50000) < 5 * np.sqrt(100000 * 0.25)
+    sv.reset()
+    sv.apply_circuit([W.Gate("H", (0,)), W.Gate("X", (1,), (0,))])
+    outs = sv.sample([0, 1], 10000, seed=3)
+    assert set(np.unique(outs).tolist()) == {0, 3}
+    sv.close()
