@@ -656,7 +656,7 @@ int plan_grid(const Plan& plan, int n_local) {
     // other's shared-memory / HBM phases); adjoint passes: one (register-heavy) CTA per SM
     bool has_grad = false;
     for (const PassDesc& p : plan.passes) has_grad |= p.n_grad > 0;
-    const int64_t want = (int64_t)num_sms() * (has_grad ? 1 : 2);
+    const int64_t want = (int64_t)num_sms() * (has_grad ? 1 : 3);  // kernels_reg.cu SV_FWD_CTAS
     return (int)(ntiles < want ? ntiles : want);
   }
   return pass_grid(n_local, pd.k, false);

@@ -24,6 +24,10 @@
 #include "cx.cuh"
 #include "sv_internal.h"
 
+#ifndef SV_FWD_CTAS
+#define SV_FWD_CTAS 3  // forward-pass CTAs per SM (register budget 65536 / (256 * CTAs))
+#endif
+
 namespace sv {
 namespace {
 
@@ -433,7 +437,7 @@ __device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, con
 // ---------------------------------------------------------------- the pass kernel
 
 template <int NR, bool DUAL>
-__global__ void __launch_bounds__(256, DUAL ? 1 : 2) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
+__global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
@@ -507,6 +511,19 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : 2) k_pass_reg(double2* __restr
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
       if constexpr (!DUAL) {
+        // L1 prefetch of the next dense stage's variant-matrix fragments (global, L2-resident):
+        // the first MMA of that stage then finds its A operand in L1 instead of waiting on L2
+        for (int nx = st + 1; nx < a.nstages; ++nx) {
+          const StageDesc& Sn = s_st[nx];
+          if (!Sn.dense) continue;
+          uint32_t var = Sn.warp_var[warp];
+          for (int b = 0; b < Sn.m_outer; ++b) var |= (uint32_t)((base >> Sn.var_outer[b]) & 1ull) << (Sn.m_tile + b);
+          const double2* U = reinterpret_cast<const double2*>(a.mats) + Sn.dense_off + var * (16u * 20u);
+          const double2* q = U + (lane >> 2) * 20 + (lane & 3) * 4;  // one 64-byte line per lane covers 4 entries
+          asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q));
+          asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q + 8 * 20));
+          break;
+        }
         if (S.dense) {
           dense_stage(tp, S, reinterpret_cast<const double2*>(a.mats), base, warp, lane);
           __syncthreads();
