@@ -127,11 +127,15 @@ int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, c
 }
 
 // Runs all passes of a plan on psi (and lam for the adjoint plan).
-int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, double* d_partials, int grid) {
+int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, double* d_partials, int grid,
+             double* r_partials, double* r_sum) {
   const Plan& plan = cp.plan;
   const char* base = static_cast<const char*>(cp.buf.p);
+  size_t da_done = 0;
   for (size_t i = 0; i < plan.passes.size(); ++i) {
     const PassDesc& pd = plan.passes[i];
+    int n_da = 0;
+    for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? 1 : 0;
     const int next_mat = (i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size();
     PassLaunch L;
     L.pd = &pd;
@@ -144,9 +148,19 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
     L.grid = grid > 0 ? grid : plan_grid(plan, h->n_local);
     L.n_local = h->n_local;
     L.rank_bits = 0;
+    L.n_da = n_da;
+    L.r_partials = r_partials;
+    if (n_da && (!r_partials || !r_sum)) return fail(SV_E_ARG, "internal: adjoint dense stage without R buffers");
     cudaError_t e = launch_pass(psi, lam, L, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "pass launch");
     h->stats.kernel_launches += 1;
+    if (n_da) {
+      const int nw = (1 << (pd.k - pd.R)) / 32;
+      e = launch_reduce_slots(r_partials, n_da * nw * 512, L.grid, r_sum + da_done * (size_t)nw * 512, h->stream);
+      if (e != cudaSuccess) return cuda_fail(h, e, "R reduction");
+      h->stats.kernel_launches += 1;
+      da_done += (size_t)n_da;
+    }
     const double amps = (double)(1ull << h->n_local);
     if (lam) {
       h->stats.adjoint_passes += 1;
@@ -164,7 +178,7 @@ int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg) {
   const CachedPlan* cp = nullptr;
   int rc = get_plan(h, bg, false, &cp);
   if (rc != SV_OK) return rc;
-  rc = run_plan(h, *cp, h->psi, nullptr, nullptr, 0);
+  rc = run_plan(h, *cp, h->psi, nullptr, nullptr, 0, nullptr, nullptr);
   if (rc != SV_OK) return rc;
   h->stats.gates_applied += (int64_t)bg.size();
   return SV_OK;
@@ -361,6 +375,7 @@ sv_status sv_destroy(sv_handle h) {
   h->state.release();
   h->work_psi.release();
   h->work_lam.release();
+  h->work_r.release();
   release_plan_cache(h);
   h->d_ops.release();
   h->d_mats.release();
@@ -523,56 +538,114 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   h->stats.algorithmic_bytes += 2.0 * (double)bytes;
   // 1. forward
   const CachedPlan* fwdp = nullptr;
-  const CachedPlan* revp = nullptr;
   rc = get_plan(h, bg, false, &fwdp);
   if (rc) return rc;
-  rc = run_plan(h, *fwdp, psi, nullptr, nullptr, 0);
+  rc = run_plan(h, *fwdp, psi, nullptr, nullptr, 0, nullptr, nullptr);
   if (rc) return rc;
-  rc = get_plan(h, bg, true, &revp);
-  if (rc) return rc;
-  const Plan& rev = revp->plan;
   h->stats.gates_applied += (int64_t)bg.size();
-  // 2. lambda = H psi, E partials
-  const int pgrid = pauli_tile_grid(h->n_local, pauli_k(h->n_local));
-  const size_t ng = G.xs.size();
-  const int agrid = plan_grid(rev, h->n_local);
-  const size_t ns = (size_t)rev.n_grad_slots;
-  const size_t part_doubles = ng * pgrid + ns * agrid;
-  if (!h->d_partials.ensure(part_doubles * 8 + 8) || !h->d_out.ensure((ng + ns) * 8 + 8)) return fail(SV_E_OOM, "partials");
-  double* dp = static_cast<double*>(h->d_partials.p);
-  int nslots = 0;
-  if (ng == 0) {
+  // 2. lambda = H psi, E
+  double E = 0.0;
+  if (G.xs.empty()) {
     e = cudaMemsetAsync(lam, 0, bytes, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "zero lambda");
   } else {
-    rc = run_groups(h, G, psi, lam, dp, pgrid, &nslots);
+    const int pgrid = pauli_tile_grid(h->n_local, pauli_k(h->n_local));
+    const size_t ng = G.xs.size();
+    if (!h->d_partials.ensure(ng * pgrid * 8 + 8) || !h->d_out.ensure(ng * 8 + 8)) return fail(SV_E_OOM, "partials");
+    int nslots = 0;
+    rc = run_groups(h, G, psi, lam, static_cast<double*>(h->d_partials.p), pgrid, &nslots);
     if (rc) return rc;
-  }
-  // 3. reverse sweep over (psi, lambda)
-  if (!rev.passes.empty()) {
-    rc = run_plan(h, *revp, psi, lam, dp + ng * pgrid, agrid);
+    e = launch_reduce_slots(static_cast<double*>(h->d_partials.p), nslots, pgrid, static_cast<double*>(h->d_out.p),
+                            h->stream);
+    std::vector<double> ev((size_t)nslots);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ev.data(), h->d_out.p, (size_t)nslots * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "energy");
+    h->stats.kernel_launches += 1;
+    // (the copy completes at the synchronisation inside run_reverse)
+    std::vector<double> d;
+    const CachedPlan* revp = nullptr;
+    rc = get_plan(h, bg, true, &revp);
     if (rc) return rc;
+    rc = run_reverse(h, *revp, psi, lam, &d);
+    if (rc) return rc;
+    e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "energy");
+    for (double v : ev) E += v;
+    *out_value = E;
+    for (int32_t p = 0; p < n_params; ++p) out_grad[p] = 0.0;
+    for (size_t sl = 0; sl < d.size(); ++sl) out_grad[revp->plan.slot_param[sl]] += revp->plan.slot_coeff[sl] * 2.0 * d[sl];
+    return SV_OK;
   }
-  // 4. reductions
-  double* dout = static_cast<double*>(h->d_out.p);
-  e = launch_reduce_slots(dp, nslots, pgrid, dout, h->stream);
-  if (e == cudaSuccess && ns) e = launch_reduce_slots(dp + ng * pgrid, (int)ns, agrid, dout + ng, h->stream);
-  if (e != cudaSuccess) return cuda_fail(h, e, "reduce");
-  h->stats.kernel_launches += (ng ? 1 : 0) + (ns ? 1 : 0);
-  std::vector<double> hv(ng + ns);
-  if (ng + ns) {
-    e = cudaMemcpyAsync(hv.data(), dout, (ng + ns) * 8, cudaMemcpyDeviceToHost, h->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    if (e != cudaSuccess) return cuda_fail(h, e, "gradient readback");
-  }
-  double E = 0.0;
-  for (int g = 0; g < nslots; ++g) E += hv[(size_t)g];
-  *out_value = E;
+  // empty H: E = 0, gradient 0 (the sweep would only produce zeros)
+  e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "sync");
+  *out_value = 0.0;
   for (int32_t p = 0; p < n_params; ++p) out_grad[p] = 0.0;
-  // chain rule, in reverse-sweep slot order (fixed): g[p] += coeff_k * 2 Re d_k
-  for (size_t s = 0; s < ns; ++s) out_grad[rev.slot_param[s]] += rev.slot_coeff[s] * 2.0 * hv[ng + s];
   return SV_OK;
 }
+
+}  // extern "C"
+
+// Runs a reverse (adjoint) plan on (psi, lambda) and returns the per-slot overlaps
+// d_s = Re<lambda|D_s|psi> in slot order: sequential stages through per-CTA partials, adjoint dense
+// stages through their correlation matrices R (host contraction with B_{j,var}). Synchronous.
+int sv::run_reverse(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, std::vector<double>* d_out) {
+  const Plan& rev = cp.plan;
+  const size_t ns = (size_t)rev.n_grad_slots;
+  d_out->assign(ns, 0.0);
+  if (rev.passes.empty()) return SV_OK;
+  const int agrid = plan_grid(rev, h->n_local);
+  const size_t nda = rev.da.size();
+  const int nw = (1 << (rev.passes[0].k - rev.passes[0].R)) / 32;
+  const size_t part_slots = ns * (size_t)agrid;
+  const size_t r_part = nda ? (size_t)rev.max_da_per_pass * nw * 512 * agrid : 0, r_sum = nda * (size_t)nw * 512;
+  if (!h->work_r.ensure((part_slots + ns + r_part + r_sum) * 8 + 64)) return fail(SV_E_OOM, "adjoint buffers");
+  double* dp = static_cast<double*>(h->work_r.p);
+  double* dout = dp + part_slots;
+  double* rp = dout + ns;
+  double* rsum = rp + r_part;
+  int rc = run_plan(h, cp, psi, lam, dp, agrid, nda ? rp : nullptr, nda ? rsum : nullptr);
+  if (rc) return rc;
+  cudaError_t e = cudaSuccess;
+  if (ns) e = launch_reduce_slots(dp, (int)ns, agrid, dout, h->stream);
+  std::vector<double> rs(r_sum);
+  if (e == cudaSuccess && ns) e = cudaMemcpyAsync(d_out->data(), dout, ns * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess && nda) e = cudaMemcpyAsync(rs.data(), rsum, r_sum * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "gradient readback");
+  h->stats.kernel_launches += ns ? 1 : 0;
+  for (size_t di = 0; di < nda; ++di) {
+    const Plan::DAStage& ds = rev.da[di];
+    const int nvar = 1 << ds.m_tile;
+    std::vector<Cx> R((size_t)nvar * 256, Cx{0, 0});
+    for (int w = 0; w < nw; ++w) {
+      const int var = w & (nvar - 1);
+      const double* f = rs.data() + (di * nw + (size_t)w) * 512;
+      for (int mt = 0; mt < 2; ++mt)
+        for (int nt = 0; nt < 2; ++nt)
+          for (int v = 0; v < 2; ++v)
+            for (int l = 0; l < 32; ++l) {
+              const int a = 8 * mt + (l >> 2), b = 8 * nt + 2 * (l & 3) + v;
+              Cx& r = R[(size_t)var * 256 + (size_t)a * 16 + b];
+              r.re += f[((((mt * 2 + nt) * 2 + 0) * 2 + v) << 5) + l];
+              r.im += f[((((mt * 2 + nt) * 2 + 1) * 2 + v) << 5) + l];
+            }
+    }
+    for (size_t j = 0; j < ds.slots.size(); ++j) {
+      double d = 0.0;  // Re tr(B R) = sum_{a,b} Re(B[a][b] R[b][a])
+      for (int var = 0; var < nvar; ++var) {
+        const Cx* Bm = ds.B[j].data() + (size_t)var * 256;
+        const Cx* Rm = R.data() + (size_t)var * 256;
+        for (int a = 0; a < 16; ++a)
+          for (int b = 0; b < 16; ++b) d += Bm[a * 16 + b].re * Rm[b * 16 + a].re - Bm[a * 16 + b].im * Rm[b * 16 + a].im;
+      }
+      (*d_out)[(size_t)ds.slots[j]] = d;
+    }
+  }
+  return SV_OK;
+}
+
+extern "C" {
 
 sv_status sv_get_stats(sv_handle h, sv_stats* out) {
   if (!h || !out) return fail(SV_E_ARG, "null argument");
@@ -617,7 +690,7 @@ extern "C" sv_status sv_plan_info(int32_t n_qubits, const sv_gate* gates, int64_
     r.tile_mask = 0;
     for (int p = 0; p < pd.k; ++p) r.tile_mask |= 1ull << pd.tq[p];
     r.n_dense = 0;
-    for (int si = pd.stage_begin; si < pd.stage_end; ++si) r.n_dense += plan.stages[si].dense;
+    for (int si = pd.stage_begin; si < pd.stage_end; ++si) r.n_dense += plan.stages[si].dense ? 1 : 0;
     r.mat_doubles = (int32_t)(((i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size()) - pd.mat_begin);
     r.fma_per_amp = pass_fma_per_amp(plan, i);
     r.pad = 0;

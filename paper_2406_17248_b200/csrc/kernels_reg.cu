@@ -50,6 +50,8 @@ __device__ __forceinline__ double2 cneg(double2 a) { return make_double2(-a.x, -
 
 struct RegArgs {
   int32_t k, low, nops, nstages, n_outer, nmats, ngrad, grid;
+  int32_t n_da, pad_da;
+  double* r_partials;  // adjoint dense stages: [da][warp][16 * 32][grid]
   int8_t tq[kMaxTileQubits + 3];
   int8_t oq[64];
   int64_t ntiles;
@@ -329,15 +331,23 @@ __device__ __forceinline__ double reg_overlap_c(const double2 (&v)[1 << NR], con
                                                 const double2* g, uint32_t tthr, uint64_t base) {
   const uint32_t cj = o.cj();
   if (o.gdiag()) {
+    // Re <w|G|v> with G diagonal: sum_j Re(g_{idx(j)} conj(w_j) v_j); the entries are read once
+    // from shared memory and selected per amplitude (no per-element indexed loads)
     const uint32_t ta = o.pa() != 31u ? (tthr >> o.pa()) & 1u : (uint32_t)((base >> o.qa()) & 1ull);
     const uint32_t tb = o.pb() != 31u ? (tthr >> o.pb()) & 1u : (uint32_t)((base >> o.qb()) & 1ull);
+    const double2 g0 = lds(g), g1 = lds(g + 1);
+    const bool two = o.gen() == 2u;
+    const double2 g2 = two ? lds(g + 2) : g0, g3 = two ? lds(g + 3) : g1;
+    const uint32_t ra = o.ra(), rb = o.rb();
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < (1 << NR); ++j) {
       SV_CTRL_SKIP(j)
-      uint32_t idx = o.ra() != 15u ? ((uint32_t)j >> o.ra()) & 1u : ta;
-      if (o.gen() == 2u) idx |= (o.rb() != 15u ? ((uint32_t)j >> o.rb()) & 1u : tb) << 1;
-      acc += re_conj_mul(w[j], cmul(g[idx], v[j]));
+      const uint32_t b0 = ra != 15u ? ((uint32_t)j >> ra) & 1u : ta;
+      const uint32_t b1 = two ? (rb != 15u ? ((uint32_t)j >> rb) & 1u : tb) : 0u;
+      const double2 gs = b1 ? (b0 ? g3 : g2) : (b0 ? g1 : g0);
+      const double2 p = make_double2(fma(w[j].x, v[j].x, w[j].y * v[j].y), fma(w[j].x, v[j].y, -w[j].y * v[j].x));
+      acc += fma(gs.x, p.x, -gs.y * p.y);  // Re(gs * conj(w) v)
     }
     return acc;
   }
@@ -434,6 +444,57 @@ __device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, con
         tp[baseD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]] = make_double2(d[mh][nt][v], d[mh + 2][nt][v]);
 }
 
+
+// Adjoint dense stage (DUAL): accumulate R = sum_v psi_v lambda_v^H over the warp's 16 vectors at
+// the stage start (FP64 MMAs with K = vectors) into the warp's private shared-memory accumulator,
+// then un-apply the stage (dense U) to psi and lambda. The overlaps of the stage's parametrised
+// ops follow on the host as tr(B_j R).
+__device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDesc& S, const double2* __restrict__ gmats2,
+                                         uint64_t base, int warp, int lane, double* racc) {
+  const uint32_t wsw = S.warp_swz[warp];
+  const uint32_t br = wsw ^ S.lane_r[lane];
+  // fragments: A = Psi[a = 8 mt + lane/4][v = 4 kt + lane%4], B = Lambda[b = 8 nt + lane/4][v]
+  double2 ps[2][4], la[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) {
+      const uint32_t ad = br ^ S.off_r[mt * 4 + kt];
+      ps[mt][kt] = tp[ad];
+      la[mt][kt] = tl[ad];
+    }
+  double rre[2][2][2], rim[2][2][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) rre[mt][nt][0] = rre[mt][nt][1] = rim[mt][nt][0] = rim[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        // Re R = Pr Lr^T + Pi Li^T ; Im R = Pi Lr^T - Pr Li^T
+        dmma(rre[mt][nt][0], rre[mt][nt][1], ps[mt][kt].x, la[nt][kt].x);
+        dmma(rim[mt][nt][0], rim[mt][nt][1], ps[mt][kt].y, la[nt][kt].x);
+        dmma(rre[mt][nt][0], rre[mt][nt][1], ps[mt][kt].y, la[nt][kt].y);
+        dmma(rim[mt][nt][0], rim[mt][nt][1], -ps[mt][kt].x, la[nt][kt].y);
+      }
+  // accumulate into the warp's slot: element e = ((mt * 2 + nt) * 2 + comp) * 2 + v, lane-contiguous
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        racc[((((mt * 2 + nt) * 2 + 0) * 2 + v) << 5) + lane] += rre[mt][nt][v];
+        racc[((((mt * 2 + nt) * 2 + 1) * 2 + v) << 5) + lane] += rim[mt][nt][v];
+      }
+  __syncwarp();
+  dense_stage(tp, S, gmats2, base, warp, lane);
+  dense_stage(tl, S, gmats2, base, warp, lane);
+}
+
 // ---------------------------------------------------------------- the pass kernel
 
 template <int NR, bool DUAL>
@@ -451,6 +512,7 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
   const int nhi = 1 << (a.k - a.low);
   uint64_t* s_hi = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
   double* s_acc = reinterpret_cast<double*>(s_hi + nhi);  // [ngrad][nwarps]
+  double* s_racc = s_acc + (DUAL ? a.ngrad * nwarps : 0);   // [n_da][nwarps][512]
 
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.ops);
@@ -466,8 +528,10 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
         if ((h >> b) & 1) off |= 1ull << a.tq[a.low + b];
       s_hi[h] = off;
     }
-    if (DUAL)
+    if (DUAL) {
       for (int i = tid; i < a.ngrad * nwarps; i += nthr) s_acc[i] = 0.0;
+      for (int i = tid; i < a.n_da * nwarps * 512; i += nthr) s_racc[i] = 0.0;
+    }
   }
   __syncthreads();
   const uint32_t lowmask = (1u << a.low) - 1u;
@@ -510,6 +574,14 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
     // ---- stages ----
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
+      if constexpr (DUAL) {
+        if (S.dense == 2) {
+          da_stage(tp, tl, S, reinterpret_cast<const double2*>(a.mats), base, warp, lane,
+                   s_racc + ((size_t)S.da_index * nwarps + warp) * 512);
+          __syncthreads();
+          continue;
+        }
+      }
       if constexpr (!DUAL) {
         // L1 prefetch of the next dense stage's variant-matrix fragments (global, L2-resident):
         // the first MMA of that stage then finds its A operand in L1 instead of waiting on L2
@@ -589,6 +661,8 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
     __syncthreads();
   }
   if (DUAL) {
+    for (int i = tid; i < a.n_da * nwarps * 512; i += nthr)
+      a.r_partials[(int64_t)i * a.grid + blockIdx.x] = s_racc[i];
     for (int i = tid; i < a.nops; i += nthr) {
       const Op o = load_op(s_ops + i);
       if (!o.gen()) continue;
@@ -599,8 +673,9 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
   }
 }
 
-size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual) {
+size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da) {
   size_t b = (size_t(16) << k) * (dual ? 2 : 1) * 2;  // double-buffered
+  b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
   b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
   b += (size_t)nmats * 8 + (size_t(8) << (k - low));
   b += dual ? (size_t)ngrad * (nthr / 32) * 8 : 0;
@@ -632,7 +707,10 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   a.partials = L.d_partials;
   const bool dual = lam != nullptr;
   const int nthr = 1 << (pd.k - pd.R);
-  const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual);
+  a.n_da = L.n_da;
+  a.pad_da = 0;
+  a.r_partials = L.r_partials;
+  const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual, a.n_da);
   static bool attr_set[2] = {false, false};
   if (!attr_set[dual]) {
     cudaError_t e = dual ? cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)

@@ -224,6 +224,10 @@ int env_int(const char* name, int dflt) {
 }
 const int g_dense_min_cost = env_int("SV_DENSE_MIN_COST", 20);
 const int g_dense_max_var = env_int("SV_DENSE_MAX_VAR", 6);
+const int g_da_min_cost = env_int("SV_DA_MIN_COST", 96);   // adjoint dense stages (0 disables: huge)
+const int g_da_enable = env_int("SV_DA", 1);
+const int g_da_max_tile = env_int("SV_DA_MAX_TILE", 2);
+const int g_da_max_outer = env_int("SV_DA_MAX_OUTER", 0);
 
 // FP64 pipe cost per amplitude of an op applied sequentially (DFMA path), for the dense choice.
 int seq_cost(const DevOp& o, const double* m) {
@@ -310,10 +314,66 @@ void dense_apply(Cx* u, const DevOp& o, const double* m, const int* reg_new, uin
   }
 }
 
+
+// u <- (Pi_C (x) G) u in register space: the generator of a parametrised op restricted to the
+// control-satisfied subspace (zero elsewhere). G: op's generator (diagonal entries if gen_diag).
+void dense_gen_apply(Cx* u, const DevOp& o, const double* gm, const int* reg_new, uint32_t tbits, uint64_t obits) {
+  uint32_t cj = 0, cthr = 0;
+  for (int p = 0; p < 32; ++p)
+    if ((o.ctile >> p) & 1ull) {
+      if (reg_new[p] >= 0) cj |= 1u << reg_new[p];
+      else cthr |= 1u << p;
+    }
+  const bool var_ok = ((cthr & tbits) == cthr) && ((o.couter & obits) == o.couter);
+  auto bit_of = [&](int pos, int q, int j) -> uint32_t {
+    if (pos >= 0 && reg_new[pos] >= 0) return ((uint32_t)j >> reg_new[pos]) & 1u;
+    if (pos >= 0) return (tbits >> pos) & 1u;
+    return (uint32_t)((obits >> q) & 1ull);
+  };
+  auto cm = [](Cx a, Cx b) { return Cx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; };
+  auto ca = [](Cx a, Cx b) { return Cx{a.re + b.re, a.im + b.im}; };
+  const Cx* G = reinterpret_cast<const Cx*>(gm);
+  Cx out[16];
+  for (int j = 0; j < 16; ++j) out[j] = Cx{0, 0};
+  if (var_ok) {
+    if (o.gen_diag) {
+      for (int j = 0; j < 16; ++j) {
+        if (((uint32_t)j & cj) != cj) continue;
+        uint32_t idx = bit_of(o.pa, o.qa, j);
+        if (o.gen_dim == 4) idx |= bit_of(o.pb, o.qb, j) << 1;
+        out[j] = cm(G[idx], u[j]);
+      }
+    } else if (o.gen_dim == 2) {
+      const int r = reg_new[o.pa];
+      for (int j = 0; j < 16; ++j) {
+        if ((j >> r) & 1) continue;
+        if (((uint32_t)j & cj) != cj) continue;
+        const int j1 = j | (1 << r);
+        out[j] = ca(cm(G[0], u[j]), cm(G[1], u[j1]));
+        out[j1] = ca(cm(G[2], u[j]), cm(G[3], u[j1]));
+      }
+    } else {
+      const int ra = reg_new[o.pa], rb = reg_new[o.pb];
+      for (int j = 0; j < 16; ++j) {
+        if (((j >> ra) & 1) || ((j >> rb) & 1)) continue;
+        if (((uint32_t)j & cj) != cj) continue;
+        const int idx[4] = {j, j | (1 << ra), j | (1 << rb), j | (1 << ra) | (1 << rb)};
+        for (int rr = 0; rr < 4; ++rr) {
+          Cx acc{0, 0};
+          for (int c = 0; c < 4; ++c) acc = ca(acc, cm(G[rr * 4 + c], u[idx[c]]));
+          out[idx[rr]] = acc;
+        }
+      }
+    }
+  }
+  for (int j = 0; j < 16; ++j) u[j] = out[j];
+}
+
 // Folds a 4-register stage into dense variant matrices (appended to plan->mats) when cheaper than
 // the sequential path and feasible: variant bits <= 3 in total, tile variant bits on warp
 // positions. Returns false (stage untouched) otherwise.
-bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles) {
+bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles, bool adjoint = false,
+                int pass_index = 0, int da_index = 0) {
   const int k = pd.k;
   const int nw_bits = k - 8;  // 2^(k-3) threads: 16 vectors of 16 amplitudes per warp
   if (nw_bits < 1 || __builtin_popcount(sp->regset) > 4) return false;
@@ -339,7 +399,15 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
   const int m_tile = __builtin_popcount(vt), m_outer = __builtin_popcountll(vo);
   if (std::getenv("SV_PLAN_DEBUG"))
     std::fprintf(stderr, "stage: ops %d cost %d m_tile %d m_outer %d\n", (int)sp->ops.size(), cost, m_tile, m_outer);
-  if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > g_dense_max_var) return false;
+  if (adjoint) {
+    // adjoint dense stage: per-warp R accumulators need warp-uniform variants (no outer bits);
+    // worth it once the sequential dual cost (psi + lambda + overlaps) passes the dense cost
+    int ngrad = 0;
+    for (const DevOp& o : sp->ops) ngrad += o.grad_slot >= 0 ? 1 : 0;
+    if (2 * cost + 8 * ngrad < g_da_min_cost || m_outer > g_da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits)) return false;
+  } else if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > g_dense_max_var) {
+    return false;
+  }
   const int nvar = 1 << (m_tile + m_outer);
   const size_t per = 2 * 16 * kDenseStride;
   const size_t used = plan->mats.size() - pd.mat_begin;
@@ -355,14 +423,15 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
   if (free_pos.size() < 4) return false;
   auto d3 = [](int a, int b, int c) { return (a % 3) != (b % 3) && (a % 3) != (c % 3) && (b % 3) != (c % 3); };
   int best[5] = {0, 1, 0, 1, 2}, best_score = -1;
-  for (int r0 = 0; r0 < 4 && best_score < 2; ++r0)
-    for (int r1 = 0; r1 < 4 && best_score < 2; ++r1) {
+  for (int r0 = 0; r0 < 4 && best_score < 3; ++r0)
+    for (int r1 = 0; r1 < 4 && best_score < 3; ++r1) {
       if (r1 == r0) continue;
-      for (size_t a = 0; a < free_pos.size() && best_score < 2; ++a)
-        for (size_t b = 0; b < free_pos.size() && best_score < 2; ++b)
-          for (size_t c = 0; c < free_pos.size() && best_score < 2; ++c) {
+      for (size_t a = 0; a < free_pos.size() && best_score < 3; ++a)
+        for (size_t b = 0; b < free_pos.size() && best_score < 3; ++b)
+          for (size_t c = 0; c < free_pos.size() && best_score < 3; ++c) {
             if (a == b || a == c || b == c) continue;
-            const int sc = (d3(regs[r0], regs[r1], free_pos[a]) ? 1 : 0) + (d3(regs[r0], free_pos[b], free_pos[c]) ? 1 : 0);
+            const int sc = (d3(regs[r0], regs[r1], free_pos[a]) ? 1 : 0) + (d3(regs[r0], free_pos[b], free_pos[c]) ? 1 : 0) +
+                           (adjoint && d3(free_pos[a], free_pos[b], regs[r0]) ? 1 : 0) + (adjoint ? 0 : 1);
             if (sc > best_score) { best_score = sc; best[0] = r0; best[1] = r1; best[2] = (int)a; best[3] = (int)b; best[4] = (int)c; }
           }
     }
@@ -435,6 +504,67 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
                                 ((lb & 1u) ? p0 : 0u) | ((lb & 2u) ? p1 : 0u));
     S.lane_d[l] = (uint16_t)swz(((lb >> 2) & 1u ? p0 : 0u) | ((lb >> 3) & 1u ? p1 : 0u) | ((lb >> 4) & 1u ? p2 : 0u) |
                                 ((lb & 1u) ? bc1 : 0u) | ((lb & 2u) ? bc2 : 0u));
+    // R layout: amp a = lane/4 (bits R0 R1 R2) + 8 mt (R3); vector v = lane%4 (c0 c1) + 4 kt (c2, n0)
+    S.lane_r[l] = (uint16_t)swz(((lb >> 2) & 1u ? p0 : 0u) | ((lb >> 3) & 1u ? p1 : 0u) | ((lb >> 4) & 1u ? p2 : 0u) |
+                                ((lb & 1u) ? bc0 : 0u) | ((lb & 2u) ? bc1 : 0u));
+  }
+  for (int mt = 0; mt < 2; ++mt)
+    for (int kt = 0; kt < 4; ++kt)
+      S.off_r[mt * 4 + kt] = (uint16_t)swz((mt ? p3 : 0u) | ((kt & 1) ? bc2 : 0u) | ((kt & 2) ? n0 : 0u));
+  S.da_index = da_index;
+  if (adjoint) {
+    S.dense = 2;
+    Plan::DAStage ds;
+    ds.pass = pass_index;
+    ds.da_index = da_index;
+    ds.m_tile = m_tile;
+    // B_{j,var} = V^dagger (Pi_C G_j) V with V the product of the stage's ops before j
+    for (size_t i = 0; i < sp->ops.size(); ++i)
+      if (sp->ops[i].grad_slot >= 0) {
+        ds.slots.push_back(sp->ops[i].grad_slot);
+        ds.B.emplace_back((size_t)nvar * 256);
+      }
+    auto cm = [](Cx a, Cx b) { return Cx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; };
+    for (int v = 0; v < nvar; ++v) {
+      uint32_t tbits = 0;
+      for (int b = 0; b < m_tile; ++b)
+        if ((v >> b) & 1) tbits |= 1u << vlist[b];
+      Cx V[256];  // columns c: V[j * 16 + c]
+      for (int j = 0; j < 16; ++j)
+        for (int c = 0; c < 16; ++c) V[j * 16 + c] = Cx{j == c ? 1.0 : 0.0, 0.0};
+      int gj = 0;
+      for (const DevOp& o : sp->ops) {
+        if (o.grad_slot >= 0) {
+          Cx GV[256];
+          for (int c = 0; c < 16; ++c) {
+            Cx u[16];
+            for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
+            dense_gen_apply(u, o, plan->mats.data() + pd.mat_begin + o.gen_off, reg_new, tbits, 0);
+            for (int j = 0; j < 16; ++j) GV[j * 16 + c] = u[j];
+          }
+          Cx* Bd = ds.B[(size_t)gj].data() + (size_t)v * 256;
+          for (int a = 0; a < 16; ++a)
+            for (int b = 0; b < 16; ++b) {
+              Cx acc{0, 0};
+              for (int j = 0; j < 16; ++j) {
+                const Cx vc = Cx{V[j * 16 + a].re, -V[j * 16 + a].im};
+                const Cx t = cm(vc, GV[j * 16 + b]);
+                acc.re += t.re;
+                acc.im += t.im;
+              }
+              Bd[a * 16 + b] = acc;
+            }
+          ++gj;
+        }
+        for (int c = 0; c < 16; ++c) {
+          Cx u[16];
+          for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
+          dense_apply(u, o, plan->mats.data() + pd.mat_begin + o.mat_off, reg_new, tbits, 0);
+          for (int j = 0; j < 16; ++j) V[j * 16 + c] = u[j];
+        }
+      }
+    }
+    plan->da.push_back(std::move(ds));
   }
   for (int nt = 0; nt < 2; ++nt)
     for (int kq = 0; kq < 4; ++kq)
@@ -462,10 +592,31 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense) {
   if (forward && dense && k >= 9) {
     const size_t budget = size_t(1) << 22;  // variant matrices live in global memory (L2-resident)
     std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(3, k - 8), g_dense_max_var);
+    std::vector<DevOp> seq;  // consecutive non-dense candidates are re-staged together
     for (StagePlan& sp : st4) {
-      if (make_dense(&sp, *pd, plan, budget)) final_stages.push_back(std::move(sp));
-      else add_sequential(split_stages(sp.ops, *pd, pd->R, -1, -1));
+      if (make_dense(&sp, *pd, plan, budget)) {
+        if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
+        final_stages.push_back(std::move(sp));
+      } else {
+        seq.insert(seq.end(), sp.ops.begin(), sp.ops.end());
+      }
     }
+    if (!seq.empty()) add_sequential(split_stages(seq, *pd, pd->R, -1, -1));
+  } else if (!forward && dense && k >= 9 && g_da_enable) {
+    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(g_da_max_tile, k - 8), g_da_max_tile + g_da_max_outer);
+    int nda = 0;
+    std::vector<DevOp> seq;
+    for (StagePlan& sp : st4) {
+      if (nda < kMaxDAPerPass && make_dense(&sp, *pd, plan, size_t(1) << 22, true, (int)plan->passes.size(), nda)) {
+        ++nda;
+        if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
+        final_stages.push_back(std::move(sp));
+      } else {
+        seq.insert(seq.end(), sp.ops.begin(), sp.ops.end());
+      }
+    }
+    if (!seq.empty()) add_sequential(split_stages(seq, *pd, pd->R, -1, -1));
+    plan->max_da_per_pass = std::max(plan->max_da_per_pass, nda);
   } else {
     add_sequential(split_stages(pops, *pd, pd->R, -1, -1));
   }
@@ -570,6 +721,8 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
   plan->ops.clear();
   plan->mats.clear();
   plan->stages.clear();
+  plan->da.clear();
+  plan->max_da_per_pass = 0;
   plan->slot_param.clear();
   plan->slot_coeff.clear();
   plan->n_grad_slots = 0;

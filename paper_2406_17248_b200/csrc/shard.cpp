@@ -303,7 +303,7 @@ int run_segment(sv_state_s* h, const std::vector<BoundGate>& phys, const std::ve
     const CachedPlan* cp = nullptr;
     int rc = get_plan(h, loc, false, &cp);
     if (rc) return rc;
-    rc = run_plan(h, *cp, vec[a], nullptr, nullptr, 0);
+    rc = run_plan(h, *cp, vec[a], nullptr, nullptr, 0, nullptr, nullptr);
     if (rc) return rc;
   }
   return SV_OK;
@@ -601,22 +601,11 @@ int shard_expectation_with_grad(sv_state_s* h, const std::vector<BoundGate>& bg,
       const CachedPlan* revp = nullptr;
       rc = get_plan(h, loc, true, &revp);
       if (rc) return rc;
-      const Plan& rev = revp->plan;
-      const int agrid = plan_grid(rev, nl);
-      const size_t ns = (size_t)rev.n_grad_slots;
-      if (!h->d_partials.ensure(ns * agrid * 8 + 8) || !h->d_out.ensure(ns * 8 + 8)) return fail(SV_E_OOM, "partials");
-      rc = run_plan(h, *revp, psi[a], lam[a], static_cast<double*>(h->d_partials.p), agrid);
+      std::vector<double> d;
+      rc = run_reverse(h, *revp, psi[a], lam[a], &d);
       if (rc) return rc;
-      if (ns) {
-        std::vector<double> hv(ns);
-        cudaError_t e = launch_reduce_slots(static_cast<double*>(h->d_partials.p), (int)ns, agrid,
-                                            static_cast<double*>(h->d_out.p), h->stream);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hv.data(), h->d_out.p, ns * 8, cudaMemcpyDeviceToHost, h->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-        if (e != cudaSuccess) return cuda_fail(h, e, "gradient readback");
-        h->stats.kernel_launches += 1;
-        for (size_t s = 0; s < ns; ++s) grad[(size_t)rev.slot_param[s]] += rev.slot_coeff[s] * 2.0 * hv[s];
-      }
+      for (size_t sl = 0; sl < d.size(); ++sl)
+        grad[(size_t)revp->plan.slot_param[sl]] += revp->plan.slot_coeff[sl] * 2.0 * d[sl];
     }
   }
   // 4. one all-reduce of (E, gradient)

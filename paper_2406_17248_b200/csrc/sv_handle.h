@@ -40,7 +40,7 @@ struct sv_state_s {
   bool poisoned = false;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  sv::DevBuf state, work_psi, work_lam;
+  sv::DevBuf state, work_psi, work_lam, work_r;
   double* psi = nullptr;
   sv::DevBuf d_ops, d_mats, d_terms, d_partials, d_out;
   std::vector<char> h_stage;
@@ -58,8 +58,10 @@ int cuda_fail(sv_state_s* h, cudaError_t e, const char* where);
 int check_handle(sv_state_s* h);
 // Returns the (cached or freshly built and uploaded) plan of `gates` (local physical qubits).
 int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, const CachedPlan** out);
-int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, double* d_partials, int grid);
+int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, double* d_partials, int grid,
+             double* r_partials, double* r_sum);
 void release_plan_cache(sv_state_s* h);
+int run_reverse(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, std::vector<double>* d_out);
 int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg);
 
 struct PauliGroups {

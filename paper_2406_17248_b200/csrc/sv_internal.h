@@ -78,8 +78,14 @@ struct StageDesc {
   uint8_t warp_var[8];       // dense: tile-variant index of warp w
   uint16_t lane_b[32];       // dense: swz(lane part of the B-fragment load address)
   uint16_t lane_d[32];       // dense: swz(lane part of the D-fragment store address)
+  // adjoint dense stages (dense == 2): R = sum_v psi_v lambda_v^H over the warp's vectors, loaded
+  // with amp = 8 mt + lane/4, vector = 4 kt + lane%4
+  uint16_t lane_r[32];       // swz(lane part of the R-fragment load address)
+  uint16_t off_r[8];         // swz(uniform part) for (mt, kt), index mt * 4 + kt
+  int32_t da_index;          // index among the pass' adjoint dense stages (R accumulator slot)
+  int32_t pad1;
 };
-static_assert(sizeof(StageDesc) == 224, "StageDesc layout");
+static_assert(sizeof(StageDesc) == 312, "StageDesc layout");
 
 
 // Compact op of the register kernel (32 bytes: two 16-byte shared loads per op).
@@ -128,7 +134,18 @@ struct Plan {
   int n_grad_slots = 0;
   std::vector<int32_t> slot_param;   // slot -> parameter index
   std::vector<double> slot_coeff;    // slot -> chain-rule coefficient (coeff of the occurrence)
+  // Adjoint dense stages (host side): the overlaps of their parametrised ops come from the
+  // per-variant correlation matrices R_var = sum psi lambda^H at the stage start (accumulated on the
+  // device) as d_j = sum_var tr(B_{j,var} R_var), B_{j,var} = V_{j-1}^dagger (Pi_C G_j) V_{j-1}.
+  struct DAStage {
+    int pass = 0, da_index = 0, m_tile = 0;
+    std::vector<int> slots;              // grad slots of the stage's parametrised ops (stage order)
+    std::vector<std::vector<Cx>> B;      // [grad op][var * 256 + a * 16 + b]
+  };
+  std::vector<DAStage> da;
+  int max_da_per_pass = 0;
 };
+constexpr int kMaxDAPerPass = 2;  // R accumulators: 32 KiB of shared memory per adjoint dense stage
 
 // ---------------------------------------------------------------------------------------------
 // Host-side gate after binding: class + entries, logical qubits.
@@ -175,6 +192,8 @@ struct PassLaunch {
   const RegOp* d_rops;        // device pointer to the plan's compact ops
   double* d_partials;      // [n_slots][grid] adjoint overlap partials (or null)
   int nmats;               // matrix doubles of this pass
+  int n_da = 0;            // adjoint dense stages of this pass
+  double* r_partials = nullptr;  // their R accumulators: [da][warp][512][grid]
   int grid;                // CTAs
   int n_local;
   uint64_t rank_bits;      // (sharded) global index bits of this shard, for controls/diagonals on
