@@ -204,6 +204,49 @@ def run_grad_config(args, P, torch):
     sv.close()
 
 
+def run_density_config(args, P, torch):
+    """NEXT-4 density matrix: gates/s of rho <- U rho U^dagger for C4's generator at n = DM<n>
+    qubits (a 2n-qubit vector), plus tr(rho H) with a 50-term JW H."""
+    n = int(args.config[2:] or 14)
+    w = W.random_circuit(n, 40, seed=3040)
+    ham = W.jw_hamiltonian(n, 50, 3030)
+    ga, pa = P.GateArray(w.gates), P.PauliArray(ham)
+    dm = P.DensityMatrix(n)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    P.sv_set_stream(dm.h, stream.cuda_stream)
+
+    def step():
+        dm.reset()
+        P.sv_apply_circuit(dm.h, ga, w.params)
+        return P.sv_expectation(dm.h, pa)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    P.sv_reset_stats(dm.h)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            E = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    st = P.sv_get_stats(dm.h)
+    line = {"metric": "density-matrix gates/sec (rho <- U rho U^dagger) + tr(rho H)", "value": len(w.gates) / (ms / 1e3),
+            "unit": "gates/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic", "config": {"workload": f"DM{n}: {n}-qubit density matrix (a {2 * n}-qubit vector), "
+                                                      "C4 generator depth 40, 50-term JW H", "n_qubits": n,
+                                            "gates": len(w.gates)},
+            "E": E, "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
+            "e2e": {"value": len(w.gates) / (ms / 1e3), "unit": "gates/s", "h2d_bytes_per_step": int(ga.nbytes + pa.nbytes),
+                    "d2h_bytes_per_step": 8}}
+    print(json.dumps(line), flush=True)
+    dm.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -225,6 +268,8 @@ def main():
 
     if args.config in GRAD_CONFIGS:
         return run_grad_config(args, P, torch)
+    if args.config.startswith("DM"):
+        return run_density_config(args, P, torch)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -139,6 +139,15 @@ sv_status sv_nccl_unique_id(void* out, int32_t out_bytes);
  * the sharded path without several GPUs. */
 sv_status sv_create_virtual_shards(int32_t n_qubits, int32_t world, sv_handle* out);
 
+/* NEXT-4 density matrix ("mqmatrix", §3.2): rho of n qubits (initially
+ * |0..0><0..0|) held as a 2n-qubit vector vec[r + 2^n c] = rho[r][c]. On such a handle
+ * sv_apply_gate / sv_apply_circuit apply rho <- U rho U^dagger (eq. at: U on the row
+ * qubits, U* on the column qubits, one fused pass plan over 2n qubits), sv_expectation returns
+ * <H> = tr(rho H) (eq. at), sv_get_state / sv_set_state transfer rho row-major
+ * (2 * 4^n doubles: rho[r][c] at 2 (r 2^n + c)), sv_reset restores |0><0|. Gradients, sampling,
+ * batch mode and sharding are not available on density handles (SV_E_ARG). 1 <= n <= 17. */
+sv_status sv_create_density(int32_t n_qubits, sv_handle* out);
+
 sv_status sv_destroy(sv_handle h);
 
 /* Use this CUDA stream (a cudaStream_t passed as void*) for all subsequent work; NULL = the

@@ -204,3 +204,47 @@ def shift_grad(n: int, gates, params, ham, psi0: Optional[np.ndarray] = None) ->
 
 def energy(n: int, gates, params, ham, psi0=None) -> float:
     return expectation(apply_circuit(n, gates, params, psi0), ham)[0]
+
+
+# ----------------------------------------------------------------------------- density matrices
+# PAPER.md §3.2: rho = sum_i p_i |psi_i><psi_i|, rho' = U rho U^dagger (eq. at),
+# <H> = tr(rho H) (eq. at). Plain definitions with full 2^n x 2^n matrices (small n only):
+# each gate's full unitary is built column by column with the oracle's plain gate application.
+
+def full_unitary(n: int, gate, params=None) -> np.ndarray:
+    """The 2^n x 2^n matrix of one gate (columns = the gate applied to basis states)."""
+    U = np.empty((1 << n, 1 << n), dtype=np.complex128)
+    for c in range(1 << n):
+        e = np.zeros(1 << n, dtype=np.complex128)
+        e[c] = 1.0
+        U[:, c] = apply_circuit(n, [gate], params, e)
+    return U
+
+
+def dm_apply_circuit(n: int, gates, params=None, rho0: Optional[np.ndarray] = None) -> np.ndarray:
+    """rho <- U_k rho U_k^dagger for every gate in order; rho0 defaults to |0><0|."""
+    rho = np.zeros((1 << n, 1 << n), dtype=np.complex128) if rho0 is None else np.array(rho0, dtype=np.complex128)
+    if rho0 is None:
+        rho[0, 0] = 1.0
+    for g in gates:
+        U = full_unitary(n, g, params)
+        rho = U @ rho @ U.conj().T
+    return rho
+
+
+def pauli_matrix(n: int, term: dict) -> np.ndarray:
+    """Dense matrix of one Pauli string (columns = the string applied to basis states)."""
+    P = np.empty((1 << n, 1 << n), dtype=np.complex128)
+    for c in range(1 << n):
+        e = np.zeros(1 << n, dtype=np.complex128)
+        e[c] = 1.0
+        for q, p in term.items():
+            e = apply_matrix(e, gate_matrix(p), [q])
+        P[:, c] = e
+    return P
+
+
+def dm_expectation(rho: np.ndarray, ham) -> float:
+    """<H> = tr(rho H) = sum_t c_t tr(rho P_t), real part."""
+    n = int(rho.shape[0]).bit_length() - 1
+    return float(sum(c * np.trace(rho @ pauli_matrix(n, term)) for c, term in ham).real)

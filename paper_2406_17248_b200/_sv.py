@@ -70,6 +70,7 @@ def _load():
         "sv_create_sharded": [i32, i32, i32, P, ctypes.POINTER(H)],
         "sv_nccl_unique_id": [P, i32],
         "sv_create_virtual_shards": [i32, i32, ctypes.POINTER(H)],
+        "sv_create_density": [i32, ctypes.POINTER(H)],
         "sv_destroy": [H],
         "sv_set_stream": [H, P],
         "sv_set_option": [H, i32, i64],
@@ -194,6 +195,12 @@ def sv_create(n_qubits: int) -> ctypes.c_void_p:
 def sv_create_virtual_shards(n_qubits: int, world: int) -> ctypes.c_void_p:
     h = ctypes.c_void_p()
     _check(lib.sv_create_virtual_shards(n_qubits, world, ctypes.byref(h)))
+    return h
+
+
+def sv_create_density(n_qubits: int) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _check(lib.sv_create_density(n_qubits, ctypes.byref(h)))
     return h
 
 
@@ -401,3 +408,20 @@ class StateVector:
 
     def sample(self, qubits, shots, seed=0):
         return sv_sample(self.h, qubits, shots, seed)
+
+
+class DensityMatrix(StateVector):
+    """rho of n qubits (NEXT-4, §3.2): apply_circuit does rho <- U rho U^dagger,
+    expectation returns tr(rho H); states transfer as 2^n x 2^n matrices."""
+
+    def __init__(self, n: int):
+        super().__init__(n, handle=sv_create_density(n))
+
+    def set_state(self, rho):
+        r = np.ascontiguousarray(np.asarray(rho, dtype=np.complex128).reshape(-1))
+        _check(lib.sv_set_state(self.h, _ptr(r)))
+
+    def get_state(self):
+        out = np.empty(1 << (2 * self.n), dtype=np.complex128)
+        _check(lib.sv_get_state(self.h, _ptr(out)))
+        return out.reshape(1 << self.n, 1 << self.n)

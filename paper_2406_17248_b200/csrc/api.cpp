@@ -335,6 +335,24 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
   return SV_OK;
 }
 
+// Density matrix: rho <- U rho U^dagger is U on the row qubits and U* on the column qubits of the
+// 2n-qubit vector vec[r + 2^n c] (§3.2 eq. at).
+std::vector<BoundGate> density_expand(const std::vector<BoundGate>& bg, int n) {
+  std::vector<BoundGate> out;
+  out.reserve(2 * bg.size());
+  for (const BoundGate& g : bg) {
+    out.push_back(g);
+    BoundGate c = g;
+    c.t0 = g.t0 + n;
+    c.t1 = g.t1 >= 0 ? g.t1 + n : -1;
+    c.controls = g.controls << n;
+    for (int e = 0; e < 16; ++e) c.m[e].im = -c.m[e].im;
+    c.param = -1;
+    out.push_back(c);
+  }
+  return out;
+}
+
 }  // namespace sv
 
 using namespace sv;
@@ -366,6 +384,18 @@ sv_status sv_create(int32_t n_qubits, sv_handle* out) {
   if (e != cudaSuccess) { sv_destroy(h); return fail(SV_E_CUDA, cudaGetErrorString(e)); }
   h->stats.kernel_launches += 1;
   *out = h;
+  return SV_OK;
+}
+
+sv_status sv_create_density(int32_t n_qubits, sv_handle* out) {
+  if (n_qubits < 1 || n_qubits > 17) {
+    if (out) *out = nullptr;
+    return fail(SV_E_ARG, "density matrices: n_qubits must be in [1, 17]");
+  }
+  int rc = sv_create(2 * n_qubits, out);
+  if (rc) return rc;
+  (*out)->n = n_qubits;
+  (*out)->density = true;
   return SV_OK;
 }
 
@@ -433,6 +463,19 @@ sv_status sv_set_state(sv_handle h, const double* host) {
   if (rc) return rc;
   if (!host) return fail(SV_E_ARG, "null host buffer");
   if (h->world > 1) return shard_set_state(h, host);
+  if (h->density) {  // row-major rho[r][c] -> vec[r + 2^n c]
+    const uint64_t D = 1ull << h->n;
+    std::vector<double> v(2 * D * D);
+    for (uint64_t r = 0; r < D; ++r)
+      for (uint64_t c = 0; c < D; ++c) {
+        v[2 * (r + D * c)] = host[2 * (r * D + c)];
+        v[2 * (r + D * c) + 1] = host[2 * (r * D + c) + 1];
+      }
+    cudaError_t e = cudaMemcpyAsync(h->psi, v.data(), v.size() * 8, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "set_state");
+    return SV_OK;
+  }
   cudaError_t e = cudaMemcpyAsync(h->psi, host, size_t(16) << h->n, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "set_state");
@@ -444,6 +487,19 @@ sv_status sv_get_state(sv_handle h, double* host) {
   if (rc) return rc;
   if (!host) return fail(SV_E_ARG, "null host buffer");
   if (h->world > 1) return shard_get_state(h, host);
+  if (h->density) {
+    const uint64_t D = 1ull << h->n;
+    std::vector<double> v(2 * D * D);
+    cudaError_t e = cudaMemcpyAsync(v.data(), h->psi, v.size() * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "get_state");
+    for (uint64_t r = 0; r < D; ++r)
+      for (uint64_t c = 0; c < D; ++c) {
+        host[2 * (r * D + c)] = v[2 * (r + D * c)];
+        host[2 * (r * D + c) + 1] = v[2 * (r + D * c) + 1];
+      }
+    return SV_OK;
+  }
   cudaError_t e = cudaMemcpyAsync(host, h->psi, size_t(16) << h->n, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "get_state");
@@ -455,7 +511,7 @@ sv_status sv_set_state_device(sv_handle h, const void* dev) {
   if (rc) return rc;
   if (!dev) return fail(SV_E_ARG, "null device buffer");
   if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
-  cudaError_t e = cudaMemcpyAsync(h->psi, dev, size_t(16) << h->n, cudaMemcpyDeviceToDevice, h->stream);
+  cudaError_t e = cudaMemcpyAsync(h->psi, dev, size_t(16) << h->n_local, cudaMemcpyDeviceToDevice, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "set_state_device");
   return SV_OK;
 }
@@ -465,7 +521,7 @@ sv_status sv_get_state_device(sv_handle h, void* dev) {
   if (rc) return rc;
   if (!dev) return fail(SV_E_ARG, "null device buffer");
   if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
-  cudaError_t e = cudaMemcpyAsync(dev, h->psi, size_t(16) << h->n, cudaMemcpyDeviceToDevice, h->stream);
+  cudaError_t e = cudaMemcpyAsync(dev, h->psi, size_t(16) << h->n_local, cudaMemcpyDeviceToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "get_state_device");
   return SV_OK;
@@ -482,6 +538,7 @@ sv_status sv_apply_circuit(sv_handle h, const sv_gate* gates, int64_t n_gates, c
   rc = bind_circuit(h, gates, n_gates, params, n_params, false, &bg);
   if (rc) return rc;
   if (h->world > 1) return shard_apply(h, bg);
+  if (h->density) return apply_bound(h, density_expand(bg, h->n));
   return apply_bound(h, bg);
 }
 
@@ -495,6 +552,36 @@ sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, do
   if (h->world > 1) return shard_expectation(h, G, out_value);
   *out_value = 0.0;
   if (G.xs.empty()) return SV_OK;
+  if (h->density) {
+    // tr(rho H): one diagonal-gather pass over 2^n elements per x-group
+    const int n = h->n;
+    int64_t gsz = ((int64_t(1) << n) + 255) / 256;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gsz, 592));
+    const size_t ng = G.xs.size();
+    const size_t zb = (G.z.size() * 8 + 15) & ~size_t(15), cb = G.c.size() * 8;
+    if (!h->d_terms.ensure(zb + cb + 16) || !h->d_partials.ensure(ng * grid * 8 + 8) || !h->d_out.ensure(ng * 8 + 8))
+      return fail(SV_E_OOM, "density expectation buffers");
+    h->h_stage.assign(zb + cb + 16, 0);
+    std::memcpy(h->h_stage.data(), G.z.data(), G.z.size() * 8);
+    std::memcpy(h->h_stage.data() + zb, G.c.data(), cb);
+    cudaError_t e = cudaMemcpyAsync(h->d_terms.p, h->h_stage.data(), zb + cb, cudaMemcpyHostToDevice, h->stream);
+    const uint64_t* dz = static_cast<const uint64_t*>(h->d_terms.p);
+    const double* dc = reinterpret_cast<const double*>(static_cast<const char*>(h->d_terms.p) + zb);
+    double* dp = static_cast<double*>(h->d_partials.p);
+    for (size_t gi = 0; gi < ng && e == cudaSuccess; ++gi)
+      e = launch_dm_trace(h->psi, n, G.xs[gi], dz + G.begin[gi], dc + 2 * G.begin[gi], G.end[gi] - G.begin[gi],
+                          dp + gi * (size_t)grid, grid, h->stream);
+    if (e == cudaSuccess) e = launch_reduce_slots(dp, (int)ng, grid, static_cast<double*>(h->d_out.p), h->stream);
+    std::vector<double> gv(ng);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(gv.data(), h->d_out.p, ng * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "density expectation");
+    h->stats.kernel_launches += (int64_t)ng + 1;
+    double E = 0.0;
+    for (double v : gv) E += v;
+    *out_value = E;
+    return SV_OK;
+  }
   const int grid = pauli_tile_grid(h->n_local, pauli_k(h->n_local));
   const size_t ng = G.xs.size();
   if (!h->d_partials.ensure(ng * grid * 8) || !h->d_out.ensure(ng * 8)) return fail(SV_E_OOM, "partials");
@@ -522,6 +609,7 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   int rc = check_handle(h);
   if (rc) return rc;
   if (!out_value || (n_params > 0 && !out_grad)) return fail(SV_E_ARG, "null output");
+  if (h->density) return fail(SV_E_ARG, "gradients are not available on density-matrix handles");
   std::vector<BoundGate> bg;
   rc = bind_circuit(h, gates, n_gates, params, n_params, true, &bg);
   if (rc) return rc;
@@ -714,6 +802,7 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
   if (n_rows < 0 || !out_values || (n_rows > 0 && n_params > 0 && (!params || !out_grads)))
     return fail(SV_E_ARG, "bad batch arguments");
   if (n_rows == 0) return SV_OK;
+  if (h->density) return fail(SV_E_ARG, "batch mode is not available on density-matrix handles");
   if (h->world > 1 || h->n_local > kBatchMaxQubits) {
     for (int32_t r = 0; r < n_rows; ++r) {
       rc = sv_expectation_with_grad(h, gates, n_gates, params ? params + (size_t)r * n_params : nullptr, n_params, terms,
@@ -844,6 +933,7 @@ extern "C" sv_status sv_sample(sv_handle h, const int32_t* qubits, int32_t n_mea
   if (shots < 0 || n_measured < 0 || n_measured > 64 || (shots > 0 && !out) || (n_measured > 0 && !qubits))
     return fail(SV_E_ARG, "bad sampling arguments");
   if (h->world > 1) return fail(SV_E_ARG, "sampling is single-GPU in this version");
+  if (h->density) return fail(SV_E_ARG, "sampling is not available on density-matrix handles");
   for (int j = 0; j < n_measured; ++j)
     if (qubits[j] < 0 || qubits[j] >= h->n) return fail(SV_E_QUBIT_RANGE, "measured qubit out of range");
   if (shots == 0) return SV_OK;

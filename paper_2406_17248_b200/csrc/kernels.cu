@@ -605,6 +605,35 @@ __global__ void __launch_bounds__(kThreads) k_sample_block(const double2* __rest
     for (; r < r1; ++r) out[r] = b0 + B - 1;
 }
 
+
+// ---- density matrix (NEXT-4, §3.2) ----
+// tr(rho P) for the Pauli terms of one x-group: rho[r'][r] is stored at r' + (r << n), and
+// (P rho)[r][r] = c' (-1)^{popc((r ^ x) & z)} rho[r ^ x][r]; E partial = Re sum_r sum_t (...).
+__global__ void __launch_bounds__(kThreads) k_dm_trace(const double2* __restrict__ vec, int n, uint64_t x,
+                                                       const uint64_t* __restrict__ z, const double2* __restrict__ c,
+                                                       int nterms, double* __restrict__ partials) {
+  __shared__ uint64_t s_z[256];
+  __shared__ double2 s_c[256];
+  __shared__ double s_red[kThreads / 32];
+  for (int i = threadIdx.x; i < nterms; i += blockDim.x) { s_z[i] = z[i]; s_c[i] = c[i]; }
+  __syncthreads();
+  const int64_t N = 1ll << n, stride = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
+    const uint64_t rp = (uint64_t)r ^ x;
+    double2 C = make_double2(0.0, 0.0);
+    for (int t = 0; t < nterms; ++t) {
+      const double sg = (__popcll(rp & s_z[t]) & 1) ? -1.0 : 1.0;
+      C.x = fma(sg, s_c[t].x, C.x);
+      C.y = fma(sg, s_c[t].y, C.y);
+    }
+    const double2 v = vec[rp | ((uint64_t)r << n)];
+    acc += fma(C.x, v.x, -C.y * v.y);
+  }
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
 // out[s] = sum_{j < per} partials[s*per + j], fixed order (strided per-thread sums, then a fixed tree).
 __global__ void __launch_bounds__(kThreads) k_reduce_slots(const double* __restrict__ partials, int per,
                                                            double* __restrict__ out) {
@@ -809,6 +838,13 @@ cudaError_t launch_sample_blocks(const double* psi, int bl, int nblk, const int6
                                  const double* target, int64_t* out, cudaStream_t s) {
   if (nblk <= 0) return cudaSuccess;
   k_sample_block<<<nblk, kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), bl, blk, beg, target, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dm_trace(const double* vec, int n, uint64_t x, const uint64_t* d_z, const double* d_c, int nterms,
+                            double* d_partials, int grid, cudaStream_t s) {
+  k_dm_trace<<<grid, kThreads, 0, s>>>(reinterpret_cast<const double2*>(vec), n, x, d_z,
+                                       reinterpret_cast<const double2*>(d_c), nterms, d_partials);
   return cudaGetLastError();
 }
 

@@ -36,6 +36,7 @@ struct sv_state_s {
   int n = 0;           // logical qubits
   int n_local = 0;     // qubits held per shard (n - log2 world)
   int world = 1, rank = 0;
+  bool density = false;  // rho of n qubits held as a 2n-qubit vector (n_local = 2n)
   int device = 0;
   bool poisoned = false;
   cudaStream_t own_stream = nullptr;

@@ -261,6 +261,9 @@ struct BatchArgs {
   double* out_g;        // [rows][nparams]
 };
 constexpr int kBatchMaxQubits = 11;
+// Density matrix: tr(rho P) over one x-group of Pauli terms (rho as a 2n-qubit vector).
+cudaError_t launch_dm_trace(const double* vec, int n, uint64_t x, const uint64_t* d_z, const double* d_c, int nterms,
+                            double* d_partials, int grid, cudaStream_t s);
 // Sampling (kernels.cu): block masses, then per-block inverse-CDF resolution of sorted draws.
 cudaError_t launch_block_prob(const double* psi, int n_local, int bl, double* out, cudaStream_t s);
 cudaError_t launch_sample_blocks(const double* psi, int bl, int nblk, const int64_t* blk, const int64_t* beg,

@@ -93,3 +93,48 @@ def test_sampling_spec_examples(P):
     outs = sv.sample([0, 1], 10000, seed=3)
     assert set(np.unique(outs).tolist()) == {0, 3}
     sv.close()
+
+
+# ----------------------------------------------------------------------------- NEXT-4 density matrix
+
+@pytest.mark.parametrize("n", [1, 2, 4, 6, 8])
+def test_density_matches_oracle(P, n):
+    """rho <- U rho U^dagger through the fused 2n-qubit passes vs the oracle's full-matrix
+    definition (§3.2), from |0><0| and from a mixed state; tr(rho H)."""
+    w = W.random_complex(n, 4, seed=300 + n, n_params=3, extra_kinds=("MAT1", "MAT2", "PS", "XLIKE"))
+    ham = W.random_hamiltonian(n, 8, seed=n)
+    dm = P.DensityMatrix(n)
+    dm.apply_circuit(w.gates, w.params)
+    ref = oracle.dm_apply_circuit(n, w.gates, w.params)
+    assert np.max(np.abs(dm.get_state() - ref)) <= 1e-10
+    assert abs(dm.expectation(ham) - oracle.dm_expectation(ref, ham)) < E_TOL
+    a, b = W.random_state(n, 1), W.random_state(n, 2)
+    mix = 0.25 * np.outer(a, a.conj()) + 0.75 * np.outer(b, b.conj())
+    dm.set_state(mix)
+    dm.apply_circuit(w.gates, w.params)
+    ref = oracle.dm_apply_circuit(n, w.gates, w.params, mix)
+    assert np.max(np.abs(dm.get_state() - ref)) <= 1e-10
+    assert abs(dm.expectation(ham) - oracle.dm_expectation(ref, ham)) < E_TOL
+    dm.reset()
+    st = dm.get_state()
+    assert st[0, 0] == 1 and np.count_nonzero(st) == 1
+    dm.close()
+
+
+def test_density_pure_state_equals_state_vector_12q(P):
+    """Pure-state consistency at 12 qubits (a 24-qubit vector): rho = |psi><psi| of the
+    state-vector path (S:700 criterion 5), checked on sampled entries; tr(rho H) = <psi|H|psi>."""
+    n = 12
+    w = W.random_complex(n, 5, seed=12)
+    psi = oracle.apply_circuit(n, w.gates)
+    dm = P.DensityMatrix(n)
+    dm.apply_circuit(w.gates)
+    rho = dm.get_state()
+    idx = np.random.default_rng(0).integers(0, 1 << n, (2000, 2))
+    np.testing.assert_allclose(rho[idx[:, 0], idx[:, 1]], psi[idx[:, 0]] * np.conj(psi[idx[:, 1]]), atol=1e-12)
+    assert abs(np.trace(rho) - 1) < 1e-10
+    ham = W.jw_hamiltonian(n, 20, seed=5)
+    assert abs(dm.expectation(ham) - oracle.expectation(psi, ham)[0]) < E_TOL
+    with pytest.raises(P.SvError):
+        dm.expectation_with_grad(w.gates, [], ham)
+    dm.close()

@@ -350,3 +350,27 @@ def test_qaoa_zero_parameters():
     E, g = oracle.adjoint_grad(w.n, w.gates, z, w.ham)
     assert abs(E + len(w.meta["edges"]) / 2) < 1e-12
     np.testing.assert_allclose(g, 0, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- density matrices
+
+def test_density_oracle_pins():
+    """§3.2: pure-state rho equals |psi><psi| of the state-vector oracle (S:700 #5),
+    tr(rho) = 1, <H> = tr(rho H) equals the state-vector expectation, and a mixture is the convex
+    combination of its components (linearity of rho -> U rho U^dagger)."""
+    n = 3
+    w = W.random_complex(n, 4, seed=21, n_params=2)
+    psi = oracle.apply_circuit(n, w.gates, w.params)
+    rho = oracle.dm_apply_circuit(n, w.gates, w.params)
+    np.testing.assert_allclose(rho, np.outer(psi, psi.conj()), atol=1e-13)
+    assert abs(np.trace(rho) - 1) < 1e-13
+    ham = W.random_hamiltonian(n, 6, seed=3)
+    assert abs(oracle.dm_expectation(rho, ham) - oracle.expectation(psi, ham)[0]) < 1e-13
+    a, b = W.random_state(n, 1), W.random_state(n, 2)
+    mix = 0.3 * np.outer(a, a.conj()) + 0.7 * np.outer(b, b.conj())
+    out = oracle.dm_apply_circuit(n, w.gates, w.params, mix)
+    pa, pb = oracle.apply_circuit(n, w.gates, w.params, a), oracle.apply_circuit(n, w.gates, w.params, b)
+    np.testing.assert_allclose(out, 0.3 * np.outer(pa, pa.conj()) + 0.7 * np.outer(pb, pb.conj()), atol=1e-13)
+    # Pauli matrices vs Kronecker products (independent construction)
+    term = {0: "X", 2: "Y"}
+    np.testing.assert_allclose(oracle.pauli_matrix(n, term), B.kron_list({0: B.PX, 2: B.PY}, n), atol=1e-15)
