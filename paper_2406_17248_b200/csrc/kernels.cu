@@ -15,6 +15,7 @@
 // Gate classes follow the paper (§3.1): X-like (anti-diagonal, "swap with scaling"),
 // Z-like (diagonal, "no pairing"), general 2x2 pairs, two-qubit quads.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "cx.cuh"
@@ -681,11 +682,13 @@ int plan_grid(const Plan& plan, int n_local) {
   const PassDesc& pd = plan.passes[0];
   if (pd.R > 0) {
     const int64_t ntiles = 1ll << (n_local - pd.k);
-    // forward passes: two CTAs per SM (their phases interleave: one CTA's MMA stage overlaps the
-    // other's shared-memory / HBM phases); adjoint passes: one (register-heavy) CTA per SM
+    // forward passes: three 2^11-tile CTAs per SM (their phases interleave: one CTA's MMA stage
+    // overlaps the others' shared-memory / HBM phases); adjoint passes: two 2^10-tile CTAs per SM
     bool has_grad = false;
     for (const PassDesc& p : plan.passes) has_grad |= p.n_grad > 0;
-    const int64_t want = (int64_t)num_sms() * (has_grad ? 1 : 3);  // kernels_reg.cu SV_FWD_CTAS
+    static const int dual_ctas = [] { const char* e = getenv("SV_DUAL_CTAS"); return e ? atoi(e) : 2; }();
+    static const int fwd_ctas = [] { const char* e = getenv("SV_FWD_GRID_CTAS"); return e ? atoi(e) : 3; }();
+    const int64_t want = (int64_t)num_sms() * (has_grad ? dual_ctas : fwd_ctas);  // kernels_reg.cu SV_FWD_CTAS
     return (int)(ntiles < want ? ntiles : want);
   }
   return pass_grid(n_local, pd.k, false);

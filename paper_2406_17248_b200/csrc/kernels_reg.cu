@@ -31,7 +31,7 @@
 namespace sv {
 namespace {
 
-__device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ ((t >> 3 ^ t >> 6 ^ t >> 9 ^ t >> 12) & 7u); }
+__host__ __device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ ((t >> 3 ^ t >> 6 ^ t >> 9 ^ t >> 12) & 7u); }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -54,6 +54,10 @@ struct RegArgs {
   double* r_partials;  // adjoint dense stages: [da][warp][16 * 32][grid]
   int8_t tq[kMaxTileQubits + 3];
   int8_t oq[64];
+  // element e = tid + i * nthr: dep(i << nthr_bits) and swz(i << nthr_bits) per i (host-computed;
+  // kernel-parameter constants, no registers)
+  uint64_t hsub[8];
+  uint32_t zsub[8];
   int64_t ntiles;
   const RegOp* ops;
   const double* mats;
@@ -509,9 +513,10 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
   RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + 2 * NB);
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
   double* s_mats = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
-  const int nhi = 1 << (a.k - a.low);
-  uint64_t* s_hi = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
-  double* s_acc = reinterpret_cast<double*>(s_hi + nhi);  // [ngrad][nwarps]
+  // tile index -> base offset of its outer qubits: four 64-entry deposit tables (tile bits
+  // 6c .. 6c+5 -> their outer qubits), replacing a per-tile loop over n_outer bits
+  uint64_t* s_ob = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
+  double* s_acc = reinterpret_cast<double*>(s_ob + 4 * 64);  // [ngrad][nwarps]
   double* s_racc = s_acc + (DUAL ? a.ngrad * nwarps : 0);   // [n_da][nwarps][512]
 
   {
@@ -522,11 +527,13 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
     uint64_t* sd = reinterpret_cast<uint64_t*>(s_st);
     for (int i = tid; i < a.nstages * (int)(sizeof(StageDesc) / 8); i += nthr) sd[i] = ss[i];
     for (int i = tid; i < a.nmats; i += nthr) s_mats[i] = a.mats[i];
-    for (int h = tid; h < nhi; h += nthr) {
+    for (int h = tid; h < 4 * 64; h += nthr) {
       uint64_t off = 0;
-      for (int b = 0; b < a.k - a.low; ++b)
-        if ((h >> b) & 1) off |= 1ull << a.tq[a.low + b];
-      s_hi[h] = off;
+      for (int b = 0; b < 6; ++b) {
+        const int j = (h >> 6) * 6 + b;
+        if (((h >> b) & 1) && j < a.n_outer) off |= 1ull << a.oq[j];
+      }
+      s_ob[h] = off;
     }
     if (DUAL) {
       for (int i = tid; i < a.ngrad * nwarps; i += nthr) s_acc[i] = 0.0;
@@ -534,25 +541,35 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
     }
   }
   __syncthreads();
-  const uint32_t lowmask = (1u << a.low) - 1u;
   const int nthr_bits = a.k - NR;
   const double2* mats2 = reinterpret_cast<const double2*>(s_mats);
+  // Element e = tid + i * nthr of the tile (i < 2^NR): its global index is base | dep(tid) | dep(i << nthr_bits)
+  // and its shared slot swz(tid) ^ swz(i << nthr_bits) (dep and swz are XOR-linear), so the
+  // per-element index work is one OR and one XOR with kernel-parameter constants.
+  uint64_t dep_t = 0;
+  for (int b = 0; b < nthr_bits; ++b)
+    if ((tid >> b) & 1) dep_t |= 1ull << a.tq[b];
+  const uint32_t swz_t = swz((uint32_t)tid);
+  static_assert(NR == 3, "element split assumes 8 amplitudes per thread");
 
   // Double-buffered tiles: while the stages of tile i run from buffer (i & 1), cp.async streams
   // tile i + gridDim.x into the other buffer, so HBM reads overlap the FP64 work.
   auto tile_base = [&](int64_t tile) {
-    uint64_t base = 0;
-    for (int j = 0; j < a.n_outer; ++j)
+    uint64_t base = s_ob[tile & 63] | s_ob[64 + ((tile >> 6) & 63)] | s_ob[128 + ((tile >> 12) & 63)] |
+                    s_ob[192 + ((tile >> 18) & 63)];
+    for (int j = 24; j < a.n_outer; ++j)
       if ((tile >> j) & 1) base |= 1ull << a.oq[j];
     return base;
   };
   auto issue_load = [&](int64_t tile, int buf) {
-    const uint64_t base = tile_base(tile);
+    const uint64_t bt = tile_base(tile) | dep_t;
     double2* dp = tp + (size_t)buf * NB;
-    for (uint32_t e = tid; e < N; e += nthr) {
-      const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
-      cp_async16(dp + swz(e), psi + gi);
-      if (DUAL) cp_async16(dp + N + swz(e), lam + gi);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint64_t gi = bt | a.hsub[i];
+      const uint32_t sl = swz_t ^ a.zsub[i];
+      cp_async16(dp + sl, psi + gi);
+      if (DUAL) cp_async16(dp + N + sl, lam + gi);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -585,16 +602,14 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
       if constexpr (!DUAL) {
         // L1 prefetch of the next dense stage's variant-matrix fragments (global, L2-resident):
         // the first MMA of that stage then finds its A operand in L1 instead of waiting on L2
-        for (int nx = st + 1; nx < a.nstages; ++nx) {
-          const StageDesc& Sn = s_st[nx];
-          if (!Sn.dense) continue;
+        if (S.next_dense) {
+          const StageDesc& Sn = s_st[st + S.next_dense];
           uint32_t var = Sn.warp_var[warp];
           for (int b = 0; b < Sn.m_outer; ++b) var |= (uint32_t)((base >> Sn.var_outer[b]) & 1ull) << (Sn.m_tile + b);
           const double2* U = reinterpret_cast<const double2*>(a.mats) + Sn.dense_off + var * (16u * 20u);
           const double2* q = U + (lane >> 2) * 20 + (lane & 3) * 4;  // one 64-byte line per lane covers 4 entries
           asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q));
           asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q + 8 * 20));
-          break;
         }
         if (S.dense) {
           dense_stage(tp, S, reinterpret_cast<const double2*>(a.mats), base, warp, lane);
@@ -653,10 +668,15 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
       __syncthreads();
     }
     // ---- store: shared -> HBM (coalesced 16-byte) ----
-    for (uint32_t e = tid; e < N; e += nthr) {
-      const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
-      psi[gi] = tp[swz(e)];
-      if (DUAL) lam[gi] = tl[swz(e)];
+    {
+      const uint64_t bt = base | dep_t;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t gi = bt | a.hsub[i];
+        const uint32_t sl = swz_t ^ a.zsub[i];
+        psi[gi] = tp[sl];
+        if (DUAL) lam[gi] = tl[sl];
+      }
     }
     __syncthreads();
   }
@@ -677,7 +697,7 @@ size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngra
   size_t b = (size_t(16) << k) * (dual ? 2 : 1) * 2;  // double-buffered
   b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
   b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
-  b += (size_t)nmats * 8 + (size_t(8) << (k - low));
+  b += (size_t)nmats * 8 + 4 * 64 * 8;
   b += dual ? (size_t)ngrad * (nthr / 32) * 8 : 0;
   return b;
 }
@@ -701,6 +721,15 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   for (int q = 0; q < L.n_local; ++q)
     if (!((tmask >> q) & 1ull)) a.oq[a.n_outer++] = (int8_t)q;
   a.ntiles = 1ll << (L.n_local - pd.k);
+  {
+    const int tb = pd.k - pd.R;
+    for (int i = 0; i < 8; ++i) {
+      a.hsub[i] = 0;
+      for (int j = 0; j < 3; ++j)
+        if ((i >> j) & 1) a.hsub[i] |= 1ull << pd.tq[tb + j];
+      a.zsub[i] = swz((uint32_t)i << tb);
+    }
+  }
   a.ops = L.d_rops + pd.op_begin;
   a.mats = L.d_mats + pd.mat_begin;
   a.stages = L.d_stages + pd.stage_begin;

@@ -638,6 +638,11 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense) {
     plan->stages.push_back(sp.sd);
   }
   pd->stage_end = (int)plan->stages.size();
+  for (int i = pd->stage_begin; i < pd->stage_end; ++i) {
+    plan->stages[i].next_dense = 0;
+    for (int j = i + 1; j < pd->stage_end && j - i < 256; ++j)
+      if (plan->stages[j].dense) { plan->stages[i].next_dense = (uint8_t)(j - i); break; }
+  }
   int gl = 0;
   for (int i = pd->op_begin; i < pd->op_end; ++i)
     plan->ops[i].grad_local = (int16_t)(plan->ops[i].grad_slot >= 0 ? gl++ : -1);
@@ -646,7 +651,16 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense) {
 }  // namespace
 
 int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual) {
-  int kmax = 11;  // 2^11-amplitude tiles: 256 threads, two double-buffered CTAs per SM
+  // forward passes: 2^11-amplitude tiles (256 threads, three double-buffered CTAs per SM);
+  // adjoint (psi + lambda) passes: 2^10 (128 threads, two register-heavy CTAs per SM — measured
+  // 8-10% faster than one 2^11 CTA per SM on C2/C3/C4g, profiles/r01_dual_tile_sweep.txt)
+  int kmax = dual ? 10 : 11;
+  {
+    static const int dk = [] { const char* e = getenv("SV_DUAL_K"); return e ? atoi(e) : 0; }();
+    static const int fk = [] { const char* e = getenv("SV_FWD_K"); return e ? atoi(e) : 0; }();
+    if (dual && dk > 0) kmax = dk;
+    if (!dual && fk > 0) kmax = fk;
+  }
   if (o.tile_qubits > 0) kmax = std::min(o.tile_qubits, kMaxTileQubits);
   kmax = std::max(kmax, std::min(n_local, 2));  // a two-qubit gate must fit a tile
   if (n_local <= kmax) return n_local;

@@ -71,7 +71,7 @@ struct StageDesc {
   uint8_t dense;             // 1: dense MMA stage
   uint8_t m_tile;            // variant bits on warp positions (thrpos[4 .. 4+m_tile))
   uint8_t m_outer;           // variant bits on outer qubits (var_outer[0 .. m_outer))
-  uint8_t pad0;
+  uint8_t next_dense;        // distance to the pass' next dense stage (0: none; L1 prefetch)
   int8_t var_outer[8];
   uint32_t dense_off;        // dense: first variant matrix (double2 units in the pass' matrix block)
   uint16_t warp_swz[8];      // dense: swz(tile-position bits of warp w)
