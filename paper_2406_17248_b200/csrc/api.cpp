@@ -145,7 +145,9 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
     L.d_rops = reinterpret_cast<const RegOp*>(base + cp.ro);
     L.d_partials = d_partials;
     L.nmats = next_mat - pd.mat_begin;
-    L.grid = grid > 0 ? grid : plan_grid(plan, h->n_local);
+    const int pg = plan_grid(plan, h->n_local);  // fills plan.pass_grid
+    L.pstride = grid > 0 ? grid : pg;
+    L.grid = i < plan.pass_grid.size() ? std::min(plan.pass_grid[i], L.pstride) : L.pstride;
     L.n_local = h->n_local;
     L.rank_bits = 0;
     L.n_da = n_da;
@@ -692,6 +694,11 @@ int sv::run_reverse(sv_state_s* h, const CachedPlan& cp, double* psi, double* la
   double* dout = dp + part_slots;
   double* rp = dout + ns;
   double* rsum = rp + r_part;
+  // passes may run fewer CTAs than the plan grid: unwritten partial columns must read as zero
+  if (ns) {
+    cudaError_t ze = cudaMemsetAsync(dp, 0, part_slots * 8, h->stream);
+    if (ze != cudaSuccess) return cuda_fail(h, ze, "partials clear");
+  }
   int rc = run_plan(h, cp, psi, lam, dp, agrid, nda ? rp : nullptr, nda ? rsum : nullptr);
   if (rc) return rc;
   cudaError_t e = cudaSuccess;

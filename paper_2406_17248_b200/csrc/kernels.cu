@@ -14,6 +14,7 @@
 //
 // Gate classes follow the paper (§3.1): X-like (anti-diagonal, "swap with scaling"),
 // Z-like (diagonal, "no pairing"), general 2x2 pairs, two-qubit quads.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -677,21 +678,45 @@ int pass_grid(int n_local, int k, bool dual) {
 
 // One grid for every pass of a plan (the adjoint partials are laid out [slot][grid]): register
 // passes run one persistent, double-buffered CTA per SM; shared-memory passes two or more.
+static int plan_grid_uncached(const Plan& plan, int n_local);
+
 int plan_grid(const Plan& plan, int n_local) {
+  if (plan.grid_cache_n != n_local) {
+    plan.grid_cache = plan_grid_uncached(plan, n_local);
+    plan.grid_cache_n = n_local;
+  }
+  return plan.grid_cache;
+}
+
+static int plan_grid_uncached(const Plan& plan, int n_local) {
+  plan.pass_grid.assign(plan.passes.size(), 1);
   if (plan.passes.empty()) return 1;
   const PassDesc& pd = plan.passes[0];
   if (pd.R > 0) {
     const int64_t ntiles = 1ll << (n_local - pd.k);
-    // forward passes: three 2^11-tile CTAs per SM (their phases interleave: one CTA's MMA stage
-    // overlaps the others' shared-memory / HBM phases); adjoint passes: two 2^10-tile CTAs per SM
-    bool has_grad = false;
-    for (const PassDesc& p : plan.passes) has_grad |= p.n_grad > 0;
-    static const int dual_ctas = [] { const char* e = getenv("SV_DUAL_CTAS"); return e ? atoi(e) : 2; }();
-    static const int fwd_ctas = [] { const char* e = getenv("SV_FWD_GRID_CTAS"); return e ? atoi(e) : 3; }();
-    const int64_t want = (int64_t)num_sms() * (has_grad ? dual_ctas : fwd_ctas);  // kernels_reg.cu SV_FWD_CTAS
-    return (int)(ntiles < want ? ntiles : want);
+    // persistent grids sized by occupancy, pass by pass: forward passes run up to three 2^11-tile
+    // CTAs per SM (their phases interleave: one CTA's MMA stage overlaps the others' shared-memory /
+    // HBM phases), adjoint passes two 2^10-tile CTAs; fewer where a pass needs more shared memory.
+    // The plan's grid (the stride of the adjoint partials) is the largest pass grid.
+    const bool dual = plan.reverse;
+    static const int dual_env = [] { const char* e = getenv("SV_DUAL_CTAS"); return e ? atoi(e) : 0; }();
+    static const int fwd_env = [] { const char* e = getenv("SV_FWD_GRID_CTAS"); return e ? atoi(e) : 0; }();
+    const int env = dual ? dual_env : fwd_env;
+    int mx = 1;
+    for (size_t i = 0; i < plan.passes.size(); ++i) {
+      const PassDesc& p = plan.passes[i];
+      const int64_t nt = 1ll << (n_local - p.k);
+      const int ctas = env > 0 ? env : reg_pass_ctas_per_sm(plan, i, dual);
+      const int64_t want = (int64_t)num_sms() * ctas;
+      plan.pass_grid[i] = (int)(nt < want ? nt : want);
+      mx = std::max(mx, plan.pass_grid[i]);
+    }
+    (void)ntiles;
+    return mx;
   }
-  return pass_grid(n_local, pd.k, false);
+  const int g = pass_grid(n_local, pd.k, false);
+  plan.pass_grid.assign(plan.passes.size(), g);
+  return g;
 }
 
 cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStream_t s) {
@@ -712,7 +737,7 @@ cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStrea
   a.mats = L.d_mats + pd.mat_begin;
   a.nmats = L.nmats;
   a.partials = L.d_partials;
-  a.grid = L.grid;
+  a.grid = L.pstride > 0 ? L.pstride : L.grid;  // slot-row stride of the partials
   const bool dual = lam != nullptr;
   const size_t smem = pass_smem_bytes(a.k, a.low, a.nops, a.nmats, dual);
   static bool attr_set[2] = {false, false};

@@ -19,13 +19,15 @@
 // compile-time register indices with a control-free fast path, so the FP64 pipe sees long runs of
 // independent DFMAs; Z-like ops with a = 1 touch only half the amplitudes and CZ-type ops
 // (a = 1, b = -1) are sign flips without FP64 work.
+#include <algorithm>
 #include <cstdint>
 
 #include "cx.cuh"
 #include "sv_internal.h"
 
 #ifndef SV_FWD_CTAS
-#define SV_FWD_CTAS 3  // forward-pass CTAs per SM (register budget 65536 / (256 * CTAs))
+#define SV_FWD_CTAS 3   // forward-pass CTAs per SM (register budget 65536 / (256 * CTAs))
+#define SV_DUAL_CTAS 2  // adjoint-pass (2^10-tile, 128-thread) CTAs per SM (3 measured slower: 160-register cap)
 #endif
 
 namespace sv {
@@ -50,7 +52,7 @@ __device__ __forceinline__ double2 cneg(double2 a) { return make_double2(-a.x, -
 
 struct RegArgs {
   int32_t k, low, nops, nstages, n_outer, nmats, ngrad, grid;
-  int32_t n_da, pad_da;
+  int32_t n_da, pstride;  // pstride: slot-row stride of partials (>= grid)
   double* r_partials;  // adjoint dense stages: [da][warp][16 * 32][grid]
   int8_t tq[kMaxTileQubits + 3];
   int8_t oq[64];
@@ -369,6 +371,54 @@ __device__ __forceinline__ double reg_overlap_c(const double2 (&v)[1 << NR], con
 }
 
 
+// DUAL (adjoint) op with ONE register-position dispatch: the overlap Re<w|(Pi_C (x) G)|v> of a
+// parametrised op (before it is un-applied) and the un-application to v and w happen inside the same
+// case, so the compiler keeps one register assignment for v and w per op instead of reshuffling
+// both arrays at three separate switch joins.
+template <int NR, bool CTRL>
+__device__ __forceinline__ double dual_op_c(double2 (&v)[1 << NR], double2 (&w)[1 << NR], const Op& o, const double2* m,
+                                            const double2* g, uint32_t tthr, uint64_t base, bool ok) {
+  const uint32_t cj = o.cj();
+  double part = 0.0;
+  const bool gen = o.gen() != 0u;
+  switch (o.type()) {
+    case OP_M1: {
+#define C1(R)                                                   \
+  {                                                             \
+    if (gen && ok) part = reg_ov1<NR, R, CTRL>(v, w, g, cj);    \
+    if (ok) {                                                   \
+      reg_m1<NR, R, CTRL>(v, m, cj);                            \
+      reg_m1<NR, R, CTRL>(w, m, cj);                            \
+    }                                                           \
+  }
+      SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      break;
+    }
+    case OP_M2: {
+#define C2(A, B)                                                   \
+  {                                                                \
+    if (gen && ok) part = reg_ov2<NR, A, B, CTRL>(v, w, g, cj);    \
+    if (ok) {                                                      \
+      reg_m2<NR, A, B, CTRL>(v, m, cj);                            \
+      reg_m2<NR, A, B, CTRL>(w, m, cj);                            \
+    }                                                              \
+  }
+      SV_DISP2(NR, o.ra(), o.rb(), C2)
+#undef C2
+      break;
+    }
+    default: {
+      if (gen && ok) part = reg_overlap_c<NR, CTRL>(v, w, o, g, tthr, base);
+      if (ok) {
+        reg_apply_c<NR, CTRL>(v, o, m, tthr, base);
+        reg_apply_c<NR, CTRL>(w, o, m, tthr, base);
+      }
+    }
+  }
+  return part;
+}
+
 // ---------------------------------------------------------------- dense FP64-MMA stage
 //
 // The stage's ops were folded on the host into a 16x16 complex matrix U per variant; with
@@ -502,7 +552,7 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
 // ---------------------------------------------------------------- the pass kernel
 
 template <int NR, bool DUAL>
-__global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
+__global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD_CTAS) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
@@ -638,23 +688,20 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
       for (int i = S.op_begin; i < S.op_end; ++i) {
         const Op o = load_op(s_ops + i);
         const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
+        const double2* m = mats2 + o.mat_off();
         if constexpr (DUAL) {
+          const double2* g = mats2 + o.gen_off();
+          double part = o.cj() ? dual_op_c<NR, true>(v, w, o, m, g, tthr, base, ok)
+                               : dual_op_c<NR, false>(v, w, o, m, g, tthr, base, ok);
           if (o.gen()) {
-            double part = 0.0;
-            if (ok) {
-              const double2* g = mats2 + o.gen_off();
-              part = o.cj() ? reg_overlap_c<NR, true>(v, w, o, g, tthr, base)
-                          : reg_overlap_c<NR, false>(v, w, o, g, tthr, base);
-            }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
             if (lane == 0) s_acc[o.grad_local() * nwarps + warp] += part;
           }
+        } else {
+          if (!ok) continue;
+          reg_apply<NR>(v, o, m, tthr, base);
         }
-        if (!ok) continue;
-        const double2* m = mats2 + o.mat_off();
-        reg_apply<NR>(v, o, m, tthr, base);
-        if constexpr (DUAL) reg_apply<NR>(w, o, m, tthr, base);
       }
 #pragma unroll
       for (int j = 0; j < (1 << NR); ++j) {
@@ -688,7 +735,7 @@ __global__ void __launch_bounds__(256, DUAL ? 1 : SV_FWD_CTAS) k_pass_reg(double
       if (!o.gen()) continue;
       double s = 0.0;
       for (int wi = 0; wi < nwarps; ++wi) s += s_acc[o.grad_local() * nwarps + wi];
-      a.partials[(int64_t)s_ops[i].grad_slot * a.grid + blockIdx.x] = s;
+      a.partials[(int64_t)s_ops[i].grad_slot * a.pstride + blockIdx.x] = s;
     }
   }
 }
@@ -703,6 +750,34 @@ size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngra
 }
 
 }  // namespace
+
+static cudaError_t set_reg_attrs() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) done = true;
+  return e;
+}
+
+// Resident CTAs per SM for the register passes of a plan: the largest pass' shared memory decides
+// (one persistent grid serves every pass of the plan, so it must not exceed what is co-resident).
+int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual) {
+  if (set_reg_attrs() != cudaSuccess) return 1;
+  const PassDesc& pd = plan.passes[i];
+  if (pd.R == 0) return 1;
+  const int next_mat = (i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size();
+  const int nm = std::min(pd.seq_mats, next_mat - pd.mat_begin);
+  int n_da = 0;
+  for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? 1 : 0;
+  const int nthr = 1 << (pd.k - pd.R);
+  const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
+                                     pd.n_grad, nthr, dual, n_da);
+  int blocks = 0;
+  cudaError_t e = dual ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem)
+                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false>, nthr, smem);
+  return (e == cudaSuccess && blocks > 0) ? blocks : 1;
+}
 
 cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaStream_t s) {
   const PassDesc& pd = *L.pd;
@@ -737,17 +812,15 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   const bool dual = lam != nullptr;
   const int nthr = 1 << (pd.k - pd.R);
   a.n_da = L.n_da;
-  a.pad_da = 0;
+  a.pstride = L.pstride > 0 ? L.pstride : L.grid;
   a.r_partials = L.r_partials;
   const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual, a.n_da);
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[dual]) {
-    cudaError_t e = dual ? cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
-                         : cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  {
+    cudaError_t e = set_reg_attrs();
     if (e != cudaSuccess) return e;
-    attr_set[dual] = true;
   }
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (dual && nthr > 128) return cudaErrorInvalidValue;  // adjoint passes run 2^10-amplitude tiles
   if (dual) {
     if (pd.R != 3) return cudaErrorInvalidValue;
     k_pass_reg<3, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);

@@ -662,6 +662,7 @@ int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual) {
     if (!dual && fk > 0) kmax = fk;
   }
   if (o.tile_qubits > 0) kmax = std::min(o.tile_qubits, kMaxTileQubits);
+  if (dual) kmax = std::min(kmax, 10);  // the DUAL register kernel runs 128-thread CTAs
   kmax = std::max(kmax, std::min(n_local, 2));  // a two-qubit gate must fit a tile
   if (n_local <= kmax) return n_local;
   // keep at least ~2^9 tiles in flight for small states (L2-resident, latency-bound).
@@ -732,6 +733,10 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
 
   // ---- 2. emit passes (forward order, or reversed with daggered ops for the adjoint sweep) ----
   plan->passes.clear();
+  plan->reverse = reverse;
+  plan->grid_cache = 0;
+  plan->grid_cache_n = -1;  // the plan_grid memo belongs to the plan being replaced
+  plan->pass_grid.clear();
   plan->ops.clear();
   plan->mats.clear();
   plan->stages.clear();

@@ -144,6 +144,9 @@ struct Plan {
   };
   std::vector<DAStage> da;
   int max_da_per_pass = 0;
+  bool reverse = false;  // adjoint plan: passes run on (psi, lambda) with the DUAL kernel
+  mutable int grid_cache = 0, grid_cache_n = -1;  // plan_grid memo (occupancy query once per plan)
+  mutable std::vector<int> pass_grid;             // per-pass CTAs (register passes: occupancy of that pass)
 };
 constexpr int kMaxDAPerPass = 2;  // R accumulators: 32 KiB of shared memory per adjoint dense stage
 
@@ -195,6 +198,7 @@ struct PassLaunch {
   int n_da = 0;            // adjoint dense stages of this pass
   double* r_partials = nullptr;  // their R accumulators: [da][warp][512][grid]
   int grid;                // CTAs
+  int pstride = 0;         // stride of d_partials' slot rows (>= grid; 0: grid)
   int n_local;
   uint64_t rank_bits;      // (sharded) global index bits of this shard, for controls/diagonals on
                            // global qubits folded by the planner (0 single-GPU)
@@ -203,6 +207,7 @@ cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStrea
 cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
 int pass_grid(int n_local, int k, bool dual);
 int plan_grid(const Plan& plan, int n_local);
+int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual);  // resident CTAs/SM of a register pass
 
 cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
 // Sharding: swap halves of two virtual shards (a[y0|2^l] <-> b[y0]); pack / unpack the half of a
