@@ -371,6 +371,65 @@ __device__ __forceinline__ double reg_overlap_c(const double2 (&v)[1 << NR], con
 }
 
 
+// DUAL diagonal op (Z-like, 1 or 2 targets) with compile-time target positions: RA / RB in
+// [0, NR) are register bits, -1 a thread / outer bit whose value (ta / tb) is uniform over the
+// thread's amplitudes (the entries are pre-selected once per op), -2 "no second target". Returns
+// this thread's Re<w|(Pi_C (x) G)|v> (diagonal generator) before un-applying the op to v and w.
+template <int NR, int RA, int RB, bool CTRL>
+__device__ __forceinline__ double dual_diag(double2 (&v)[1 << NR], double2 (&w)[1 << NR], const double2* m,
+                                            const double2* g, bool gen, bool g2, uint32_t cj, uint32_t ta,
+                                            uint32_t tb, bool ok) {
+  constexpr bool TWO = RB != -2;
+  double2 d[4], q[4];
+  d[0] = lds(m);
+  d[1] = lds(m + 1);
+  if (TWO) {
+    d[2] = lds(m + 2);
+    d[3] = lds(m + 3);
+  }
+  if (gen) {
+    q[0] = lds(g);
+    q[1] = lds(g + 1);
+    q[2] = g2 ? lds(g + 2) : q[0];
+    q[3] = g2 ? lds(g + 3) : q[1];
+  } else {
+    q[0] = q[1] = q[2] = q[3] = make_double2(0.0, 0.0);
+  }
+  if (!TWO) {
+    d[2] = d[0];
+    d[3] = d[1];
+  }
+  // uniform target bits: fold them into the entry index once
+  if (RA == -1) {
+    d[0] = ta ? d[1] : d[0];
+    d[2] = ta ? d[3] : d[2];
+    q[0] = ta ? q[1] : q[0];
+    q[2] = ta ? q[3] : q[2];
+  }
+  if (RB == -1) {
+    d[0] = tb ? d[2] : d[0];
+    d[1] = tb ? d[3] : d[1];
+    q[0] = tb ? q[2] : q[0];
+    q[1] = tb ? q[3] : q[1];
+  }
+  double acc = 0.0;
+  if (!ok) return 0.0;
+#pragma unroll
+  for (int j = 0; j < (1 << NR); ++j) {
+    SV_CTRL_SKIP(j)
+    const int i0 = RA >= 0 ? ((j >> RA) & 1) : 0;
+    const int i1 = RB >= 0 ? ((j >> RB) & 1) : 0;
+    const int idx = i0 | (i1 << 1);
+    if (gen) {
+      const double2 p = make_double2(fma(w[j].x, v[j].x, w[j].y * v[j].y), fma(w[j].x, v[j].y, -w[j].y * v[j].x));
+      acc += fma(q[idx].x, p.x, -q[idx].y * p.y);  // Re(g conj(w) v)
+    }
+    v[j] = cmul(d[idx], v[j]);
+    w[j] = cmul(d[idx], w[j]);
+  }
+  return acc;
+}
+
 // DUAL (adjoint) op with ONE register-position dispatch: the overlap Re<w|(Pi_C (x) G)|v> of a
 // parametrised op (before it is un-applied) and the un-application to v and w happen inside the same
 // case, so the compiler keeps one register assignment for v and w per op instead of reshuffling
@@ -406,6 +465,41 @@ __device__ __forceinline__ double dual_op_c(double2 (&v)[1 << NR], double2 (&w)[
   }
       SV_DISP2(NR, o.ra(), o.rb(), C2)
 #undef C2
+      break;
+    }
+    case OP_D1: {
+      const uint32_t ta = o.pa() != 31u ? (tthr >> o.pa()) & 1u : (uint32_t)((base >> o.qa()) & 1ull);
+      const bool g2 = o.gen() == 2u;
+      switch (o.ra()) {
+        case 0: part = dual_diag<NR, 0, -2, CTRL>(v, w, m, g, gen, g2, cj, ta, 0, ok); break;
+        case 1: part = dual_diag<NR, 1, -2, CTRL>(v, w, m, g, gen, g2, cj, ta, 0, ok); break;
+        case 2: part = dual_diag<NR, 2, -2, CTRL>(v, w, m, g, gen, g2, cj, ta, 0, ok); break;
+        default: part = dual_diag<NR, -1, -2, CTRL>(v, w, m, g, gen, g2, cj, ta, 0, ok); break;
+      }
+      break;
+    }
+    case OP_D2: {
+      const uint32_t ta = o.pa() != 31u ? (tthr >> o.pa()) & 1u : (uint32_t)((base >> o.qa()) & 1ull);
+      const uint32_t tb = o.pb() != 31u ? (tthr >> o.pb()) & 1u : (uint32_t)((base >> o.qb()) & 1ull);
+      const bool g2 = o.gen() == 2u;
+      const uint32_t ra = o.ra() > 2u ? 3u : o.ra(), rb = o.rb() > 2u ? 3u : o.rb();
+#define CD(A, B) part = dual_diag<NR, A, B, CTRL>(v, w, m, g, gen, g2, cj, ta, tb, ok)
+      switch (ra * 4 + rb) {
+        case 1: CD(0, 1); break;
+        case 2: CD(0, 2); break;
+        case 3: CD(0, -1); break;
+        case 4: CD(1, 0); break;
+        case 6: CD(1, 2); break;
+        case 7: CD(1, -1); break;
+        case 8: CD(2, 0); break;
+        case 9: CD(2, 1); break;
+        case 11: CD(2, -1); break;
+        case 12: CD(-1, 0); break;
+        case 13: CD(-1, 1); break;
+        case 14: CD(-1, 2); break;
+        default: CD(-1, -1); break;
+      }
+#undef CD
       break;
     }
     default: {
