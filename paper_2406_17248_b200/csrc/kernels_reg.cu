@@ -215,6 +215,23 @@ __device__ __forceinline__ void reg_swap(double2 (&v)[1 << NR], uint32_t cj) {
   }
 }
 
+// Same with an anti-diagonal G (the generators of RX, RY: -i/2 X, -i/2 Y): half the products.
+template <int NR, int RB, bool CTRL>
+__device__ __forceinline__ double reg_ov1_anti(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR],
+                                               const double2* g, uint32_t cj) {
+  const double2 g01 = g[1], g10 = g[2];
+  double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < (1 << NR); ++j) {
+    if (j & (1 << RB)) continue;
+    SV_CTRL_SKIP(j)
+    const int j1 = j | (1 << RB);
+    acc0 += re_conj_mul(w[j], cmul(g01, v[j1]));
+    acc1 += re_conj_mul(w[j1], cmul(g10, v[j]));
+  }
+  return acc0 + acc1;
+}
+
 // Re <w| (Pi_C (x) G) |v> over this thread's amplitudes, G on register bit RB (2x2).
 template <int NR, int RB, bool CTRL>
 __device__ __forceinline__ double reg_ov1(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR], const double2* g,
@@ -442,9 +459,14 @@ __device__ __forceinline__ double dual_op_c(double2 (&v)[1 << NR], double2 (&w)[
   const bool gen = o.gen() != 0u;
   switch (o.type()) {
     case OP_M1: {
+      bool anti = false;
+      if (gen) {
+        const double2 g00 = lds(g), g11 = lds(g + 3);
+        anti = g00.x == 0.0 && g00.y == 0.0 && g11.x == 0.0 && g11.y == 0.0;
+      }
 #define C1(R)                                                   \
   {                                                             \
-    if (gen && ok) part = reg_ov1<NR, R, CTRL>(v, w, g, cj);    \
+    if (gen && ok) part = anti ? reg_ov1_anti<NR, R, CTRL>(v, w, g, cj) : reg_ov1<NR, R, CTRL>(v, w, g, cj); \
     if (ok) {                                                   \
       reg_m1<NR, R, CTRL>(v, m, cj);                            \
       reg_m1<NR, R, CTRL>(w, m, cj);                            \
