@@ -27,7 +27,7 @@
 
 #ifndef SV_FWD_CTAS
 #define SV_FWD_CTAS 3   // forward-pass CTAs per SM (register budget 65536 / (256 * CTAs))
-#define SV_DUAL_CTAS 2  // adjoint-pass (2^10-tile, 128-thread) CTAs per SM (3 measured slower: 160-register cap)
+#define SV_DUAL_CTAS 3  // adjoint-pass (2^10-tile, 128-thread) CTAs per SM (register cap 65536 / (128 * 3))
 #endif
 
 namespace sv {
