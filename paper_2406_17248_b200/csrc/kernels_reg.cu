@@ -542,6 +542,8 @@ __device__ __forceinline__ double dual_op_c(double2 (&v)[1 << NR], double2 (&w)[
 // real 32 x 32 x 2^(k-4) GEMM, run as mma.sync m8n8k4 f64 (DMMA): per warp 4 N-tiles of 8 vectors,
 // 4 M-tiles x 8 K-tiles. Fragment layouts (PTX m8n8k4 .f64): A[r = lane/4][c = lane%4],
 // B[k = lane%4][n = lane/4], D[r = lane/4][c = 2 (lane%4) + {0,1}].
+constexpr uint32_t kDenseRow = 16;  // complex entries per stored variant-matrix row (plan.cpp kDenseStride)
+
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -561,12 +563,12 @@ __device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, con
   // host-precomputed swizzled offsets (the swizzle is XOR-linear)
   uint32_t var = S.warp_var[warp];
   for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
-  const double2* U = gmats2 + S.dense_off + var * (16u * 20u);  // global (L1/L2-resident)
+  const double2* U = gmats2 + S.dense_off + var * (16u * kDenseRow);  // global (L1/L2-resident)
   double2 ue[2][4];
 #pragma unroll
   for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
-    for (int kh = 0; kh < 4; ++kh) ue[mh][kh] = __ldg(U + (8 * mh + (lane >> 2)) * 20 + 4 * kh + (lane & 3));
+    for (int kh = 0; kh < 4; ++kh) ue[mh][kh] = __ldg(U + (8 * mh + (lane >> 2)) * kDenseRow + 4 * kh + (lane & 3));
   const uint32_t wsw = S.warp_swz[warp];
   const uint32_t baseB = wsw ^ S.lane_b[lane];
   double b[2][8];
@@ -772,10 +774,10 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
           const StageDesc& Sn = s_st[st + S.next_dense];
           uint32_t var = Sn.warp_var[warp];
           for (int b = 0; b < Sn.m_outer; ++b) var |= (uint32_t)((base >> Sn.var_outer[b]) & 1ull) << (Sn.m_tile + b);
-          const double2* U = reinterpret_cast<const double2*>(a.mats) + Sn.dense_off + var * (16u * 20u);
-          const double2* q = U + (lane >> 2) * 20 + (lane & 3) * 4;  // one 64-byte line per lane covers 4 entries
+          const double2* U = reinterpret_cast<const double2*>(a.mats) + Sn.dense_off + var * (16u * kDenseRow);
+          const double2* q = U + (lane >> 2) * kDenseRow + (lane & 3) * 4;  // one 64-byte line per lane covers 4 entries
           asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q));
-          asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q + 8 * 20));
+          asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q + 8 * kDenseRow));
         }
         if (S.dense) {
           dense_stage(tp, S, reinterpret_cast<const double2*>(a.mats), base, warp, lane);

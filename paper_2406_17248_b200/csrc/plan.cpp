@@ -215,7 +215,7 @@ void layout_sequential(StagePlan* sp, const PassDesc& pd, int R) {
 
 // ---------------------------------------------------------------- dense (FP64-MMA) stages
 
-constexpr int kDenseStride = 20;  // complex entries per row of a stored variant matrix
+constexpr int kDenseStride = 16;  // complex entries per row of a stored variant matrix (kernels_reg.cu kDenseRow)
 // Dense-stage policy (tunable by environment for A/B runs): minimum sequential FP64 cost
 // (FMA/amp) worth a 64 FMA/amp dense stage, and the maximum number of variant bits.
 int env_int(const char* name, int dflt) {

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256, 3) k_stage(const double2* __restrict__ gm
   for (int r = 0; r < reps; ++r) {
     for (int s = 0; s < stages; ++s) {
       if (MODE & 1) {
-        const double2* Us = gm + ((s + blockIdx.x) & 7) * 320;
+        const double2* Us = gm + ((s * 37 + blockIdx.x * 11 + r * 5) & (MODE & 8 ? 255 : 7)) * 320;
 #pragma unroll
         for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
@@ -122,8 +122,8 @@ void run(const double2* gm, double* out, int blocks_per_sm, int sms) {
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
   const double flops = (double)grid * 8 * 64 * 512.0 * stages * reps;
-  printf("{\"mode\":%d,\"a_global\":%d,\"bd_smem\":%d,\"barrier\":%d,\"blocks_per_sm\":%d,\"ms\":%.3f,\"tflops\":%.2f}\n",
-         MODE, MODE & 1, (MODE >> 1) & 1, (MODE >> 2) & 1, blocks_per_sm, ms, flops / ms / 1e9);
+  printf("{\"mode\":%d,\"a_l2\":%d,\"a_global\":%d,\"bd_smem\":%d,\"barrier\":%d,\"blocks_per_sm\":%d,\"ms\":%.3f,\"tflops\":%.2f}\n",
+         MODE, (MODE >> 3) & 1, MODE & 1, (MODE >> 1) & 1, (MODE >> 2) & 1, blocks_per_sm, ms, flops / ms / 1e9);
 }
 
 int main() {
@@ -131,8 +131,8 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double2* gm;
   double* out;
-  cudaMalloc(&gm, 8 * 320 * sizeof(double2));
-  cudaMemset(gm, 0, 8 * 320 * sizeof(double2));
+  cudaMalloc(&gm, 256 * 320 * sizeof(double2));
+  cudaMemset(gm, 0, 256 * 320 * sizeof(double2));
   cudaMalloc(&out, 8);
   for (int bps : {2, 3}) {
     run<0>(gm, out, bps, sms);
@@ -141,6 +141,7 @@ int main() {
     run<4>(gm, out, bps, sms);
     run<6>(gm, out, bps, sms);
     run<7>(gm, out, bps, sms);
+    run<15>(gm, out, bps, sms);
   }
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
