@@ -21,6 +21,7 @@
 // (a = 1, b = -1) are sign flips without FP64 work.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "cx.cuh"
 #include "sv_internal.h"
@@ -557,18 +558,22 @@ __device__ __forceinline__ double lds64(const double* p) {
   return r;
 }
 
-__device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, const double2* __restrict__ gmats2,
-                                            uint64_t base, int warp, int lane) {
-  // warp-owned vectors: 2 N-tiles (n0) x 8 MMA columns (c0 c1 c2); all address parts are
-  // host-precomputed swizzled offsets (the swizzle is XOR-linear)
+// A operand of a dense stage: this warp's variant matrix (global, L2-resident), 8 entries per lane.
+__device__ __forceinline__ void dense_load_a(const StageDesc& S, const double2* __restrict__ gmats2, uint64_t base,
+                                             int warp, int lane, double2 (&ue)[2][4]) {
   uint32_t var = S.warp_var[warp];
   for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
-  const double2* U = gmats2 + S.dense_off + var * (16u * kDenseRow);  // global (L1/L2-resident)
-  double2 ue[2][4];
+  const double2* U = gmats2 + S.dense_off + var * (16u * kDenseRow);
 #pragma unroll
   for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
     for (int kh = 0; kh < 4; ++kh) ue[mh][kh] = __ldg(U + (8 * mh + (lane >> 2)) * kDenseRow + 4 * kh + (lane & 3));
+}
+
+// warp-owned vectors: 2 N-tiles (n0) x 8 MMA columns (c0 c1 c2); all address parts are
+// host-precomputed swizzled offsets (the swizzle is XOR-linear)
+__device__ __forceinline__ void dense_apply_a(double2* tp, const StageDesc& S, const double2 (&ue)[2][4], int warp,
+                                              int lane) {
   const uint32_t wsw = S.warp_swz[warp];
   const uint32_t baseB = wsw ^ S.lane_b[lane];
   double b[2][8];
@@ -616,6 +621,13 @@ __device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, con
         tp[baseD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]] = make_double2(d[mh][nt][v], d[mh + 2][nt][v]);
 }
 
+
+__device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, const double2* __restrict__ gmats2,
+                                            uint64_t base, int warp, int lane) {
+  double2 ue[2][4];
+  dense_load_a(S, gmats2, base, warp, lane, ue);
+  dense_apply_a(tp, S, ue, warp, lane);
+}
 
 // Adjoint dense stage (DUAL): accumulate R = sum_v psi_v lambda_v^H over the warp's 16 vectors at
 // the stage start (FP64 MMAs with K = vectors) into the warp's private shared-memory accumulator,
@@ -858,6 +870,89 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   }
 }
 
+// ---------------------------------------------------------------- all-dense forward passes
+//
+// Most forward passes of deep circuits consist of dense stages only (C4: 53 of 58). For them a
+// leaner kernel: no op list, no sequential-stage code, so the register budget of three CTAs per SM
+// leaves room to load the next stage's A operand (its variant matrix, from L2) into registers
+// before the barrier that ends the current stage, and the first stage's before the tile wait:
+// the L2 latency overlaps barrier / load waits instead of stalling the first MMA of every stage.
+__global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __restrict__ psi, RegArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t N = 1u << a.k;
+  const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double2* smem_tiles = reinterpret_cast<double2*>(smem_raw);
+  StageDesc* s_st = reinterpret_cast<StageDesc*>(smem_tiles + 2 * N);
+  uint64_t* s_ob = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
+  {
+    const uint64_t* ss = reinterpret_cast<const uint64_t*>(a.stages);
+    uint64_t* sd = reinterpret_cast<uint64_t*>(s_st);
+    for (int i = tid; i < a.nstages * (int)(sizeof(StageDesc) / 8); i += nthr) sd[i] = ss[i];
+    for (int h = tid; h < 4 * 64; h += nthr) {
+      uint64_t off = 0;
+      for (int b = 0; b < 6; ++b) {
+        const int j = (h >> 6) * 6 + b;
+        if (((h >> b) & 1) && j < a.n_outer) off |= 1ull << a.oq[j];
+      }
+      s_ob[h] = off;
+    }
+  }
+  __syncthreads();
+  const int nthr_bits = a.k - 3;
+  uint64_t dep_t = 0;
+  for (int b = 0; b < nthr_bits; ++b)
+    if ((tid >> b) & 1) dep_t |= 1ull << a.tq[b];
+  const uint32_t swz_t = swz((uint32_t)tid);
+  const double2* gm2 = reinterpret_cast<const double2*>(a.mats);
+  auto tile_base = [&](int64_t tile) {
+    uint64_t base = s_ob[tile & 63] | s_ob[64 + ((tile >> 6) & 63)] | s_ob[128 + ((tile >> 12) & 63)] |
+                    s_ob[192 + ((tile >> 18) & 63)];
+    for (int j = 24; j < a.n_outer; ++j)
+      if ((tile >> j) & 1) base |= 1ull << a.oq[j];
+    return base;
+  };
+  auto issue_load = [&](int64_t tile, int buf) {
+    const uint64_t bt = tile_base(tile) | dep_t;
+    double2* dp = smem_tiles + (size_t)buf * N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cp_async16(dp + (swz_t ^ a.zsub[i]), psi + (bt | a.hsub[i]));
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if ((int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
+  double2 ue[2][4];
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+    const int cur = it & 1;
+    const uint64_t base = tile_base(tile);
+    const int64_t next = tile + gridDim.x;
+    dense_load_a(s_st[0], gm2, base, warp, lane, ue);
+    if (next < a.ntiles) {
+      issue_load(next, cur ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    double2* tp = smem_tiles + (size_t)cur * N;
+    for (int st = 0; st < a.nstages; ++st) {
+      dense_apply_a(tp, s_st[st], ue, warp, lane);
+      if (st + 1 < a.nstages) dense_load_a(s_st[st + 1], gm2, base, warp, lane, ue);
+      __syncthreads();
+    }
+    {
+      const uint64_t bt = base | dep_t;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) psi[bt | a.hsub[i]] = tp[swz_t ^ a.zsub[i]];
+    }
+    __syncthreads();
+  }
+}
+
+size_t dense_pass_smem_bytes(int k, int nstages) {
+  return (size_t(16) << k) * 2 + (size_t)nstages * sizeof(StageDesc) + 16 + 4 * 64 * 8;
+}
+
+
 size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da) {
   size_t b = (size_t(16) << k) * (dual ? 2 : 1) * 2;  // double-buffered
   b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
@@ -869,11 +964,20 @@ size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngra
 
 }  // namespace
 
+bool pass_all_dense(const Plan& plan, const PassDesc& pd) {
+  static const bool off = [] { const char* e = getenv("SV_DENSE_KERNEL"); return e && atoi(e) == 0; }();
+  if (off || plan.reverse || pd.R != 3 || pd.stage_end <= pd.stage_begin) return false;
+  for (int si = pd.stage_begin; si < pd.stage_end; ++si)
+    if (plan.stages[si].dense != 1) return false;
+  return true;
+}
+
 static cudaError_t set_reg_attrs() {
   static bool done = false;
   if (done) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e == cudaSuccess) done = true;
   return e;
 }
@@ -892,6 +996,11 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual) {
   const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
                                      pd.n_grad, nthr, dual, n_da);
   int blocks = 0;
+  if (pass_all_dense(plan, pd)) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense, nthr,
+                                                                  dense_pass_smem_bytes(pd.k, pd.stage_end - pd.stage_begin));
+    return (e == cudaSuccess && blocks > 0) ? blocks : 1;
+  }
   cudaError_t e = dual ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem)
                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false>, nthr, smem);
   return (e == cudaSuccess && blocks > 0) ? blocks : 1;
@@ -944,7 +1053,11 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
     k_pass_reg<3, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
   } else {
     if (pd.R != 3) return cudaErrorInvalidValue;
-    k_pass_reg<3, false><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
+    if (L.all_dense) {
+      k_pass_dense<<<L.grid, nthr, dense_pass_smem_bytes(a.k, a.nstages), s>>>(reinterpret_cast<double2*>(psi), a);
+    } else {
+      k_pass_reg<3, false><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
+    }
   }
   return cudaGetLastError();
 }

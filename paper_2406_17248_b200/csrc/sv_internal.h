@@ -199,6 +199,7 @@ struct PassLaunch {
   double* r_partials = nullptr;  // their R accumulators: [da][warp][512][grid]
   int grid;                // CTAs
   int pstride = 0;         // stride of d_partials' slot rows (>= grid; 0: grid)
+  bool all_dense = false;  // forward register pass of dense stages only (k_pass_dense)
   int n_local;
   uint64_t rank_bits;      // (sharded) global index bits of this shard, for controls/diagonals on
                            // global qubits folded by the planner (0 single-GPU)
@@ -207,7 +208,8 @@ cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStrea
 cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
 int pass_grid(int n_local, int k, bool dual);
 int plan_grid(const Plan& plan, int n_local);
-int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual);  // resident CTAs/SM of a register pass
+int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual);
+bool pass_all_dense(const Plan& plan, const PassDesc& pd);  // k_pass_dense eligible  // resident CTAs/SM of a register pass
 
 cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
 // Sharding: swap halves of two virtual shards (a[y0|2^l] <-> b[y0]); pack / unpack the half of a
