@@ -39,7 +39,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_TFLOPS = 36.9  # measured FP64 tensor (DMMA) peak = DMMA+DFMA mixed peak on this pool's B200
 # dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
 # --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
-TRAFFIC_PER_LAUNCH = {"C4": (17.183848 + 17.122593) * 1e9}  # profiles/r01_ncu_pass30_full.txt
+TRAFFIC_PER_LAUNCH = {"C4": (17.220996 + 17.460672) * 1e9}  # profiles/r01_ncu_pass30_full.txt (k_pass_dense)
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
 
@@ -361,7 +361,7 @@ def main():
         fma_per_amp = sum(p["fma_per_amp"] for p in plan)
         fp64_flops = 2.0 * fma_per_amp * amps  # algorithmic FP64 work of the executed plan
         roof = {
-            "bound": "tensor", "kernel": "k_pass_reg<3,false> (fused forward tile pass: FP64 DMMA + DFMA stages)",
+            "bound": "tensor", "kernel": "k_pass_dense / k_pass_reg<3,false> (fused forward tile passes: FP64 DMMA dense stages + register stages)",
             "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
             "peak_source": "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
                            "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)",

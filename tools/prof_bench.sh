@@ -12,6 +12,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 echo "launches_rc=$?"
 # full capture of one steady-state forward pass at 30q
 python tools/prof_pass.py 30 40 > gpurun_out/prof30_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_pass_reg -s 70 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:k_pass -s 70 -c 1 \
     -o gpurun_out/prof_pass30 python tools/prof_pass.py 30 40 > gpurun_out/ncu_full.log 2>&1
 echo "full_rc=$?"
