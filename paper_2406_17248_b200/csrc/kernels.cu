@@ -408,6 +408,16 @@ struct PauliTileArgs {
   double* partials;
 };
 
+// Walsh row of a 4-bit mask h: bit j (j < 16) = parity(j & h).
+__device__ __forceinline__ uint32_t walsh16(uint32_t h) {
+  uint32_t r = 0;
+  if (h & 1u) r ^= 0xAAAAu;  // bit 0 of j
+  if (h & 2u) r ^= 0xCCCCu;  // bit 1
+  if (h & 4u) r ^= 0xF0F0u;  // bit 2
+  if (h & 8u) r ^= 0xFF00u;  // bit 3
+  return r;
+}
+
 __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restrict__ psi, double2* __restrict__ lam,
                                                          PauliTileArgs a) {
   // Per tile the rank / outer-bit part of every term's sign is folded into its coefficient; per
@@ -485,26 +495,46 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
       double2 l[EPT];
 #pragma unroll
       for (int j = 0; j < EPT; ++j) l[j] = make_double2(0.0, 0.0);
+      // e = tid + 256 j: the sign (-1)^{popc(e & zt)} factors into a per-thread part
+      // (-1)^{popc(tid & zt)}, folded into the coefficient once per term, and a j part read from
+      // the term's 16-bit Walsh row W(zt >> 8) (bit j = parity(j & (zt >> 8))). A single-term
+      // group needs no accumulation at all: its j sign goes onto the product.
+      const uint32_t tid = threadIdx.x;
       for (int g = 0; g < a.ngroups; ++g) {
+        const uint32_t xt = a.xtile[g];
+        const int tb = a.tbeg[g], te = a.tend[g];
+        if (te - tb == 1) {
+          const uint32_t zt = s_zt[tb];
+          double2 c = s_c[tb];
+          if (__popc(tid & zt & 0xffu) & 1) c = make_double2(-c.x, -c.y);
+          const uint32_t wr = walsh16(zt >> 8);
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) {
+            const double2 w = cmul(c, tp[(tid + (uint32_t)j * 256u) ^ xt]);
+            const bool neg = (wr >> j) & 1u;
+            l[j].x += neg ? -w.x : w.x;
+            l[j].y += neg ? -w.y : w.y;
+          }
+          continue;
+        }
         double2 C[EPT];
 #pragma unroll
         for (int j = 0; j < EPT; ++j) C[j] = make_double2(0.0, 0.0);
-        for (int t = a.tbeg[g]; t < a.tend[g]; ++t) {
+        for (int t = tb; t < te; ++t) {
           const uint32_t zt = s_zt[t];
-          const double2 c = s_c[t];
+          double2 c = s_c[t];
+          if (__popc(tid & zt & 0xffu) & 1) c = make_double2(-c.x, -c.y);
+          const uint32_t wr = walsh16(zt >> 8);
 #pragma unroll
           for (int j = 0; j < EPT; ++j) {
-            const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
-            const bool neg = __popc(e & zt) & 1;
+            const bool neg = (wr >> j) & 1u;
             C[j].x += neg ? -c.x : c.x;
             C[j].y += neg ? -c.y : c.y;
           }
         }
-        const uint32_t xt = a.xtile[g];
 #pragma unroll
         for (int j = 0; j < EPT; ++j) {
-          const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
-          const double2 w = cmul(C[j], tp[e ^ xt]);
+          const double2 w = cmul(C[j], tp[(tid + (uint32_t)j * 256u) ^ xt]);
           l[j].x += w.x;
           l[j].y += w.y;
         }
