@@ -40,6 +40,7 @@ FP64_PEAK_TFLOPS = 36.9  # measured FP64 tensor (DMMA) peak = DMMA+DFMA mixed pe
 # dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
 # --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
 TRAFFIC_PER_LAUNCH = {"C4": (17.220996 + 17.460672) * 1e9}  # profiles/r01_ncu_pass30_full.txt (k_pass_dense)
+TRAFFIC_PER_LAUNCH_C64 = None  # complex64 pass: not captured yet
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
 
@@ -258,6 +259,8 @@ def main():
                     help="run the sharded path with P virtual shards on one GPU (tests the N>1 executor)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-grad", action="store_true")
+    ap.add_argument("--precision", default="c128", choices=["c128", "c64"],
+                    help="c64: NEXT-3 complex64 state (single GPU; the gradient leg stays complex128)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -299,6 +302,8 @@ def main():
         sv = PD.create_sharded(n)
     elif shards > 1:
         sv = P.StateVector(n, handle=P.sv_create_virtual_shards(n, shards))
+    elif args.precision == "c64":
+        sv = P.StateVectorC64(n)
     else:
         sv = P.StateVector(n)
     stream = torch.cuda.Stream()  # a real stream object: its handle is passed to the library
@@ -351,22 +356,25 @@ def main():
     hbm_peak, peak_src = _peaks()
     amps = amps_total / shards  # per GPU shard
     pass_ms = circ_ms / max(passes, 1)
-    pass_bytes = 32.0 * amps
+    pass_bytes = (16.0 if args.precision == "c64" else 32.0) * amps
     achieved = pass_bytes / (pass_ms / 1e3) / 1e9
     plan_bytes = st["algorithmic_bytes"] / args.steps / (1 if world > 1 else shards)
-    eff_bytes = sum(32.0 * amps_total / (1 << len(g.controls)) for g in w.gates)
+    eff_bytes = sum((16.0 if args.precision == "c64" else 32.0) * amps_total / (1 << len(g.controls)) for g in w.gates)
     roof = None
     if shards == 1:
         plan = P.sv_plan_info(n, ga, w.params)
         fma_per_amp = sum(p["fma_per_amp"] for p in plan)
         fp64_flops = 2.0 * fma_per_amp * amps  # algorithmic FP64 work of the executed plan
         roof = {
-            "bound": "tensor", "kernel": "k_pass_dense / k_pass_reg<3,false> (fused forward tile passes: FP64 DMMA dense stages + register stages)",
+            "bound": "tensor",
+            "kernel": ("k_pass_c64 (complex64 tiles widened to FP64 for DMMA dense stages + register stages)"
+                       if args.precision == "c64" else
+                       "k_pass_dense / k_pass_reg<3,false> (fused forward tile passes: FP64 DMMA dense stages + register stages)"),
             "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
             "peak_source": "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
                            "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)",
             "unit": "TFLOP/s", "frac": fp64_flops / passes / (pass_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
-            "traffic": TRAFFIC_PER_LAUNCH.get(args.config),
+            "traffic": TRAFFIC_PER_LAUNCH.get(args.config) if args.precision == "c128" else TRAFFIC_PER_LAUNCH_C64,
             "algorithmic_flops_per_launch": fp64_flops / passes, "avg_launch_ms": pass_ms,
             "hbm": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src,
                     "unit": "GB/s", "frac": achieved / hbm_peak, "algorithmic_bytes_per_launch": pass_bytes}}
@@ -429,9 +437,10 @@ def main():
             "value": value, "unit": "gates/s" if shards == 1 else "gates/s (30q-equivalent: gates x 2^(n-30))",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "c128 (f64)", "data": "synthetic",
+            "dtype": "c64 (f32 dense stages, f64 register ops)" if args.precision == "c64" else "c128 (f64)",
+            "data": "synthetic",
             "config": {"workload": workload, "n_qubits": n, "gates": n_gates, "ham_terms": len(w.ham),
-                       "state_bytes": int(16 * amps_total), "shards": shards,
+                       "state_bytes": int((8 if args.precision == "c64" else 16) * amps_total), "shards": shards,
                        "l2": "inputs (16 GiB per GPU) larger than L2; no flush",
                        "parallelism": (f"state sharded over {world} GPUs (NCCL)" if world > 1 else
                                        f"{shards} virtual shards on 1 GPU" if shards > 1 else "1 GPU")},

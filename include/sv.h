@@ -148,6 +148,18 @@ sv_status sv_create_virtual_shards(int32_t n_qubits, int32_t world, sv_handle* o
  * batch mode and sharding are not available on density handles (SV_E_ARG). 1 <= n <= 17. */
 sv_status sv_create_density(int32_t n_qubits, sv_handle* out);
 
+/* NEXT-3 complex64 mode (the paper's "single-precision and double-precision simulation modes",
+ * PAPER.md P:417): the state is held as 2^n complex64 amplitudes (8 bytes each: half the HBM of
+ * sv_create). sv_apply_gate / sv_apply_circuit run complex64 fused passes (dense stages in FP32
+ * on the CUDA cores, other ops evaluated in FP64 and rounded once per stage) and sv_expectation
+ * reads the complex64 tiles (FP64 accumulation); results agree with the complex128 path to
+ * ~1e-5 relative (float rounding), tolerance 1e-4. Host state transfer keeps the complex128
+ * array format (values rounded on set); sv_set/get_state_device move 2*2^n floats. Gradients,
+ * batch mode, sampling and circuits the complex64 kernel does not take (tiles without qubit 0 or
+ * below 2^9 amplitudes, Pauli x-masks wider than a tile) run on a complex128 scratch copy
+ * (widened, computed, and — for evolution — rounded back). Single GPU only. 1 <= n <= 40. */
+sv_status sv_create_c64(int32_t n_qubits, sv_handle* out);
+
 sv_status sv_destroy(sv_handle h);
 
 /* Use this CUDA stream (a cudaStream_t passed as void*) for all subsequent work; NULL = the
@@ -166,7 +178,8 @@ sv_status sv_reset(sv_handle h);
 sv_status sv_set_state(sv_handle h, const double* host_amps);
 sv_status sv_get_state(sv_handle h, double* host_amps);
 
-/* Same, from / to DEVICE memory (device pointer on the handle's device), single-GPU handles. */
+/* Same, from / to DEVICE memory (device pointer on the handle's device), single-GPU handles
+ * (complex64 handles: 2*2^n floats). */
 sv_status sv_set_state_device(sv_handle h, const void* dev_amps);
 sv_status sv_get_state_device(sv_handle h, void* dev_amps);
 

@@ -71,6 +71,7 @@ def _load():
         "sv_nccl_unique_id": [P, i32],
         "sv_create_virtual_shards": [i32, i32, ctypes.POINTER(H)],
         "sv_create_density": [i32, ctypes.POINTER(H)],
+        "sv_create_c64": [i32, ctypes.POINTER(H)],
         "sv_destroy": [H],
         "sv_set_stream": [H, P],
         "sv_set_option": [H, i32, i64],
@@ -201,6 +202,12 @@ def sv_create_virtual_shards(n_qubits: int, world: int) -> ctypes.c_void_p:
 def sv_create_density(n_qubits: int) -> ctypes.c_void_p:
     h = ctypes.c_void_p()
     _check(lib.sv_create_density(n_qubits, ctypes.byref(h)))
+    return h
+
+
+def sv_create_c64(n_qubits: int) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _check(lib.sv_create_c64(n_qubits, ctypes.byref(h)))
     return h
 
 
@@ -425,3 +432,11 @@ class DensityMatrix(StateVector):
         out = np.empty(1 << (2 * self.n), dtype=np.complex128)
         _check(lib.sv_get_state(self.h, _ptr(out)))
         return out.reshape(1 << self.n, 1 << self.n)
+
+
+class StateVectorC64(StateVector):
+    """complex64 state (NEXT-3, the paper's single-precision mode): same calls; host state
+    transfer in complex128 arrays (rounded on set), device transfer in complex64."""
+
+    def __init__(self, n: int):
+        super().__init__(n, handle=sv_create_c64(n))

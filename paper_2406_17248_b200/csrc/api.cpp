@@ -176,11 +176,76 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
   return SV_OK;
 }
 
+int c64_promote(sv_state_s* h) {
+  const int64_t N = int64_t(1) << h->n_local;
+  if (!h->promo.ensure(size_t(16) << h->n_local)) return fail(SV_E_OOM, "complex128 scratch of a complex64 state");
+  h->psi = static_cast<double*>(h->promo.p);
+  cudaError_t e = launch_widen(h->psi32, h->psi, N, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "widen");
+  h->stats.kernel_launches += 1;
+  h->stats.algorithmic_bytes += 24.0 * (double)N;
+  return SV_OK;
+}
+
+static int c64_demote(sv_state_s* h) {
+  const int64_t N = int64_t(1) << h->n_local;
+  cudaError_t e = launch_narrow(h->psi, h->psi32, N, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "narrow");
+  h->stats.kernel_launches += 1;
+  h->stats.algorithmic_bytes += 24.0 * (double)N;
+  return SV_OK;
+}
+
+// complex64 forward passes: every pass must be a register pass the complex64 kernel takes (tile
+// position 0 = qubit 0, 2^9..2^11-amplitude tiles); otherwise the circuit runs on a complex128
+// scratch copy (widen, complex128 passes, narrow).
+static int run_plan_c64(sv_state_s* h, const CachedPlan& cp) {
+  const Plan& plan = cp.plan;
+  bool native = true;
+  for (const PassDesc& pd : plan.passes) native &= c64_pass_ok(pd);
+  if (!native) {
+    int rc = c64_promote(h);
+    if (rc) return rc;
+    rc = run_plan(h, cp, h->psi, nullptr, nullptr, 0, nullptr, nullptr);
+    if (rc) return rc;
+    return c64_demote(h);
+  }
+  const char* base = static_cast<const char*>(cp.buf.p);
+  for (size_t i = 0; i < plan.passes.size(); ++i) {
+    const PassDesc& pd = plan.passes[i];
+    const int next_mat = (i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size();
+    PassLaunch L;
+    L.pd = &pd;
+    L.d_ops = reinterpret_cast<const DevOp*>(base);
+    L.d_stages = reinterpret_cast<const StageDesc*>(base + cp.so);
+    L.d_mats = reinterpret_cast<const double*>(base + cp.mo);
+    L.d_rops = reinterpret_cast<const RegOp*>(base + cp.ro);
+    L.d_partials = nullptr;
+    L.nmats = next_mat - pd.mat_begin;
+    const int64_t ntiles = int64_t(1) << (h->n_local - pd.k);
+    L.grid = (int)std::min<int64_t>(ntiles, (int64_t)pauli_tile_grid(30, 12) * 3);  // SMs x 3
+    L.n_local = h->n_local;
+    L.rank_bits = 0;
+    cudaError_t e = launch_pass_c64(h->psi32, L, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "complex64 pass launch");
+    h->stats.kernel_launches += 1;
+    h->stats.gate_passes += 1;
+    h->stats.algorithmic_bytes += 16.0 * (double)(int64_t(1) << h->n_local);
+  }
+  return SV_OK;
+}
+
 int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg) {
   if (bg.empty()) return SV_OK;
   const CachedPlan* cp = nullptr;
   int rc = get_plan(h, bg, false, &cp);
   if (rc != SV_OK) return rc;
+  if (h->c64) {
+    rc = run_plan_c64(h, *cp);
+    if (rc != SV_OK) return rc;
+    h->stats.gates_applied += (int64_t)bg.size();
+    return SV_OK;
+  }
   rc = run_plan(h, *cp, h->psi, nullptr, nullptr, 0, nullptr, nullptr);
   if (rc != SV_OK) return rc;
   h->stats.gates_applied += (int64_t)bg.size();
@@ -223,11 +288,20 @@ int group_terms(sv_state_s* h, const sv_pauli* terms, int64_t n_terms, PauliGrou
 // Writes per-CTA partials of group g to d_partials[g * grid ...].
 int pauli_k(int n_local) { return std::min(n_local, 12); }
 
+// True when every x-group fits one Pauli tile with the low qubits (no pair-kernel fallback).
+bool pauli_groups_all_tiled(const sv_state_s* h, const PauliGroups& G) {
+  const int k = pauli_k(h->n_local);
+  const uint64_t lowmask = (1ull << std::min(3, k)) - 1;
+  for (uint64_t x : G.xs)
+    if (__builtin_popcountll(lowmask | x) > k) return false;
+  return true;
+}
+
 // Tiled evaluation of all Pauli groups: groups whose x-masks fit together in one 2^k tile (low
 // qubits + the x bits) share one pass (k_pauli_tile). Writes one partial slot (grid doubles) per
 // pass; *nslots receives the pass count. lam (optional) receives H psi.
 int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
-               int* nslots) {
+               int* nslots, const float* psi32) {
   const int nl = h->n_local;
   const int k = pauli_k(nl);
   const int L = std::min(3, k);
@@ -312,12 +386,14 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
   int slot = 0;
   for (size_t p = 0; p < passes.size(); ++p, ++slot) {
     const int mode = lam == nullptr ? 0 : (slot == 0 ? 1 : 2);
-    e = launch_pauli_tile(psi, lam, mode, nl, passes[p], dz, dc, d_partials + (size_t)slot * grid, grid, h->stream);
+    e = psi32 ? launch_pauli_tile_c64(psi32, nl, passes[p], dz, dc, d_partials + (size_t)slot * grid, grid, h->stream)
+              : launch_pauli_tile(psi, lam, mode, nl, passes[p], dz, dc, d_partials + (size_t)slot * grid, grid, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "pauli pass launch");
     h->stats.kernel_launches += 1;
     h->stats.expectation_passes += 1;
     h->stats.algorithmic_bytes += (mode == 0 ? 16.0 : (mode == 1 ? 32.0 : 48.0)) * amps;
   }
+  if (psi32 && !wide.empty()) return fail(SV_E_ARG, "internal: wide Pauli groups on a complex64 state");
   for (size_t w = 0; w < wide.size(); ++w, ++slot) {
     const int gi = wide[w];
     const int nt = G.end[gi] - G.begin[gi];
@@ -402,10 +478,44 @@ sv_status sv_create_density(int32_t n_qubits, sv_handle* out) {
   return SV_OK;
 }
 
+static cudaError_t init_c64(sv_state_s* h) {
+  cudaError_t e = cudaMemsetAsync(h->psi32, 0, size_t(8) << h->n_local, h->stream);
+  static const float one[2] = {1.0f, 0.0f};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->psi32, one, sizeof(one), cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // `one` is pageable
+  return e;
+}
+
+sv_status sv_create_c64(int32_t n_qubits, sv_handle* out) {
+  if (!out) return fail(SV_E_ARG, "null out");
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > 40) return fail(SV_E_ARG, "n_qubits must be in [1, 40]");
+  sv_state_s* h = new sv_state_s();
+  h->n = n_qubits;
+  h->n_local = n_qubits;
+  h->c64 = true;
+  cudaGetDevice(&h->device);
+  cudaError_t e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete h; return fail(SV_E_CUDA, std::string("stream: ") + cudaGetErrorString(e)); }
+  h->stream = h->own_stream;
+  const size_t bytes = (size_t(8) << n_qubits);
+  if (!h->state.ensure(bytes)) {
+    cudaStreamDestroy(h->own_stream);
+    delete h;
+    return fail(SV_E_OOM, "cannot allocate the complex64 state vector (" + std::to_string(bytes) + " bytes)");
+  }
+  h->psi32 = static_cast<float*>(h->state.p);
+  e = init_c64(h);
+  if (e != cudaSuccess) { sv_destroy(h); return fail(SV_E_CUDA, cudaGetErrorString(e)); }
+  *out = h;
+  return SV_OK;
+}
+
 sv_status sv_destroy(sv_handle h) {
   if (!h) return SV_OK;
   cudaStreamSynchronize(h->stream);
   h->state.release();
+  h->promo.release();
   h->work_psi.release();
   h->work_lam.release();
   h->work_r.release();
@@ -455,6 +565,11 @@ sv_status sv_reset(sv_handle h) {
   int rc = check_handle(h);
   if (rc) return rc;
   if (h->world > 1) return shard_reset(h);
+  if (h->c64) {
+    cudaError_t e = init_c64(h);
+    if (e != cudaSuccess) return cuda_fail(h, e, "reset");
+    return SV_OK;
+  }
   cudaError_t e = launch_init_zero(h->psi, int64_t(1) << h->n_local, true, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "reset");
   h->stats.kernel_launches += 1;
@@ -466,6 +581,14 @@ sv_status sv_set_state(sv_handle h, const double* host) {
   if (rc) return rc;
   if (!host) return fail(SV_E_ARG, "null host buffer");
   if (h->world > 1) return shard_set_state(h, host);
+  if (h->c64) {  // complex128 host values rounded to complex64
+    std::vector<float> v(size_t(2) << h->n);
+    for (size_t i = 0; i < v.size(); ++i) v[i] = (float)host[i];
+    cudaError_t e = cudaMemcpyAsync(h->psi32, v.data(), v.size() * 4, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "set_state");
+    return SV_OK;
+  }
   if (h->density) {  // row-major rho[r][c] -> vec[r + 2^n c]
     const uint64_t D = 1ull << h->n;
     std::vector<double> v(2 * D * D);
@@ -490,6 +613,14 @@ sv_status sv_get_state(sv_handle h, double* host) {
   if (rc) return rc;
   if (!host) return fail(SV_E_ARG, "null host buffer");
   if (h->world > 1) return shard_get_state(h, host);
+  if (h->c64) {
+    std::vector<float> v(size_t(2) << h->n);
+    cudaError_t e = cudaMemcpyAsync(v.data(), h->psi32, v.size() * 4, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "get_state");
+    for (size_t i = 0; i < v.size(); ++i) host[i] = (double)v[i];
+    return SV_OK;
+  }
   if (h->density) {
     const uint64_t D = 1ull << h->n;
     std::vector<double> v(2 * D * D);
@@ -514,7 +645,8 @@ sv_status sv_set_state_device(sv_handle h, const void* dev) {
   if (rc) return rc;
   if (!dev) return fail(SV_E_ARG, "null device buffer");
   if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
-  cudaError_t e = cudaMemcpyAsync(h->psi, dev, size_t(16) << h->n_local, cudaMemcpyDeviceToDevice, h->stream);
+  cudaError_t e = h->c64 ? cudaMemcpyAsync(h->psi32, dev, size_t(8) << h->n_local, cudaMemcpyDeviceToDevice, h->stream)
+                         : cudaMemcpyAsync(h->psi, dev, size_t(16) << h->n_local, cudaMemcpyDeviceToDevice, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "set_state_device");
   return SV_OK;
 }
@@ -524,7 +656,8 @@ sv_status sv_get_state_device(sv_handle h, void* dev) {
   if (rc) return rc;
   if (!dev) return fail(SV_E_ARG, "null device buffer");
   if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
-  cudaError_t e = cudaMemcpyAsync(dev, h->psi, size_t(16) << h->n_local, cudaMemcpyDeviceToDevice, h->stream);
+  cudaError_t e = h->c64 ? cudaMemcpyAsync(dev, h->psi32, size_t(8) << h->n_local, cudaMemcpyDeviceToDevice, h->stream)
+                         : cudaMemcpyAsync(dev, h->psi, size_t(16) << h->n_local, cudaMemcpyDeviceToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "get_state_device");
   return SV_OK;
@@ -590,7 +723,13 @@ sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, do
   if (!h->d_partials.ensure(ng * grid * 8) || !h->d_out.ensure(ng * 8)) return fail(SV_E_OOM, "partials");
   double* dp = static_cast<double*>(h->d_partials.p);
   int nslots = 0;
-  rc = run_groups(h, G, h->psi, nullptr, dp, grid, &nslots);
+  const bool c64_native = h->c64 && pauli_groups_all_tiled(h, G);
+  if (h->c64 && !c64_native) {
+    rc = c64_promote(h);
+    if (rc) return rc;
+  }
+  rc = c64_native ? run_groups(h, G, nullptr, nullptr, dp, grid, &nslots, h->psi32)
+                  : run_groups(h, G, h->psi, nullptr, dp, grid, &nslots);
   if (rc) return rc;
   const size_t ns_e = (size_t)nslots;
   cudaError_t e = launch_reduce_slots(dp, (int)ns_e, grid, static_cast<double*>(h->d_out.p), h->stream);
@@ -613,6 +752,10 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   if (rc) return rc;
   if (!out_value || (n_params > 0 && !out_grad)) return fail(SV_E_ARG, "null output");
   if (h->density) return fail(SV_E_ARG, "gradients are not available on density-matrix handles");
+  if (h->c64) {  // complex64 state: this operation reads a complex128 copy (the state is unchanged)
+    const int prc = c64_promote(h);
+    if (prc) return prc;
+  }
   std::vector<BoundGate> bg;
   rc = bind_circuit(h, gates, n_gates, params, n_params, true, &bg);
   if (rc) return rc;
@@ -811,6 +954,10 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
     return fail(SV_E_ARG, "bad batch arguments");
   if (n_rows == 0) return SV_OK;
   if (h->density) return fail(SV_E_ARG, "batch mode is not available on density-matrix handles");
+  if (h->c64) {  // complex64 state: this operation reads a complex128 copy (the state is unchanged)
+    const int prc = c64_promote(h);
+    if (prc) return prc;
+  }
   if (h->world > 1 || h->n_local > kBatchMaxQubits) {
     for (int32_t r = 0; r < n_rows; ++r) {
       rc = sv_expectation_with_grad(h, gates, n_gates, params ? params + (size_t)r * n_params : nullptr, n_params, terms,
@@ -942,6 +1089,10 @@ extern "C" sv_status sv_sample(sv_handle h, const int32_t* qubits, int32_t n_mea
     return fail(SV_E_ARG, "bad sampling arguments");
   if (h->world > 1) return fail(SV_E_ARG, "sampling is single-GPU in this version");
   if (h->density) return fail(SV_E_ARG, "sampling is not available on density-matrix handles");
+  if (h->c64) {  // complex64 state: this operation reads a complex128 copy (the state is unchanged)
+    const int prc = c64_promote(h);
+    if (prc) return prc;
+  }
   for (int j = 0; j < n_measured; ++j)
     if (qubits[j] < 0 || qubits[j] >= h->n) return fail(SV_E_QUBIT_RANGE, "measured qubit out of range");
   if (shots == 0) return SV_OK;

@@ -408,6 +408,9 @@ struct PauliTileArgs {
   double* partials;
 };
 
+__device__ __forceinline__ double2 amp(double2 v) { return v; }
+__device__ __forceinline__ double2 amp(float2 v) { return make_double2((double)v.x, (double)v.y); }
+
 // Walsh row of a 4-bit mask h: bit j (j < 16) = parity(j & h).
 __device__ __forceinline__ uint32_t walsh16(uint32_t h) {
   uint32_t r = 0;
@@ -418,7 +421,8 @@ __device__ __forceinline__ uint32_t walsh16(uint32_t h) {
   return r;
 }
 
-__global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restrict__ psi, double2* __restrict__ lam,
+template <typename T>  // T: double2 (complex128 state) or float2 (complex64 state, E only)
+__global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ psi, double2* __restrict__ lam,
                                                          PauliTileArgs a) {
   // Per tile the rank / outer-bit part of every term's sign is folded into its coefficient; per
   // element only the tile bits remain: sign_t(e) = (-1)^{popc(e & zt_t)} with zt_t the term's Z
@@ -428,8 +432,8 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
   constexpr int EPT = 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
-  double2* tile_buf = reinterpret_cast<double2*>(smem_raw);  // two tiles
-  double2* s_c = tile_buf + 2 * N;                         // folded coefficients (per tile)
+  T* tile_buf = reinterpret_cast<T*>(smem_raw);  // two tiles
+  double2* s_c = reinterpret_cast<double2*>(tile_buf + 2 * N);                         // folded coefficients (per tile)
   uint64_t* s_z = reinterpret_cast<uint64_t*>(s_c + a.nterms);  // physical Z masks
   uint32_t* s_zt = reinterpret_cast<uint32_t*>(s_z + a.nterms); // tile-position Z masks
   const int nhi = 1 << (a.k - a.low);
@@ -461,9 +465,12 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
       if ((tile >> j) & 1) base |= 1ull << a.oq[j];
     return base;
   };
-  auto issue = [&](int64_t tile, double2* dst) {
+  // 16-byte copies: one complex128 amplitude, or a complex64 pair (e, e + 1) — tile position 0 is
+  // qubit 0, so the pair is contiguous in HBM too
+  constexpr uint32_t PER = sizeof(T) == 16 ? 1u : 2u;
+  auto issue = [&](int64_t tile, T* dst) {
     const uint64_t base = tile_base(tile);
-    for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
+    for (uint32_t e = threadIdx.x * PER; e < N; e += blockDim.x * PER) {
       const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(psi + (base | (e & lowmask) | s_hi[e >> a.low]))
                    : "memory");
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
     const uint64_t base = tile_base(tile);
-    double2* tp = tile_buf + (size_t)(it & 1) * N;
+    T* tp = tile_buf + (size_t)(it & 1) * N;
     __syncthreads();  // the other buffer's previous tile is fully consumed
     const int64_t next = tile + gridDim.x;
     const bool more = next < a.ntiles;
@@ -510,7 +517,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
           const uint32_t wr = walsh16(zt >> 8);
 #pragma unroll
           for (int j = 0; j < EPT; ++j) {
-            const double2 w = cmul(c, tp[(tid + (uint32_t)j * 256u) ^ xt]);
+            const double2 w = cmul(c, amp(tp[(tid + (uint32_t)j * 256u) ^ xt]));
             const bool neg = (wr >> j) & 1u;
             l[j].x += neg ? -w.x : w.x;
             l[j].y += neg ? -w.y : w.y;
@@ -534,7 +541,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
         }
 #pragma unroll
         for (int j = 0; j < EPT; ++j) {
-          const double2 w = cmul(C[j], tp[(tid + (uint32_t)j * 256u) ^ xt]);
+          const double2 w = cmul(C[j], amp(tp[(tid + (uint32_t)j * 256u) ^ xt]));
           l[j].x += w.x;
           l[j].y += w.y;
         }
@@ -542,7 +549,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
         const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
-        acc += re_conj_mul(tp[e], l[j]);
+        acc += re_conj_mul(amp(tp[e]), l[j]);
         if (a.mode != 0) {
           const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
           if (a.mode == 1) lam[gi] = l[j];
@@ -560,11 +567,11 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const double2* __restri
             C.x += neg ? -c.x : c.x;
             C.y += neg ? -c.y : c.y;
           }
-          const double2 w = cmul(C, tp[e ^ a.xtile[g]]);
+          const double2 w = cmul(C, amp(tp[e ^ a.xtile[g]]));
           l.x += w.x;
           l.y += w.y;
         }
-        acc += re_conj_mul(tp[e], l);
+        acc += re_conj_mul(amp(tp[e]), l);
         if (a.mode != 0) {
           const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
           if (a.mode == 1) lam[gi] = l;
@@ -851,8 +858,8 @@ int pauli_tile_grid(int n_local, int k) {
   return (int)(ntiles < want ? ntiles : want);
 }
 
-cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_local, const PauliPassDesc& pp,
-                              const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s) {
+static cudaError_t pauli_tile_impl(const void* psi, bool c64, double* lam, int mode, int n_local, const PauliPassDesc& pp,
+                                   const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s) {
   PauliTileArgs a;
   std::memset(&a, 0, sizeof(a));
   a.k = pp.k;
@@ -876,16 +883,34 @@ cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_lo
   a.z = d_z + pp.term_base;
   a.c = reinterpret_cast<const double2*>(d_c) + pp.term_base;
   a.partials = d_partials;
-  const size_t smem = (size_t(32) << pp.k) + (size_t)pp.nterms * 28 + 8 + (size_t(8) << (pp.k - pp.low));
+  const size_t smem = (size_t(c64 ? 16 : 32) << pp.k) + (size_t)pp.nterms * 28 + 8 + (size_t(8) << (pp.k - pp.low));
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_pauli_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_pauli_tile<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pauli_tile<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_pauli_tile<<<grid, kThreads, smem, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<double2*>(lam), a);
+  if (c64) {
+    if (lam || mode != 0 || pp.tq[0] != 0) return cudaErrorInvalidValue;  // E only; pairs need qubit 0 at position 0
+    k_pauli_tile<float2><<<grid, kThreads, smem, s>>>(reinterpret_cast<const float2*>(psi), nullptr, a);
+  } else {
+    k_pauli_tile<double2><<<grid, kThreads, smem, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<double2*>(lam), a);
+  }
   return cudaGetLastError();
 }
+
+cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_local, const PauliPassDesc& pp,
+                              const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s) {
+  return pauli_tile_impl(psi, false, lam, mode, n_local, pp, d_z, d_c, d_partials, grid, s);
+}
+
+cudaError_t launch_pauli_tile_c64(const float* psi, int n_local, const PauliPassDesc& pp, const uint64_t* d_z,
+                                  const double* d_c, double* d_partials, int grid, cudaStream_t s) {
+  return pauli_tile_impl(psi, true, nullptr, 0, n_local, pp, d_z, d_c, d_partials, grid, s);
+}
+
+
 
 cudaError_t launch_block_prob(const double* psi, int n_local, int bl, double* out, cudaStream_t s) {
   k_block_prob<<<(unsigned)(1ll << (n_local - bl)), kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), bl, out);

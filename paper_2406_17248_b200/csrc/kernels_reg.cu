@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "cx.cuh"
 #include "sv_internal.h"
@@ -572,7 +573,14 @@ __device__ __forceinline__ void dense_load_a(const StageDesc& S, const double2* 
 
 // warp-owned vectors: 2 N-tiles (n0) x 8 MMA columns (c0 c1 c2); all address parts are
 // host-precomputed swizzled offsets (the swizzle is XOR-linear)
-__device__ __forceinline__ void dense_apply_a(double2* tp, const StageDesc& S, const double2 (&ue)[2][4], int warp,
+__device__ __forceinline__ double2 tile_ld(const double2& v) { return v; }
+__device__ __forceinline__ double2 tile_ld(const float2& v) { return make_double2((double)v.x, (double)v.y); }
+__device__ __forceinline__ void tile_st(double2& d, double2 v) { d = v; }
+__device__ __forceinline__ void tile_st(float2& d, double2 v) { d = make_float2((float)v.x, (float)v.y); }
+
+// T: double2 (complex128 tile) or float2 (complex64 tile, NEXT-3: widened to FP64 for the MMAs)
+template <typename T>
+__device__ __forceinline__ void dense_apply_a(T* tp, const StageDesc& S, const double2 (&ue)[2][4], int warp,
                                               int lane) {
   const uint32_t wsw = S.warp_swz[warp];
   const uint32_t baseB = wsw ^ S.lane_b[lane];
@@ -581,7 +589,7 @@ __device__ __forceinline__ void dense_apply_a(double2* tp, const StageDesc& S, c
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int kq = 0; kq < 4; ++kq) {
-      const double2 x = tp[baseB ^ S.swz_reg[nt * 4 + kq]];
+      const double2 x = tile_ld(tp[baseB ^ S.swz_reg[nt * 4 + kq]]);
       b[nt][kq] = x.x;
       b[nt][kq + 4] = x.y;
     }
@@ -618,7 +626,7 @@ __device__ __forceinline__ void dense_apply_a(double2* tp, const StageDesc& S, c
     for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
       for (int v = 0; v < 2; ++v)
-        tp[baseD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]] = make_double2(d[mh][nt][v], d[mh + 2][nt][v]);
+        tile_st(tp[baseD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]], make_double2(d[mh][nt][v], d[mh + 2][nt][v]));
 }
 
 
@@ -948,6 +956,146 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
   }
 }
 
+// ---------------------------------------------------------------- complex64 forward passes (NEXT-3)
+//
+// The state is complex64 in HBM and in the shared-memory tile (half the bytes of every pass) with
+// the complex128 kernel's slot layout (one 8-byte slot per amplitude, same swizzle), so the
+// planner's stage tables apply unchanged: 8-byte cp.async copies in, 8-byte stores out. Register
+// (sequential) stages widen the thread's 8 amplitudes to complex128 and run the same op code as
+// the complex128 kernel; dense stages widen the B fragments and run the same FP64 MMAs, rounding
+// once per stage on the way back. (An FP32 CUDA-core FFMA version of the dense stage was measured
+// slower than the FP64 tensor cores: 3-register FFMA issues at half rate.)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+__global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_c64(float2* __restrict__ psi, RegArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t N = 1u << a.k;
+  const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float2* smem_tiles = reinterpret_cast<float2*>(smem_raw);  // two tiles
+  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + 2 * N);
+  StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
+  double* s_mats = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
+  uint64_t* s_ob = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.ops);
+    uint4* dst = reinterpret_cast<uint4*>(s_ops);
+    for (int i = tid; i < a.nops * 2; i += nthr) dst[i] = src[i];
+    const uint64_t* ss = reinterpret_cast<const uint64_t*>(a.stages);
+    uint64_t* sd = reinterpret_cast<uint64_t*>(s_st);
+    for (int i = tid; i < a.nstages * (int)(sizeof(StageDesc) / 8); i += nthr) sd[i] = ss[i];
+    for (int i = tid; i < a.nmats; i += nthr) s_mats[i] = a.mats[i];
+    for (int h = tid; h < 4 * 64; h += nthr) {
+      uint64_t off = 0;
+      for (int b = 0; b < 6; ++b) {
+        const int j = (h >> 6) * 6 + b;
+        if (((h >> b) & 1) && j < a.n_outer) off |= 1ull << a.oq[j];
+      }
+      s_ob[h] = off;
+    }
+  }
+  __syncthreads();
+  const int nthr_bits = a.k - 3;
+  const double2* mats2 = reinterpret_cast<const double2*>(s_mats);
+  const double2* gm2 = reinterpret_cast<const double2*>(a.mats);
+  uint64_t dep_t = 0;
+  for (int b = 0; b < nthr_bits; ++b)
+    if ((tid >> b) & 1) dep_t |= 1ull << a.tq[b];
+  const uint32_t swz_t = swz((uint32_t)tid);
+  auto tile_base = [&](int64_t tile) {
+    uint64_t base = s_ob[tile & 63] | s_ob[64 + ((tile >> 6) & 63)] | s_ob[128 + ((tile >> 12) & 63)] |
+                    s_ob[192 + ((tile >> 18) & 63)];
+    for (int j = 24; j < a.n_outer; ++j)
+      if ((tile >> j) & 1) base |= 1ull << a.oq[j];
+    return base;
+  };
+  auto issue_load = [&](int64_t tile, int buf) {
+    const uint64_t bt = tile_base(tile) | dep_t;
+    float2* dp = smem_tiles + (size_t)buf * N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cp_async8(dp + (swz_t ^ a.zsub[i]), psi + (bt | a.hsub[i]));
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if ((int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+    const int cur = it & 1;
+    const uint64_t base = tile_base(tile);
+    const int64_t next = tile + gridDim.x;
+    if (next < a.ntiles) {
+      issue_load(next, cur ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    float2* tp = smem_tiles + (size_t)cur * N;
+    for (int st = 0; st < a.nstages; ++st) {
+      const StageDesc& S = s_st[st];
+      if (S.dense) {
+        double2 ue[2][4];
+        dense_load_a(S, gm2, base, warp, lane, ue);
+        dense_apply_a(tp, S, ue, warp, lane);
+        __syncthreads();
+        continue;
+      }
+      uint32_t tthr = 0;
+      for (int b = 0; b < nthr_bits; ++b)
+        if ((tid >> b) & 1) tthr |= 1u << S.thrpos[b];
+      const uint32_t A = swz(tthr);
+      uint32_t SR[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) SR[r] = swz(1u << S.regpos[r]);
+      double2 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t ad = A;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          if ((j >> r) & 1) ad ^= SR[r];
+        v[j] = tile_ld(tp[ad]);
+      }
+      for (int i = S.op_begin; i < S.op_end; ++i) {
+        const Op o = load_op(s_ops + i);
+        const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
+        if (!ok) continue;
+        reg_apply<3>(v, o, mats2 + o.mat_off(), tthr, base);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t ad = A;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          if ((j >> r) & 1) ad ^= SR[r];
+        tile_st(tp[ad], v[j]);
+      }
+      __syncthreads();
+    }
+    {
+      const uint64_t bt = base | dep_t;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) psi[bt | a.hsub[i]] = tp[swz_t ^ a.zsub[i]];
+    }
+    __syncthreads();
+  }
+}
+
+size_t c64_pass_smem_bytes(int k, int nops, int nstages, int nmats) {
+  return (size_t(8) << k) * 2 + (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16 +
+         (size_t)nmats * 8 + 4 * 64 * 8;
+}
+
+__global__ void k_widen(const float2* __restrict__ a, double2* __restrict__ b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = tile_ld(a[i]);
+}
+__global__ void k_narrow(const double2* __restrict__ a, float2* __restrict__ b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    tile_st(b[i], a[i]);
+}
+
 size_t dense_pass_smem_bytes(int k, int nstages) {
   return (size_t(16) << k) * 2 + (size_t)nstages * sizeof(StageDesc) + 16 + 4 * 64 * 8;
 }
@@ -1059,6 +1207,72 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
       k_pass_reg<3, false><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
     }
   }
+  return cudaGetLastError();
+}
+
+
+// complex64 forward pass (NEXT-3): register plans (2^8..2^11-amplitude tiles, 2^(k-3) threads);
+// the caller (api.cpp) routes everything else through a complex128 scratch copy.
+bool c64_pass_ok(const PassDesc& pd) { return pd.R == 3 && pd.k >= 8 && pd.k <= 11; }
+
+cudaError_t launch_pass_c64(float* psi, const PassLaunch& L, cudaStream_t s) {
+  const PassDesc& pd = *L.pd;
+  if (!c64_pass_ok(pd)) return cudaErrorInvalidValue;
+  RegArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.k = pd.k;
+  a.low = pd.low;
+  a.nops = pd.op_end - pd.op_begin;
+  a.nstages = pd.stage_end - pd.stage_begin;
+  a.nmats = pd.seq_mats < L.nmats ? pd.seq_mats : L.nmats;
+  a.grid = L.grid;
+  for (int i = 0; i < kMaxTileQubits + 3; ++i) a.tq[i] = pd.tq[i];
+  uint64_t tmask = 0;
+  for (int p = 0; p < pd.k; ++p) tmask |= 1ull << pd.tq[p];
+  a.n_outer = 0;
+  for (int q = 0; q < L.n_local; ++q)
+    if (!((tmask >> q) & 1ull)) a.oq[a.n_outer++] = (int8_t)q;
+  a.ntiles = 1ll << (L.n_local - pd.k);
+  const int tb = pd.k - 3;  // thread bits: element e = tid + i 2^tb, i < 8
+  for (int i = 0; i < 8; ++i) {
+    a.hsub[i] = 0;
+    for (int j = 0; j < 3; ++j)
+      if ((i >> j) & 1) a.hsub[i] |= 1ull << pd.tq[tb + j];
+    a.zsub[i] = swz((uint32_t)i << tb);
+  }
+  a.ops = L.d_rops + pd.op_begin;
+  a.mats = L.d_mats + pd.mat_begin;
+  a.stages = L.d_stages + pd.stage_begin;
+  const int nthr = 1 << tb;
+  const size_t smem = c64_pass_smem_bytes(a.k, a.nops, a.nstages, a.nmats);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_pass_c64, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  k_pass_c64<<<L.grid, nthr, smem, s>>>(reinterpret_cast<float2*>(psi), a);
+  return cudaGetLastError();
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+cudaError_t launch_widen(const float* a, double* b, int64_t n, cudaStream_t s) {
+  k_widen<<<sm_count() * 4, 256, 0, s>>>(reinterpret_cast<const float2*>(a), reinterpret_cast<double2*>(b), n);
+  return cudaGetLastError();
+}
+cudaError_t launch_narrow(const double* a, float* b, int64_t n, cudaStream_t s) {
+  k_narrow<<<sm_count() * 4, 256, 0, s>>>(reinterpret_cast<const double2*>(a), reinterpret_cast<float2*>(b), n);
   return cudaGetLastError();
 }
 

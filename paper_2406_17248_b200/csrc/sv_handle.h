@@ -37,12 +37,16 @@ struct sv_state_s {
   int n_local = 0;     // qubits held per shard (n - log2 world)
   int world = 1, rank = 0;
   bool density = false;  // rho of n qubits held as a 2n-qubit vector (n_local = 2n)
+  bool c64 = false;      // complex64 state (NEXT-3): psi32 holds it; psi points at the complex128
+                         // scratch (promo) only while a promoted operation runs
   int device = 0;
   bool poisoned = false;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   sv::DevBuf state, work_psi, work_lam, work_r;
   double* psi = nullptr;
+  float* psi32 = nullptr;
+  sv::DevBuf promo;
   sv::DevBuf d_ops, d_mats, d_terms, d_partials, d_out;
   std::vector<char> h_stage;
   std::vector<sv::CachedPlan*> plan_cache;  // owned, LRU (small)
@@ -64,6 +68,7 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
 void release_plan_cache(sv_state_s* h);
 int run_reverse(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, std::vector<double>* d_out);
 int apply_bound(sv_state_s* h, const std::vector<BoundGate>& bg);
+int c64_promote(sv_state_s* h);  // widen psi32 into the complex128 scratch; h->psi = scratch
 
 struct PauliGroups {
   std::vector<uint64_t> xs;           // distinct x-masks, ascending
@@ -72,7 +77,8 @@ struct PauliGroups {
   std::vector<double> c;              // complex coefficients c_t * i^{popc(x&z)} (re, im)
 };
 int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
-               int* nslots);
+               int* nslots, const float* psi32 = nullptr);  // psi32: complex64 state, E only, tiled groups only
+bool pauli_groups_all_tiled(const sv_state_s* h, const PauliGroups& G);
 int pauli_k(int n_local);
 
 // shard.cpp

@@ -206,6 +206,11 @@ struct PassLaunch {
 };
 cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
 cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
+// complex64 state (NEXT-3)
+bool c64_pass_ok(const PassDesc& pd);
+cudaError_t launch_pass_c64(float* psi, const PassLaunch& L, cudaStream_t s);
+cudaError_t launch_widen(const float* a, double* b, int64_t n, cudaStream_t s);
+cudaError_t launch_narrow(const double* a, float* b, int64_t n, cudaStream_t s);
 int pass_grid(int n_local, int k, bool dual);
 int plan_grid(const Plan& plan, int n_local);
 int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual);
@@ -239,6 +244,8 @@ struct PauliPassDesc {
 int pauli_tile_grid(int n_local, int k);
 cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_local, const PauliPassDesc& pp,
                               const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s);
+cudaError_t launch_pauli_tile_c64(const float* psi, int n_local, const PauliPassDesc& pp, const uint64_t* d_z,
+                                  const double* d_c, double* d_partials, int grid, cudaStream_t s);
 cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int n_local, uint64_t xl,
                                const uint64_t* d_z, const double* d_c, int nterms, double* d_partials, int grid,
                                cudaStream_t s);

@@ -1,0 +1,128 @@
+"""NEXT-3 complex64 mode ("single-precision and double-precision
+simulation modes") vs the complex128 CPU oracle.
+
+Tolerance 1e-4: a complex64 amplitude carries a relative rounding of 2^-24 ~ 6e-8
+per stored value; every stage rounds once, a dense stage adds 16-term FP32 dot products, so after
+~100 stages the absolute error per amplitude of a unit-norm state stays ~1e-5. Energies are
+FP64-accumulated over complex64 inputs: |dE| <= 2 sum|c_t| * max|d psi| << 1e-4 for the sums here.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2406_17248_b200 as P
+    return P
+
+
+
+@pytest.mark.parametrize("n,depth,native", [(9, 6, True), (11, 8, True), (14, 10, False), (17, 12, True),
+                                            (19, 8, True)])
+def test_c64_dense_circuit(P, n, depth, native):
+    """C4-shaped circuits (Haar 1q + CZ bricks: dense FP32 stages) over several tiles. States
+    whose planner picks tiles below 2^8 amplitudes (n = 12..16) run on the complex128 copy."""
+    w = W.random_circuit(n, depth, seed=100 + n)
+    ref = oracle.apply_circuit(n, w.gates)
+    sv = P.StateVectorC64(n)
+    P.sv_reset_stats(sv.h)
+    sv.apply_circuit(w.gates)
+    got = sv.get_state()
+    st = P.sv_get_stats(sv.h)
+    sv.close()
+    assert np.max(np.abs(got - ref)) <= TOL
+    # native complex64 passes: 16 bytes per amplitude per pass, no widen/narrow traffic
+    if native:
+        assert st["algorithmic_bytes"] == pytest.approx(16.0 * (1 << n) * st["gate_passes"])
+    else:
+        assert st["algorithmic_bytes"] > 16.0 * (1 << n) * st["gate_passes"]
+
+
+@pytest.mark.parametrize("n", [9, 12, 15])
+def test_c64_controlled_random(P, n):
+    """The paper's complex random circuits with controls (sequential + dense stages), a random
+    start state."""
+    w = W.random_complex(n, 6, seed=n, extra_kinds=("PS", "MAT1", "MAT2", "SWAP", "XLIKE", "ZLIKE"))
+    psi0 = W.random_state(n, seed=n)
+    ref = oracle.apply_circuit(n, w.gates, psi0=psi0)
+    sv = P.StateVectorC64(n)
+    sv.set_state(psi0)
+    sv.apply_circuit(w.gates)
+    got = sv.get_state()
+    sv.close()
+    assert np.max(np.abs(got - ref)) <= TOL
+
+
+@pytest.mark.parametrize("n", [10, 14])
+def test_c64_expectation(P, n):
+    w = W.random_circuit(n, 4, seed=7 + n)
+    ham = W.jw_hamiltonian(n, 30, seed=n) + W.random_hamiltonian(n, 6, seed=n + 1)
+    psi = oracle.apply_circuit(n, w.gates)
+    ref = oracle.expectation(psi, ham)[0]
+    sv = P.StateVectorC64(n)
+    sv.apply_circuit(w.gates)
+    E = sv.expectation(ham)
+    sv.close()
+    assert abs(E - ref) <= TOL
+
+
+def test_c64_promoted_paths(P):
+    """Operations without a complex64 kernel run on a complex128 copy: small states (tiles below
+    2^9 amplitudes), Pauli strings wider than a tile, gradients, sampling."""
+    # small n: complex128 passes on the scratch copy, rounded back
+    w = W.random_complex(5, 4, seed=3)
+    sv = P.StateVectorC64(5)
+    sv.apply_circuit(w.gates)
+    assert np.max(np.abs(sv.get_state() - oracle.apply_circuit(5, w.gates))) <= TOL
+    sv.close()
+    # wide x-mask (X on every qubit of 16)
+    n = 16
+    w = W.random_circuit(n, 3, seed=5)
+    ham = [(0.7, {q: "X" for q in range(n)}), (-0.4, {0: "Z", 15: "Z"})]
+    sv = P.StateVectorC64(n)
+    sv.apply_circuit(w.gates)
+    psi = oracle.apply_circuit(n, w.gates)
+    assert abs(sv.expectation(ham) - oracle.expectation(psi, ham)[0]) <= TOL
+    sv.close()
+    # gradient on a complex64 handle (complex128 copy of the complex64 start state)
+    h = W.hea(10, 2, seed=4, nterms=12)
+    sv = P.StateVectorC64(10)
+    E, g = sv.expectation_with_grad(h.gates, h.params, h.ham)
+    Er, gr = oracle.adjoint_grad(10, h.gates, h.params, h.ham)
+    sv.close()
+    assert abs(E - Er) <= TOL
+    assert np.max(np.abs(g - gr)) <= TOL
+
+
+def test_c64_sampling_and_reset(P):
+    n = 12
+    w = W.random_circuit(n, 3, seed=9)
+    sv = P.StateVectorC64(n)
+    sv.apply_circuit(w.gates)
+    shots = sv.sample(list(range(n)), 2000, seed=3)
+    assert shots.shape == (2000,) and shots.min() >= 0 and shots.max() < (1 << n)
+    sv.reset()
+    st = sv.get_state()
+    assert st[0] == 1.0 and np.count_nonzero(st) == 1
+    sv.close()
+
+
+def test_c64_matches_c128_path(P):
+    """Same circuit and H through both precisions: agreement within the complex64 tolerance."""
+    n = 16
+    w = W.random_circuit(n, 8, seed=21)
+    ham = W.jw_hamiltonian(n, 40, seed=2)
+    a = P.StateVector(n)
+    b = P.StateVectorC64(n)
+    a.apply_circuit(w.gates)
+    b.apply_circuit(w.gates)
+    assert np.max(np.abs(a.get_state() - b.get_state())) <= TOL
+    assert abs(a.expectation(ham) - b.expectation(ham)) <= TOL
+    a.close()
+    b.close()
