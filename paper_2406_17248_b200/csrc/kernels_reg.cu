@@ -36,6 +36,8 @@ namespace sv {
 namespace {
 
 __host__ __device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ ((t >> 3 ^ t >> 6 ^ t >> 9 ^ t >> 12) & 7u); }
+// complex64 tiles: 8-byte slots, 16 per 128-byte bank row -> 4-bit XOR fold
+__host__ __device__ __forceinline__ uint32_t swz8(uint32_t t) { return t ^ ((t >> 4 ^ t >> 8 ^ t >> 12) & 15u); }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -958,16 +960,118 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
 
 // ---------------------------------------------------------------- complex64 forward passes (NEXT-3)
 //
-// The state is complex64 in HBM and in the shared-memory tile (half the bytes of every pass) with
-// the complex128 kernel's slot layout (one 8-byte slot per amplitude, same swizzle), so the
-// planner's stage tables apply unchanged: 8-byte cp.async copies in, 8-byte stores out. Register
-// (sequential) stages widen the thread's 8 amplitudes to complex128 and run the same op code as
-// the complex128 kernel; dense stages widen the B fragments and run the same FP64 MMAs, rounding
-// once per stage on the way back. (An FP32 CUDA-core FFMA version of the dense stage was measured
-// slower than the FP64 tensor cores: 3-register FFMA issues at half rate.)
+// The state is complex64 in HBM and in the shared-memory tile (half the bytes of every pass): one
+// 8-byte slot per amplitude, swizzled with a 4-bit XOR fold (16 slots per bank row), 8-byte
+// cp.async copies in and 8-byte stores out; every address is derived in-kernel from the stage's
+// positions. Register (sequential) stages widen the thread's 8 amplitudes to complex128 and run the
+// same op code as the complex128 kernel (one rounding per stage); dense stages run on the TF32
+// tensor cores with a 3-term split (dense_stage_tf32). Measured alternatives: FP32 FFMA on the CUDA
+// cores and widening to the FP64 MMAs were both slower.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// ---- complex64 dense stage on TF32 tensor cores with a 3-term split ("3xTF32") ----
+// Y = [[Ur, -Ui], [Ui, Ur]] [Xr; Xi] as mma.sync m16n8k8 (TF32 in, FP32 accumulate): per warp
+// 2 M-tiles (Re / Im out) x 2 N-tiles (its 16 vectors) x 4 K-steps. Every FP32 operand v is split
+// into hi = tf32(v) and lo = tf32(v - hi); D += A_hi B_hi + A_hi B_lo + A_lo B_hi keeps ~21
+// mantissa bits (the dropped A_lo B_lo term is ~2^-21 relative), i.e. near-FP32 accuracy at the
+// TF32 tensor rate (measured 277 TF legacy mma.sync vs 37 TF for FP64). Fragment layouts (PTX
+// m16n8k8 .tf32): A[g (+8)][t (+4)], B[k = t (+4)][n = g], D[g (+8)][2t (+1)]; g = lane/4, t = lane%4.
+// hi keeps the top 10 mantissa bits (truncation: one LOP3; cvt.rna.tf32 is a multi-instruction
+// sequence on sm_100a), lo = v - hi is exact in FP32 and the MMA reads its top 10 mantissa bits:
+// together ~21 bits, the dropped remainder is <= 2^-21 relative.
+__device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(v) & 0xFFFFE000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S, const double2* __restrict__ gm2,
+                                                 uint64_t base, int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t var = S.warp_var[warp];
+  for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
+  const double2* U = gm2 + S.dense_off + var * (16u * kDenseRow);
+  // A entries U[o][i], o in {g, g+8} (a), i = 8 kh + t (+4) (c): complex -> split re / im
+  uint32_t ur_h[2][2][2], ur_l[2][2][2], ui_h[2][2][2], ui_l[2][2][2];  // [kh][a][c]
+#pragma unroll
+  for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double2 u = __ldg(U + (g + 8 * a) * kDenseRow + 8 * kh + t + 4 * c);
+        split_tf32((float)u.x, ur_h[kh][a][c], ur_l[kh][a][c]);
+        split_tf32((float)u.y, ui_h[kh][a][c], ui_l[kh][a][c]);
+      }
+  // slot parts (swz is XOR-linear): vector n = 8 nt + col (col bits -> thrpos[0..2], nt -> thrpos[3]),
+  // register index r (bit i -> regpos[i])
+  auto sp = [&](int pos) { return swz8(1u << pos); };
+  uint32_t wsw = 0;
+  for (int b = 0; b < 3; ++b)
+    if (((warp >> b) & 1) && S.thrpos[4 + b] >= 0) wsw ^= sp(S.thrpos[4 + b]);
+  uint32_t bB = wsw, bD = wsw;
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    if ((g >> b) & 1) bB ^= sp(S.thrpos[b]);   // B: n col = g
+    if ((g >> b) & 1) bD ^= sp(S.regpos[b]);   // D: out amp o = g (+8)
+  }
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    if ((t >> b) & 1) bB ^= sp(S.regpos[b]);      // B: in amp r = t (+4, +8)
+    if ((t >> b) & 1) bD ^= sp(S.thrpos[b + 1]);  // D: n col = 2 t (+1)
+  }
+  const uint32_t sN = sp(S.thrpos[3]), sR2 = sp(S.regpos[2]), sR3 = sp(S.regpos[3]), sC0 = sp(S.thrpos[0]);
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    // B fragments: in amps r = t + 4 c + 8 kh of vector (8 nt + g): Re for K-steps 0-1, Im for 2-3
+    uint32_t xr_h[2][2], xr_l[2][2], xi_h[2][2], xi_l[2][2];  // [kh][c]
+#pragma unroll
+    for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const float2 x = tp[bB ^ (nt ? sN : 0u) ^ (c ? sR2 : 0u) ^ (kh ? sR3 : 0u)];
+        split_tf32(x.x, xr_h[kh][c], xr_l[kh][c]);
+        split_tf32(x.y, xi_h[kh][c], xi_l[kh][c]);
+      }
+    float dre[4] = {0.f, 0.f, 0.f, 0.f}, dim[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kh = 0; kh < 2; ++kh) {
+      // Re out += Ur Xr - Ui Xi ; Im out += Ui Xr + Ur Xi
+      const uint32_t arh[4] = {ur_h[kh][0][0], ur_h[kh][1][0], ur_h[kh][0][1], ur_h[kh][1][1]};
+      const uint32_t arl[4] = {ur_l[kh][0][0], ur_l[kh][1][0], ur_l[kh][0][1], ur_l[kh][1][1]};
+      const uint32_t aih[4] = {ui_h[kh][0][0], ui_h[kh][1][0], ui_h[kh][0][1], ui_h[kh][1][1]};
+      const uint32_t ail[4] = {ui_l[kh][0][0], ui_l[kh][1][0], ui_l[kh][0][1], ui_l[kh][1][1]};
+      const uint32_t nih[4] = {aih[0] ^ 0x80000000u, aih[1] ^ 0x80000000u, aih[2] ^ 0x80000000u, aih[3] ^ 0x80000000u};
+      const uint32_t nil[4] = {ail[0] ^ 0x80000000u, ail[1] ^ 0x80000000u, ail[2] ^ 0x80000000u, ail[3] ^ 0x80000000u};
+      mma_tf32(dre, arh, xr_h[kh][0], xr_h[kh][1]);
+      mma_tf32(dim, aih, xr_h[kh][0], xr_h[kh][1]);
+      mma_tf32(dre, nih, xi_h[kh][0], xi_h[kh][1]);
+      mma_tf32(dim, arh, xi_h[kh][0], xi_h[kh][1]);
+      mma_tf32(dre, arh, xr_l[kh][0], xr_l[kh][1]);
+      mma_tf32(dim, aih, xr_l[kh][0], xr_l[kh][1]);
+      mma_tf32(dre, nih, xi_l[kh][0], xi_l[kh][1]);
+      mma_tf32(dim, arh, xi_l[kh][0], xi_l[kh][1]);
+      mma_tf32(dre, arl, xr_h[kh][0], xr_h[kh][1]);
+      mma_tf32(dim, ail, xr_h[kh][0], xr_h[kh][1]);
+      mma_tf32(dre, nil, xi_h[kh][0], xi_h[kh][1]);
+      mma_tf32(dim, arl, xi_h[kh][0], xi_h[kh][1]);
+    }
+    // D: rows o = g (+8: d[2], d[3]), cols n = 8 nt + 2 t (+1: d[1], d[3])
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t ad = bD ^ (nt ? sN : 0u) ^ ((q & 1) ? sC0 : 0u) ^ ((q & 2) ? sR3 : 0u);
+      tp[ad] = make_float2(dre[q], dim[q]);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_c64(float2* __restrict__ psi, RegArgs a) {
@@ -1003,7 +1107,7 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_c64(float2* __restric
   uint64_t dep_t = 0;
   for (int b = 0; b < nthr_bits; ++b)
     if ((tid >> b) & 1) dep_t |= 1ull << a.tq[b];
-  const uint32_t swz_t = swz((uint32_t)tid);
+  const uint32_t swz_t = swz8((uint32_t)tid);
   auto tile_base = [&](int64_t tile) {
     uint64_t base = s_ob[tile & 63] | s_ob[64 + ((tile >> 6) & 63)] | s_ob[128 + ((tile >> 12) & 63)] |
                     s_ob[192 + ((tile >> 18) & 63)];
@@ -1035,19 +1139,17 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_c64(float2* __restric
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
       if (S.dense) {
-        double2 ue[2][4];
-        dense_load_a(S, gm2, base, warp, lane, ue);
-        dense_apply_a(tp, S, ue, warp, lane);
+        dense_stage_tf32(tp, S, gm2, base, warp, lane);
         __syncthreads();
         continue;
       }
       uint32_t tthr = 0;
       for (int b = 0; b < nthr_bits; ++b)
         if ((tid >> b) & 1) tthr |= 1u << S.thrpos[b];
-      const uint32_t A = swz(tthr);
+      const uint32_t A = swz8(tthr);
       uint32_t SR[3];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) SR[r] = swz(1u << S.regpos[r]);
+      for (int r = 0; r < 3; ++r) SR[r] = swz8(1u << S.regpos[r]);
       double2 v[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -1238,7 +1340,7 @@ cudaError_t launch_pass_c64(float* psi, const PassLaunch& L, cudaStream_t s) {
     a.hsub[i] = 0;
     for (int j = 0; j < 3; ++j)
       if ((i >> j) & 1) a.hsub[i] |= 1ull << pd.tq[tb + j];
-    a.zsub[i] = swz((uint32_t)i << tb);
+    a.zsub[i] = swz8((uint32_t)i << tb);
   }
   a.ops = L.d_rops + pd.op_begin;
   a.mats = L.d_mats + pd.mat_begin;

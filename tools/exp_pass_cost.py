@@ -12,7 +12,7 @@ import paper_2406_17248_b200 as P  # noqa: E402
 import workloads as W  # noqa: E402
 
 n = 30
-sv = P.StateVector(n)
+sv = P.StateVectorC64(n) if os.environ.get("EXP_C64") else P.StateVector(n)
 stream = torch.cuda.Stream()
 P.sv_set_stream(sv.h, stream.cuda_stream)
 G = W.Gate
