@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   const uint32_t NB = DUAL ? 2 * N : N;  // doubles2 per buffer (psi [+ lambda])
   double2* smem_tiles = reinterpret_cast<double2*>(smem_raw);
   double2* tp = smem_tiles;  // (setup-phase alias; the tile loop rebinds per buffer)
-  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + 2 * NB);
+  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + ((DUAL && a.n_da > 0) ? 1 : 2) * NB);
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
   double* s_mats = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
   // tile index -> base offset of its outer qubits: four 64-entry deposit tables (tile bits
@@ -763,13 +763,20 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  if ((int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
+  // Adjoint passes with adjoint dense stages keep ONE (psi, lambda) tile buffer: their R
+  // accumulators need the shared memory, and a third CTA per SM hides the exposed load better than
+  // a second buffer does (the other passes double-buffer).
+  const bool dbuf = !(DUAL && a.n_da > 0);
+  if (dbuf && (int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-    const int cur = it & 1;
+    const int cur = dbuf ? (it & 1) : 0;
     const uint64_t base = tile_base(tile);
     const int64_t next = tile + gridDim.x;
-    if (next < a.ntiles) {
+    if (!dbuf) {
+      issue_load(tile, 0);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    } else if (next < a.ntiles) {
       issue_load(next, cur ^ 1);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
@@ -1204,7 +1211,7 @@ size_t dense_pass_smem_bytes(int k, int nstages) {
 
 
 size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da) {
-  size_t b = (size_t(16) << k) * (dual ? 2 : 1) * 2;  // double-buffered
+  size_t b = (size_t(16) << k) * (dual ? 2 : 1) * ((dual && n_da > 0) ? 1 : 2);  // tile buffers
   b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
   b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
   b += (size_t)nmats * 8 + 4 * 64 * 8;
