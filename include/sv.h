@@ -119,7 +119,12 @@ enum {
   SV_OPT_FUSION = 2,             /* 1 (default) fuse gates into tile passes; 0 one pass per gate  */
   SV_OPT_LOW_QUBITS = 3,         /* qubits 0..L-1 always in a tile (coalescing granule), default 3 */
   SV_OPT_DENSE = 4,              /* 1 (default): fold register stages into dense FP64-MMA stages  */
-  SV_OPT_KERNEL = 5              /* 1 (default): register-blocked kernel; 0: shared-memory kernel */
+  SV_OPT_KERNEL = 5,             /* 1 (default): register-blocked kernel; 0: shared-memory kernel */
+  SV_OPT_ADJOINT_DENSE_COST = 6 /* reverse-sweep stages whose sequential cost (2 x FMA/amp + 8 per
+                                   parametrised op) reaches this run as adjoint dense MMA stages;
+                                   -1 (default): 96 for states of >= 24 local qubits, else 250
+                                   (their fixed per-pass costs amortise over large states only);
+                                   0: every eligible stage; 1 << 20: none */
 };
 
 /* a1: |0...0> on n_qubits (1 <= n <= 40 subject to memory), current CUDA device, new stream. */

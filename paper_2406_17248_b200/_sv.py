@@ -20,6 +20,7 @@ STATUS = {0: "SV_OK", 1: "SV_E_ARG", 2: "SV_E_QUBIT_RANGE", 3: "SV_E_TARGET_CONT
           4: "SV_E_DUPLICATE_TARGET", 5: "SV_E_PARAM_RANGE", 6: "SV_E_NOT_DIFFERENTIABLE", 7: "SV_E_NOT_UNITARY",
           8: "SV_E_OOM", 9: "SV_E_CUDA", 10: "SV_E_NCCL", 11: "SV_E_POISONED"}
 SV_OPT_TILE_QUBITS, SV_OPT_FUSION, SV_OPT_LOW_QUBITS, SV_OPT_DENSE, SV_OPT_KERNEL = 1, 2, 3, 4, 5
+SV_OPT_ADJOINT_DENSE_COST = 6
 
 
 class SvError(RuntimeError):

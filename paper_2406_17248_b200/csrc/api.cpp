@@ -83,8 +83,8 @@ int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, c
   const int kCacheEntries = 8;
   uint64_t key = 1469598103934665603ull;
   key = fnv1a(gates.data(), gates.size() * sizeof(BoundGate), key);
-  const int meta[8] = {h->n_local, reverse ? 1 : 0, h->opts.tile_qubits, h->opts.low_qubits, h->opts.fusion ? 1 : 0,
-                       h->opts.kernel, h->opts.dense, (int)gates.size()};
+  const int meta[9] = {h->n_local, reverse ? 1 : 0, h->opts.tile_qubits, h->opts.low_qubits, h->opts.fusion ? 1 : 0,
+                       h->opts.kernel, h->opts.dense, h->opts.da_cost, (int)gates.size()};
   key = fnv1a(meta, sizeof(meta), key);
   for (CachedPlan* c : h->plan_cache)
     if (c->key == key) {
@@ -551,6 +551,10 @@ sv_status sv_set_option(sv_handle h, int32_t key, int64_t value) {
       return SV_OK;
     case SV_OPT_DENSE: h->opts.dense = value != 0 ? 1 : 0; return SV_OK;
     case SV_OPT_KERNEL: h->opts.kernel = value != 0 ? 1 : 0; return SV_OK;
+    case SV_OPT_ADJOINT_DENSE_COST:
+      if (value < -1 || value > (1 << 20)) return fail(SV_E_ARG, "adjoint dense cost threshold out of range");
+      h->opts.da_cost = (int)value;
+      return SV_OK;
     default: return fail(SV_E_ARG, "unknown option");
   }
 }

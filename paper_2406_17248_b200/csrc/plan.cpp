@@ -224,8 +224,19 @@ int env_int(const char* name, int dflt) {
 }
 const int g_dense_min_cost = env_int("SV_DENSE_MIN_COST", 20);
 const int g_dense_max_var = env_int("SV_DENSE_MAX_VAR", 6);
-const int g_da_min_cost = env_int("SV_DA_MIN_COST", 96);   // adjoint dense stages (0 disables: huge)
+const int g_da_min_cost = env_int("SV_DA_MIN_COST", -1);   // adjoint dense stages: cost threshold override
+// Default threshold by state size: the per-pass fixed costs of adjoint dense stages (R partials
+// written and reduced per CTA, host contraction) amortise over large states only. Measured
+// (profiles/r01_da_sweep.txt, r01_c2_da_sweep.txt): C4g 30q best at 96-150 (1.60 grad evals/s vs
+// 1.46 at 200), C2 20q best at 200-300 (303 vs 263 at 96).
+int da_min_cost_for(int n_local, int opt) {
+  if (g_da_min_cost >= 0) return g_da_min_cost;
+  if (opt >= 0) return opt;
+  return n_local >= 24 ? 96 : 250;
+}
+thread_local int t_da_min_cost = 96;
 const int g_da_enable = env_int("SV_DA", 1);
+
 const int g_da_max_tile = env_int("SV_DA_MAX_TILE", 2);
 const int g_da_max_outer = env_int("SV_DA_MAX_OUTER", 0);
 
@@ -404,7 +415,7 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     // worth it once the sequential dual cost (psi + lambda + overlaps) passes the dense cost
     int ngrad = 0;
     for (const DevOp& o : sp->ops) ngrad += o.grad_slot >= 0 ? 1 : 0;
-    if (2 * cost + 8 * ngrad < g_da_min_cost || m_outer > g_da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits)) return false;
+    if (2 * cost + 8 * ngrad < t_da_min_cost || m_outer > g_da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits)) return false;
   } else if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > g_dense_max_var) {
     return false;
   }
@@ -578,7 +589,7 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
 
 // Plans the register stages of pass `pd` (ops already emitted in pass order) and rewrites the
 // pass' op range in stage order.
-void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense) {
+void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_local, int da_cost) {
   const int k = pd->k;
   std::vector<DevOp> pops(plan->ops.begin() + pd->op_begin, plan->ops.begin() + pd->op_end);
   std::vector<StagePlan> final_stages;
@@ -603,6 +614,7 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense) {
     }
     if (!seq.empty()) add_sequential(split_stages(seq, *pd, pd->R, -1, -1));
   } else if (!forward && dense && k >= 9 && g_da_enable) {
+    t_da_min_cost = da_min_cost_for(n_local, da_cost);
     std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(g_da_max_tile, k - 8), g_da_max_tile + g_da_max_outer);
     int nda = 0;
     std::vector<DevOp> seq;
@@ -813,7 +825,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
     pd.op_end = (int)plan->ops.size();
     if (o.kernel == 1 && k - 3 >= 5) {
       pd.R = 3;
-      plan_pass_stages(plan, &pd, !reverse, o.dense != 0);
+      plan_pass_stages(plan, &pd, !reverse, o.dense != 0, n_local, o.da_cost);
     } else {
       pd.R = 0;
       pd.seq_mats = (int32_t)(plan->mats.size() - pd.mat_begin);

@@ -178,6 +178,7 @@ struct PlanOptions {
   bool fusion = true;
   int kernel = 1;        // 1: register-blocked stage kernel where possible, 0: shared-memory kernel
   int dense = 1;         // 1: dense FP64-MMA stages in forward passes where cheaper, 0: never
+  int da_cost = -1;  // adjoint dense stage cost threshold (SV_OPT_ADJOINT_DENSE_COST; -1 auto by size)
 };
 int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual);
 void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOptions& o, bool reverse_for_adjoint,

@@ -202,12 +202,33 @@ def test_gradient_random_tasks(P, n, seed):
     np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
 
 
-def test_gradient_c2_hea_20q(P):
-    """C2: 20q HEA, 10 layers, 50-term JW-shaped H (400 params)."""
+@pytest.mark.parametrize("da_cost", [-1, 0, 1 << 20])
+def test_gradient_c2_hea_20q(P, da_cost):
+    """C2: 20q HEA, 10 layers, 50-term JW-shaped H (400 params): default plan, adjoint dense
+    stages wherever eligible, and none."""
     w = W.config("C2")
     E0, g0 = oracle.adjoint_grad(w.n, w.gates, w.params, w.ham)
     sv = P.StateVector(w.n)
+    sv.set_option(P.SV_OPT_ADJOINT_DENSE_COST, da_cost)
     E, g = sv.expectation_with_grad(w.gates, w.params, w.ham)
+    sv.close()
+    assert abs(E - E0) < E_TOL
+    np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
+
+
+@pytest.mark.parametrize("n,seed", [(12, 7), (16, 8)])
+def test_gradient_adjoint_dense_forced(P, n, seed):
+    """Adjoint dense stages (R = sum psi lambda^H by MMA, host contraction) at small n: HEA
+    layers (dense-friendly) plus a random controlled tail, every eligible stage taken."""
+    h = W.hea(n, 3, seed=seed, nterms=20)
+    tail = W.random_complex(n, 2, seed=seed, n_params=0, extra_kinds=("PS",))
+    gates = list(h.gates) + list(tail.gates)
+    psi0 = W.random_state(n, seed)
+    E0, g0 = oracle.adjoint_grad(n, gates, h.params, h.ham, psi0)
+    sv = P.StateVector(n)
+    sv.set_option(P.SV_OPT_ADJOINT_DENSE_COST, 0)
+    sv.set_state(psi0)
+    E, g = sv.expectation_with_grad(gates, h.params, h.ham)
     sv.close()
     assert abs(E - E0) < E_TOL
     np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
