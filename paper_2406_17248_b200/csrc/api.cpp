@@ -385,7 +385,13 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
   const double amps = (double)(1ull << nl);
   int slot = 0;
   for (size_t p = 0; p < passes.size(); ++p, ++slot) {
-    const int mode = lam == nullptr ? 0 : (slot == 0 ? 1 : 2);
+    // lambda passes: the first writes (and gives its E), later ones accumulate; the last tiled
+    // pass reports E = Re<psi|lambda> over all tiled groups (earlier accumulating passes report 0)
+    const int mode = lam == nullptr ? 0 : (slot == 0 ? 1 : (p + 1 == passes.size() ? 3 : 2));
+    if (mode == 3) {  // its partial supersedes the first pass' one
+      e = cudaMemsetAsync(d_partials, 0, (size_t)grid * 8, h->stream);
+      if (e != cudaSuccess) return cuda_fail(h, e, "partials");
+    }
     e = psi32 ? launch_pauli_tile_c64(psi32, nl, passes[p], dz, dc, d_partials + (size_t)slot * grid, grid, h->stream)
               : launch_pauli_tile(psi, lam, mode, nl, passes[p], dz, dc, d_partials + (size_t)slot * grid, grid, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "pauli pass launch");

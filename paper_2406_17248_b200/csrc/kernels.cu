@@ -396,7 +396,8 @@ __global__ void __launch_bounds__(kThreads) k_pauli_cross(const double2* __restr
 // groups; every element evaluates all those groups from the on-chip tile: one HBM read of psi (and
 // one write / read-modify-write of lambda) for many groups instead of one pass per group.
 struct PauliTileArgs {
-  int32_t k, low, n_outer, ngroups, nterms, mode;  // mode 0: E only, 1: lam = H psi, 2: lam += H psi
+  int32_t k, low, n_outer, ngroups, nterms, mode;  // 0: E only; 1: lam = H_pass psi (+E); 2: lam += H_pass psi;
+                                                   // 3: lam += H_pass psi, E = Re<psi|lam> (last tiled pass)
   int8_t tq[16];
   int8_t oq[64];
   int64_t ntiles;
@@ -499,9 +500,18 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
     else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     if (per_thread == EPT) {
+      // modes 2 / 3 (lambda += this pass' groups): the old lambda values are loaded first, so
+      // their HBM latency overlaps the group evaluation, and the sum is stored once
       double2 l[EPT];
 #pragma unroll
-      for (int j = 0; j < EPT; ++j) l[j] = make_double2(0.0, 0.0);
+      for (int j = 0; j < EPT; ++j) {
+        if (a.mode >= 2) {
+          const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
+          l[j] = lam[base | (e & lowmask) | s_hi[e >> a.low]];
+        } else {
+          l[j] = make_double2(0.0, 0.0);
+        }
+      }
       // e = tid + 256 j: the sign (-1)^{popc(e & zt)} factors into a per-thread part
       // (-1)^{popc(tid & zt)}, folded into the coefficient once per term, and a j part read from
       // the term's 16-bit Walsh row W(zt >> 8) (bit j = parity(j & (zt >> 8))). A single-term
@@ -549,12 +559,8 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
         const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
-        acc += re_conj_mul(amp(tp[e]), l[j]);
-        if (a.mode != 0) {
-          const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
-          if (a.mode == 1) lam[gi] = l[j];
-          else { double2 o = lam[gi]; o.x += l[j].x; o.y += l[j].y; lam[gi] = o; }
-        }
+        if (a.mode != 2) acc += re_conj_mul(amp(tp[e]), l[j]);  // mode 3: Re<psi|lambda> of all passes so far
+        if (a.mode != 0) lam[base | (e & lowmask) | s_hi[e >> a.low]] = l[j];
       }
     } else {
       for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
@@ -571,12 +577,14 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
           l.x += w.x;
           l.y += w.y;
         }
-        acc += re_conj_mul(amp(tp[e]), l);
-        if (a.mode != 0) {
-          const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
-          if (a.mode == 1) lam[gi] = l;
-          else { double2 o = lam[gi]; o.x += l.x; o.y += l.y; lam[gi] = o; }
+        const uint64_t gi = base | (e & lowmask) | s_hi[e >> a.low];
+        if (a.mode >= 2) {
+          const double2 o = lam[gi];
+          l.x += o.x;
+          l.y += o.y;
         }
+        if (a.mode != 2) acc += re_conj_mul(amp(tp[e]), l);
+        if (a.mode != 0) lam[gi] = l;
       }
     }
   }
