@@ -413,6 +413,10 @@ __device__ __forceinline__ double2 amp(double2 v) { return v; }
 __device__ __forceinline__ double2 amp(float2 v) { return make_double2((double)v.x, (double)v.y); }
 
 // Walsh row of a 4-bit mask h: bit j (j < 16) = parity(j & h).
+// k_pauli_tile geometry: 2^12-amplitude tiles, 512 threads (16 warps: the kernel is latency-bound
+// with one 8-warp CTA per SM), 8 elements per thread
+constexpr int kPauliThreads = 512, kPauliTidBits = 9;
+
 __device__ __forceinline__ uint32_t walsh16(uint32_t h) {
   uint32_t r = 0;
   if (h & 1u) r ^= 0xAAAAu;  // bit 0 of j
@@ -423,14 +427,14 @@ __device__ __forceinline__ uint32_t walsh16(uint32_t h) {
 }
 
 template <typename T>  // T: double2 (complex128 state) or float2 (complex64 state, E only)
-__global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ psi, double2* __restrict__ lam,
+__global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __restrict__ psi, double2* __restrict__ lam,
                                                          PauliTileArgs a) {
   // Per tile the rank / outer-bit part of every term's sign is folded into its coefficient; per
   // element only the tile bits remain: sign_t(e) = (-1)^{popc(e & zt_t)} with zt_t the term's Z
   // support in tile-position space. Loops run term-outer / element-inner (EPT elements per thread
   // in registers) so each term's data is read once per thread per tile and the element updates are
   // independent (ILP).
-  constexpr int EPT = 16;
+  constexpr int EPT = 4096 / kPauliThreads;  // elements per thread of a 2^12 tile
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
   T* tile_buf = reinterpret_cast<T*>(smem_raw);  // two tiles
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
   uint32_t* s_zt = reinterpret_cast<uint32_t*>(s_z + a.nterms); // tile-position Z masks
   const int nhi = 1 << (a.k - a.low);
   uint64_t* s_hi = reinterpret_cast<uint64_t*>(s_zt + ((a.nterms + 1) & ~1));
-  __shared__ double s_red[kThreads / 32];
+  __shared__ double s_red[kPauliThreads / 32];
   uint64_t tmask = 0;
   for (int p = 0; p < a.k; ++p) tmask |= 1ull << a.tq[p];
   for (int i = threadIdx.x; i < a.nterms; i += blockDim.x) {
@@ -512,9 +516,9 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
           l[j] = make_double2(0.0, 0.0);
         }
       }
-      // e = tid + 256 j: the sign (-1)^{popc(e & zt)} factors into a per-thread part
+      // e = tid + kPauliThreads j: the sign (-1)^{popc(e & zt)} factors into a per-thread part
       // (-1)^{popc(tid & zt)}, folded into the coefficient once per term, and a j part read from
-      // the term's 16-bit Walsh row W(zt >> 8) (bit j = parity(j & (zt >> 8))). A single-term
+      // the term's Walsh row W(zt >> tid bits) (bit j = parity(j & (zt >> tid bits))). A single-term
       // group needs no accumulation at all: its j sign goes onto the product.
       const uint32_t tid = threadIdx.x;
       for (int g = 0; g < a.ngroups; ++g) {
@@ -523,11 +527,11 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
         if (te - tb == 1) {
           const uint32_t zt = s_zt[tb];
           double2 c = s_c[tb];
-          if (__popc(tid & zt & 0xffu) & 1) c = make_double2(-c.x, -c.y);
-          const uint32_t wr = walsh16(zt >> 8);
+          if (__popc(tid & zt & (uint32_t)(kPauliThreads - 1)) & 1) c = make_double2(-c.x, -c.y);
+          const uint32_t wr = walsh16(zt >> kPauliTidBits);
 #pragma unroll
           for (int j = 0; j < EPT; ++j) {
-            const double2 w = cmul(c, amp(tp[(tid + (uint32_t)j * 256u) ^ xt]));
+            const double2 w = cmul(c, amp(tp[(tid + (uint32_t)j * (uint32_t)kPauliThreads) ^ xt]));
             const bool neg = (wr >> j) & 1u;
             l[j].x += neg ? -w.x : w.x;
             l[j].y += neg ? -w.y : w.y;
@@ -540,8 +544,8 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
         for (int t = tb; t < te; ++t) {
           const uint32_t zt = s_zt[t];
           double2 c = s_c[t];
-          if (__popc(tid & zt & 0xffu) & 1) c = make_double2(-c.x, -c.y);
-          const uint32_t wr = walsh16(zt >> 8);
+          if (__popc(tid & zt & (uint32_t)(kPauliThreads - 1)) & 1) c = make_double2(-c.x, -c.y);
+          const uint32_t wr = walsh16(zt >> kPauliTidBits);
 #pragma unroll
           for (int j = 0; j < EPT; ++j) {
             const bool neg = (wr >> j) & 1u;
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_tile(const T* __restrict__ p
         }
 #pragma unroll
         for (int j = 0; j < EPT; ++j) {
-          const double2 w = cmul(C[j], amp(tp[(tid + (uint32_t)j * 256u) ^ xt]));
+          const double2 w = cmul(C[j], amp(tp[(tid + (uint32_t)j * (uint32_t)kPauliThreads) ^ xt]));
           l[j].x += w.x;
           l[j].y += w.y;
         }
@@ -901,9 +905,9 @@ static cudaError_t pauli_tile_impl(const void* psi, bool c64, double* lam, int m
   }
   if (c64) {
     if (lam || mode != 0 || pp.tq[0] != 0) return cudaErrorInvalidValue;  // E only; pairs need qubit 0 at position 0
-    k_pauli_tile<float2><<<grid, kThreads, smem, s>>>(reinterpret_cast<const float2*>(psi), nullptr, a);
+    k_pauli_tile<float2><<<grid, kPauliThreads, smem, s>>>(reinterpret_cast<const float2*>(psi), nullptr, a);
   } else {
-    k_pauli_tile<double2><<<grid, kThreads, smem, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<double2*>(lam), a);
+    k_pauli_tile<double2><<<grid, kPauliThreads, smem, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<double2*>(lam), a);
   }
   return cudaGetLastError();
 }
