@@ -236,6 +236,7 @@ int da_min_cost_for(int n_local, int opt) {
 }
 thread_local int t_da_min_cost = 96;
 const int g_da_enable = env_int("SV_DA", 1);
+const int g_da_max_per_pass = env_int("SV_DA_MAX_PER_PASS", kMaxDAPerPass);
 
 const int g_da_max_tile = env_int("SV_DA_MAX_TILE", 2);
 const int g_da_max_outer = env_int("SV_DA_MAX_OUTER", 0);
@@ -619,7 +620,7 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
     int nda = 0;
     std::vector<DevOp> seq;
     for (StagePlan& sp : st4) {
-      if (nda < kMaxDAPerPass && make_dense(&sp, *pd, plan, size_t(1) << 22, true, (int)plan->passes.size(), nda)) {
+      if (nda < g_da_max_per_pass && make_dense(&sp, *pd, plan, size_t(1) << 22, true, (int)plan->passes.size(), nda)) {
         ++nda;
         if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
         final_stages.push_back(std::move(sp));

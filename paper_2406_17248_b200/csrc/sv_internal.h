@@ -148,7 +148,7 @@ struct Plan {
   mutable int grid_cache = 0, grid_cache_n = -1;  // plan_grid memo (occupancy query once per plan)
   mutable std::vector<int> pass_grid;             // per-pass CTAs (register passes: occupancy of that pass)
 };
-constexpr int kMaxDAPerPass = 2;  // R accumulators: 32 KiB of shared memory per adjoint dense stage
+constexpr int kMaxDAPerPass = 4;  // adjoint dense stages per pass (16 KiB of R accumulators each at 2^10 tiles; measured best, profiles/r01_da_per_pass_sweep.txt)
 
 // ---------------------------------------------------------------------------------------------
 // Host-side gate after binding: class + entries, logical qubits.

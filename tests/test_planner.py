@@ -38,7 +38,7 @@ def test_plan_invariants(n, adjoint):
                 else:
                     assert p["n_stages"] >= 1 and p["k"] - p["R"] >= 5
                 if adjoint:
-                    assert p["n_dense"] <= 2  # adjoint dense stages (R accumulators) per reverse pass
+                    assert p["n_dense"] <= 4  # adjoint dense stages (R accumulators) per reverse pass
 
 
 def test_fusion_reduces_passes_for_c4():
