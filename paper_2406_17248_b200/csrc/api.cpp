@@ -134,8 +134,8 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
   size_t da_done = 0;
   for (size_t i = 0; i < plan.passes.size(); ++i) {
     const PassDesc& pd = plan.passes[i];
-    int n_da = 0;
-    for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? 1 : 0;
+    int n_da = 0;  // R accumulator slots
+    for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? (1 << plan.stages[si].m_outer) : 0;
     const int next_mat = (i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size();
     PassLaunch L;
     L.pd = &pd;
@@ -840,9 +840,10 @@ int sv::run_reverse(sv_state_s* h, const CachedPlan& cp, double* psi, double* la
   if (rev.passes.empty()) return SV_OK;
   const int agrid = plan_grid(rev, h->n_local);
   const size_t nda = rev.da.size();
+  const size_t nslots_r = (size_t)rev.da_slots_total;
   const int nw = (1 << (rev.passes[0].k - rev.passes[0].R)) / 32;
   const size_t part_slots = ns * (size_t)agrid;
-  const size_t r_part = nda ? (size_t)rev.max_da_per_pass * nw * 512 * agrid : 0, r_sum = nda * (size_t)nw * 512;
+  const size_t r_part = nda ? (size_t)rev.max_da_per_pass * nw * 512 * agrid : 0, r_sum = nslots_r * (size_t)nw * 512;
   if (!h->work_r.ensure((part_slots + ns + r_part + r_sum) * 8 + 64)) return fail(SV_E_OOM, "adjoint buffers");
   double* dp = static_cast<double*>(h->work_r.p);
   double* dout = dp + part_slots;
@@ -865,11 +866,12 @@ int sv::run_reverse(sv_state_s* h, const CachedPlan& cp, double* psi, double* la
   h->stats.kernel_launches += ns ? 1 : 0;
   for (size_t di = 0; di < nda; ++di) {
     const Plan::DAStage& ds = rev.da[di];
-    const int nvar = 1 << ds.m_tile;
+    const int ntv = 1 << ds.m_tile, nvar = 1 << (ds.m_tile + ds.m_outer);
     std::vector<Cx> R((size_t)nvar * 256, Cx{0, 0});
+    for (int ov = 0; ov < (1 << ds.m_outer); ++ov)
     for (int w = 0; w < nw; ++w) {
-      const int var = w & (nvar - 1);
-      const double* f = rs.data() + (di * nw + (size_t)w) * 512;
+      const int var = (w & (ntv - 1)) | (ov << ds.m_tile);
+      const double* f = rs.data() + ((size_t)(ds.global_slot + ov) * nw + (size_t)w) * 512;
       for (int mt = 0; mt < 2; ++mt)
         for (int nt = 0; nt < 2; ++nt)
           for (int v = 0; v < 2; ++v)

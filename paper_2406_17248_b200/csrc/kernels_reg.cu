@@ -790,8 +790,10 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
       const StageDesc& S = s_st[st];
       if constexpr (DUAL) {
         if (S.dense == 2) {
+          uint32_t ov = 0;  // outer variant of this tile: its own R slot
+          for (int b = 0; b < S.m_outer; ++b) ov |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << b;
           da_stage(tp, tl, S, reinterpret_cast<const double2*>(a.mats), base, warp, lane,
-                   s_racc + ((size_t)S.da_index * nwarps + warp) * 512);
+                   s_racc + ((size_t)(S.da_index + ov) * nwarps + warp) * 512);
           __syncthreads();
           continue;
         }
@@ -1248,7 +1250,7 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual) {
   const int next_mat = (i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size();
   const int nm = std::min(pd.seq_mats, next_mat - pd.mat_begin);
   int n_da = 0;
-  for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? 1 : 0;
+  for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? (1 << plan.stages[si].m_outer) : 0;
   const int nthr = 1 << (pd.k - pd.R);
   const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
                                      pd.n_grad, nthr, dual, n_da);

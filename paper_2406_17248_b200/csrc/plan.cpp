@@ -239,7 +239,7 @@ const int g_da_enable = env_int("SV_DA", 1);
 const int g_da_max_per_pass = env_int("SV_DA_MAX_PER_PASS", kMaxDAPerPass);
 
 const int g_da_max_tile = env_int("SV_DA_MAX_TILE", 2);
-const int g_da_max_outer = env_int("SV_DA_MAX_OUTER", 0);
+const int g_da_max_outer = env_int("SV_DA_MAX_OUTER", 1);  // outer variant bits of an adjoint dense stage (profiles/r01_da_outer_sweep.txt)
 
 // FP64 pipe cost per amplitude of an op applied sequentially (DFMA path), for the dense choice.
 int seq_cost(const DevOp& o, const double* m) {
@@ -385,7 +385,7 @@ void dense_gen_apply(Cx* u, const DevOp& o, const double* gm, const int* reg_new
 // the sequential path and feasible: variant bits <= 3 in total, tile variant bits on warp
 // positions. Returns false (stage untouched) otherwise.
 bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles, bool adjoint = false,
-                int pass_index = 0, int da_index = 0) {
+                int pass_index = 0, int da_index = 0, int da_slots_left = 0) {
   const int k = pd.k;
   const int nw_bits = k - 8;  // 2^(k-3) threads: 16 vectors of 16 amplitudes per warp
   if (nw_bits < 1 || __builtin_popcount(sp->regset) > 4) return false;
@@ -416,7 +416,9 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     // worth it once the sequential dual cost (psi + lambda + overlaps) passes the dense cost
     int ngrad = 0;
     for (const DevOp& o : sp->ops) ngrad += o.grad_slot >= 0 ? 1 : 0;
-    if (2 * cost + 8 * ngrad < t_da_min_cost || m_outer > g_da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits)) return false;
+    if (2 * cost + 8 * ngrad < t_da_min_cost || m_outer > g_da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits) ||
+        (1 << m_outer) > da_slots_left)
+      return false;
   } else if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > g_dense_max_var) {
     return false;
   }
@@ -530,6 +532,8 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     ds.pass = pass_index;
     ds.da_index = da_index;
     ds.m_tile = m_tile;
+    ds.m_outer = m_outer;
+    ds.global_slot = plan->da_slots_total + da_index;
     // B_{j,var} = V^dagger (Pi_C G_j) V with V the product of the stage's ops before j
     for (size_t i = 0; i < sp->ops.size(); ++i)
       if (sp->ops[i].grad_slot >= 0) {
@@ -541,6 +545,9 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
       uint32_t tbits = 0;
       for (int b = 0; b < m_tile; ++b)
         if ((v >> b) & 1) tbits |= 1u << vlist[b];
+      uint64_t obits = 0;
+      for (int b = 0; b < m_outer; ++b)
+        if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
       Cx V[256];  // columns c: V[j * 16 + c]
       for (int j = 0; j < 16; ++j)
         for (int c = 0; c < 16; ++c) V[j * 16 + c] = Cx{j == c ? 1.0 : 0.0, 0.0};
@@ -551,7 +558,7 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
           for (int c = 0; c < 16; ++c) {
             Cx u[16];
             for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
-            dense_gen_apply(u, o, plan->mats.data() + pd.mat_begin + o.gen_off, reg_new, tbits, 0);
+            dense_gen_apply(u, o, plan->mats.data() + pd.mat_begin + o.gen_off, reg_new, tbits, obits);
             for (int j = 0; j < 16; ++j) GV[j * 16 + c] = u[j];
           }
           Cx* Bd = ds.B[(size_t)gj].data() + (size_t)v * 256;
@@ -571,7 +578,7 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
         for (int c = 0; c < 16; ++c) {
           Cx u[16];
           for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
-          dense_apply(u, o, plan->mats.data() + pd.mat_begin + o.mat_off, reg_new, tbits, 0);
+          dense_apply(u, o, plan->mats.data() + pd.mat_begin + o.mat_off, reg_new, tbits, obits);
           for (int j = 0; j < 16; ++j) V[j * 16 + c] = u[j];
         }
       }
@@ -617,11 +624,12 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
   } else if (!forward && dense && k >= 9 && g_da_enable) {
     t_da_min_cost = da_min_cost_for(n_local, da_cost);
     std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(g_da_max_tile, k - 8), g_da_max_tile + g_da_max_outer);
-    int nda = 0;
+    int nda = 0;  // R accumulator slots of this pass (2^m_outer per adjoint dense stage)
     std::vector<DevOp> seq;
     for (StagePlan& sp : st4) {
-      if (nda < g_da_max_per_pass && make_dense(&sp, *pd, plan, size_t(1) << 22, true, (int)plan->passes.size(), nda)) {
-        ++nda;
+      if (nda < g_da_max_per_pass &&
+          make_dense(&sp, *pd, plan, size_t(1) << 22, true, (int)plan->passes.size(), nda, g_da_max_per_pass - nda)) {
+        nda += 1 << sp.sd.m_outer;
         if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
         final_stages.push_back(std::move(sp));
       } else {
@@ -630,6 +638,7 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
     }
     if (!seq.empty()) add_sequential(split_stages(seq, *pd, pd->R, -1, -1));
     plan->max_da_per_pass = std::max(plan->max_da_per_pass, nda);
+    plan->da_slots_total += nda;
   } else {
     add_sequential(split_stages(pops, *pd, pd->R, -1, -1));
   }
@@ -755,6 +764,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
   plan->stages.clear();
   plan->da.clear();
   plan->max_da_per_pass = 0;
+  plan->da_slots_total = 0;
   plan->slot_param.clear();
   plan->slot_coeff.clear();
   plan->n_grad_slots = 0;

@@ -82,7 +82,7 @@ struct StageDesc {
   // with amp = 8 mt + lane/4, vector = 4 kt + lane%4
   uint16_t lane_r[32];       // swz(lane part of the R-fragment load address)
   uint16_t off_r[8];         // swz(uniform part) for (mt, kt), index mt * 4 + kt
-  int32_t da_index;          // index among the pass' adjoint dense stages (R accumulator slot)
+  int32_t da_index;          // first R accumulator slot of this adjoint dense stage in its pass (+ outer variant)
   int32_t pad1;
 };
 static_assert(sizeof(StageDesc) == 312, "StageDesc layout");
@@ -138,12 +138,14 @@ struct Plan {
   // per-variant correlation matrices R_var = sum psi lambda^H at the stage start (accumulated on the
   // device) as d_j = sum_var tr(B_{j,var} R_var), B_{j,var} = V_{j-1}^dagger (Pi_C G_j) V_{j-1}.
   struct DAStage {
-    int pass = 0, da_index = 0, m_tile = 0;
+    int pass = 0, da_index = 0, m_tile = 0, m_outer = 0;
+    int global_slot = 0;                 // first R slot (plan order); one slot per outer variant
     std::vector<int> slots;              // grad slots of the stage's parametrised ops (stage order)
     std::vector<std::vector<Cx>> B;      // [grad op][var * 256 + a * 16 + b]
   };
   std::vector<DAStage> da;
-  int max_da_per_pass = 0;
+  int max_da_per_pass = 0;  // R accumulator slots (2^m_outer per adjoint dense stage) of the largest pass
+  int da_slots_total = 0;
   bool reverse = false;  // adjoint plan: passes run on (psi, lambda) with the DUAL kernel
   mutable int grid_cache = 0, grid_cache_n = -1;  // plan_grid memo (occupancy query once per plan)
   mutable std::vector<int> pass_grid;             // per-pass CTAs (register passes: occupancy of that pass)

@@ -234,6 +234,20 @@ def test_gradient_adjoint_dense_forced(P, n, seed):
     np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
 
 
+@pytest.mark.parametrize("n,dc", [(12, False), (14, True), (16, False)])
+def test_gradient_qaoa_adjoint_dense_outer_variants(P, n, dc):
+    """QAOA (RZZ edges leaving the tile): adjoint dense stages whose variant bits include outer
+    qubits (one R accumulator per outer variant), forced on at small n."""
+    w = W.qaoa(n, 3, seed_graph=n, seed_angles=n + 1, dc=dc)
+    E0, g0 = oracle.adjoint_grad(n, w.gates, w.params, w.ham)
+    sv = P.StateVector(n)
+    sv.set_option(P.SV_OPT_ADJOINT_DENSE_COST, 0)
+    E, g = sv.expectation_with_grad(w.gates, w.params, w.ham)
+    sv.close()
+    assert abs(E - E0) < E_TOL
+    np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
+
+
 def test_gradient_qaoa_p1_24q_closed_form(P):
     """C3 graph at p=1: E and the shared-parameter gradient vs the Wang et al. closed form."""
     from test_oracle import _qaoa_p1_closed_form
