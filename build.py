@@ -31,6 +31,7 @@ def build_lib(force=False, verbose=False):
         return LIB
     cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *srcs, "-lnccl"]
+    cmd[1:1] = os.environ.get("SV_NVCC_DEFS", "").split()  # experiment knobs, e.g. -DSV_DUAL_CTAS=4
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

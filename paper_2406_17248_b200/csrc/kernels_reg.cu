@@ -29,7 +29,12 @@
 
 #ifndef SV_FWD_CTAS
 #define SV_FWD_CTAS 3   // forward-pass CTAs per SM (register budget 65536 / (256 * CTAs))
+#endif
+#ifndef SV_DUAL_CTAS
 #define SV_DUAL_CTAS 3  // adjoint-pass (2^10-tile, 128-thread) CTAs per SM (register cap 65536 / (128 * 3))
+#endif
+#ifndef SV_DUAL_SINGLE_BUF
+#define SV_DUAL_SINGLE_BUF 0  // 1: every adjoint pass single-buffers its tile (more CTAs per SM)
 #endif
 
 namespace sv {
@@ -433,7 +438,7 @@ __device__ __forceinline__ double dual_diag(double2 (&v)[1 << NR], double2 (&w)[
     q[0] = tb ? q[2] : q[0];
     q[1] = tb ? q[3] : q[1];
   }
-  double acc = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains (FP64 latency, few warps)
   if (!ok) return 0.0;
 #pragma unroll
   for (int j = 0; j < (1 << NR); ++j) {
@@ -443,12 +448,12 @@ __device__ __forceinline__ double dual_diag(double2 (&v)[1 << NR], double2 (&w)[
     const int idx = i0 | (i1 << 1);
     if (gen) {
       const double2 p = make_double2(fma(w[j].x, v[j].x, w[j].y * v[j].y), fma(w[j].x, v[j].y, -w[j].y * v[j].x));
-      acc += fma(q[idx].x, p.x, -q[idx].y * p.y);  // Re(g conj(w) v)
+      acc[j & 3] = fma(q[idx].x, p.x, fma(-q[idx].y, p.y, acc[j & 3]));  // Re(g conj(w) v)
     }
     v[j] = cmul(d[idx], v[j]);
     w[j] = cmul(d[idx], w[j]);
   }
-  return acc;
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // DUAL (adjoint) op with ONE register-position dispatch: the overlap Re<w|(Pi_C (x) G)|v> of a
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   const uint32_t NB = DUAL ? 2 * N : N;  // doubles2 per buffer (psi [+ lambda])
   double2* smem_tiles = reinterpret_cast<double2*>(smem_raw);
   double2* tp = smem_tiles;  // (setup-phase alias; the tile loop rebinds per buffer)
-  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + ((DUAL && a.n_da > 0) ? 1 : 2) * NB);
+  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + ((DUAL && (a.n_da > 0 || SV_DUAL_SINGLE_BUF)) ? 1 : 2) * NB);
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
   double* s_mats = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
   // tile index -> base offset of its outer qubits: four 64-entry deposit tables (tile bits
@@ -766,7 +771,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   // Adjoint passes with adjoint dense stages keep ONE (psi, lambda) tile buffer: their R
   // accumulators need the shared memory, and a third CTA per SM hides the exposed load better than
   // a second buffer does (the other passes double-buffer).
-  const bool dbuf = !(DUAL && a.n_da > 0);
+  const bool dbuf = !(DUAL && (a.n_da > 0 || SV_DUAL_SINGLE_BUF));
   if (dbuf && (int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
@@ -1213,7 +1218,7 @@ size_t dense_pass_smem_bytes(int k, int nstages) {
 
 
 size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da) {
-  size_t b = (size_t(16) << k) * (dual ? 2 : 1) * ((dual && n_da > 0) ? 1 : 2);  // tile buffers
+  size_t b = (size_t(16) << k) * (dual ? 2 : 1) * ((dual && (n_da > 0 || SV_DUAL_SINGLE_BUF)) ? 1 : 2);  // tile buffers
   b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
   b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
   b += (size_t)nmats * 8 + 4 * 64 * 8;
