@@ -17,6 +17,23 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
+def _nccl_flags():
+    """Link the NCCL that PyTorch loads (the nvidia-nccl wheel, 2.28) rather than the system one
+    (2.27): one process can hold only one libnccl.so.2, and torch needs the newer symbols — if this
+    library pulled in the system copy first, a later `import torch` would fail."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            lib = os.path.join(base, "lib")
+            if os.path.exists(os.path.join(lib, "libnccl.so.2")):
+                return ["-I", os.path.join(base, "include"), "-L", lib, "-l:libnccl.so.2",
+                        "-Xlinker", "-rpath=" + lib]
+    except Exception:
+        pass
+    return ["-lnccl"]
+
+
 def _stale(target, deps):
     if not os.path.exists(target):
         return True
@@ -30,7 +47,7 @@ def build_lib(force=False, verbose=False):
     if not force and not _stale(LIB, deps):
         return LIB
     cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *srcs, "-lnccl"]
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *srcs, *_nccl_flags()]
     cmd[1:1] = os.environ.get("SV_NVCC_DEFS", "").split()  # experiment knobs, e.g. -DSV_DUAL_CTAS=4
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -57,3 +57,14 @@ def test_no_oracle_in_product_path():
             if f.endswith((".py", ".cpp", ".cu", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "sv_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_library_then_torch_import():
+    """libsv.so loaded before torch must not shadow torch's NCCL (one libnccl.so.2 per process):
+    __graft_entry__.build() imports the package first, smoke() imports torch afterwards."""
+    import subprocess
+    import sys
+    code = ("import ctypes, os; ctypes.CDLL(os.path.join('paper_2406_17248_b200', 'libsv.so')); "
+            "import torch; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
