@@ -20,6 +20,7 @@
 // shards (all P shards on one GPU, sv_create_virtual_shards) used to test the sharded executor on
 // one device.
 #include <nccl.h>
+#include <cstdlib>
 
 #include <algorithm>
 #include <cstring>
@@ -237,6 +238,35 @@ int swap_qubits(sv_state_s* h, const std::vector<std::vector<double*>>& vecs, in
   const int nl = h->n_local;
   const int j = G - nl;
   h->stats.exchanges += 1;
+  // SV_VIRTUAL_BOUNCE=<chunk amplitudes>: virtual shards exchange through the NCCL path's
+  // pack / bounce-buffer / unpack sequence (device copies instead of ncclSend/ncclRecv), chunked,
+  // so the tests exercise that code on one GPU.
+  const char* bounce_env = std::getenv("SV_VIRTUAL_BOUNCE");
+  const int64_t bounce_chunk = bounce_env ? std::max<int64_t>(1, std::atoll(bounce_env)) : 0;
+  if (S.virt && bounce_chunk > 0) {
+    const int64_t half = int64_t(1) << (nl - 1);
+    const int64_t chunk = std::min(half, bounce_chunk);
+    if (!S.sendb.ensure((size_t)chunk * 16) || !S.recvb.ensure((size_t)chunk * 16)) return fail(SV_E_OOM, "bounce buffers");
+    for (const auto& v : vecs) {
+      for (size_t a = 0; a < S.ranks.size(); ++a) {
+        const int r = S.ranks[a];
+        if ((r >> j) & 1) continue;
+        const size_t p = (size_t)(r | (1 << j));
+        for (int64_t off = 0; off < half; off += chunk) {
+          const int64_t cnt = std::min(chunk, half - off);
+          // r packs its half with bit L = 1, p its half with bit L = 0; each unpacks the other's
+          cudaError_t e = launch_pack_half(v[a], static_cast<double*>(S.sendb.p), L, 1, off, cnt, true, h->stream);
+          if (e == cudaSuccess) e = launch_pack_half(v[p], static_cast<double*>(S.recvb.p), L, 0, off, cnt, true, h->stream);
+          if (e == cudaSuccess) e = launch_pack_half(v[a], static_cast<double*>(S.recvb.p), L, 1, off, cnt, false, h->stream);
+          if (e == cudaSuccess) e = launch_pack_half(v[p], static_cast<double*>(S.sendb.p), L, 0, off, cnt, false, h->stream);
+          if (e != cudaSuccess) return cuda_fail(h, e, "bounce exchange");
+          h->stats.kernel_launches += 4;
+        }
+      }
+    }
+    h->stats.algorithmic_bytes += 32.0 * (double)(1ull << nl) * (double)S.ranks.size() * vecs.size() / 2.0;
+    return SV_OK;
+  }
   if (S.virt) {
     for (const auto& v : vecs) {
       for (size_t a = 0; a < S.ranks.size(); ++a) {
