@@ -11,7 +11,7 @@ import torch  # noqa: E402
 import paper_2406_17248_b200 as P  # noqa: E402
 import workloads as W  # noqa: E402
 
-n = 30
+n = int(os.environ.get("EXP_N", "30"))
 sv = P.StateVectorC64(n) if os.environ.get("EXP_C64") else P.StateVector(n)
 stream = torch.cuda.Stream()
 P.sv_set_stream(sv.h, stream.cuda_stream)
@@ -49,7 +49,7 @@ ms = a.elapsed_time(b) / 5
 print(f"torch copy 16 GiB: {ms:.2f} ms {2 * 16 * 2**n / ms / 1e6:.0f} GB/s", flush=True)
 del x, y
 rng = np.random.default_rng(1)
-for name, gates in (("Z q0", [G("Z", (0,))]), ("X q0", [G("X", (0,))]), ("H q29", [G("H", (29,))])):
+for name, gates in (("Z q0", [G("Z", (0,))]), ("X q0", [G("X", (0,))]), ("H q(n-1)", [G("H", (n - 1,))])):
     ms = t(gates)
     print(f"{name}: {ms:.2f} ms {2 * 16 * 2**n / ms / 1e6:.0f} GB/s", flush=True)
 width = int(os.environ.get("EXP_WIDTH", "11"))
