@@ -979,40 +979,11 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
     }
     return SV_OK;
   }
-  // bind every row (validates every row; the structure is row-independent): row 0 through the
-  // normal path, the others on host threads (binding = angle -> matrix per gate and row, the
-  // host-side cost that dominated small-n batches)
-  std::vector<std::vector<BoundGate>> rows((size_t)n_rows);
+  // row 0 is bound (and validated) through the normal path; the other rows only re-bind their
+  // parametrised gates (below, on host threads, straight into the matrix block)
+  std::vector<std::vector<BoundGate>> rows(1);
   rc = bind_circuit(h, gates, n_gates, params, n_params, true, &rows[0]);
   if (rc) return fail(rc, std::string("row 0: ") + g_last_error);
-  {
-    std::vector<int> row_rc((size_t)n_rows, SV_OK);
-    std::vector<std::string> row_err((size_t)n_rows);
-    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    const int nt = std::max(1, std::min(hw, (n_rows - 1 + 63) / 64));
-    auto work = [&](int t) {
-      for (int32_t r = 1 + t; r < n_rows; r += nt) {
-        std::vector<BoundGate>& out = rows[(size_t)r];
-        out.resize((size_t)n_gates);
-        const double* pr = params ? params + (size_t)r * n_params : nullptr;
-        for (int64_t i = 0; i < n_gates; ++i) {
-          std::string err;
-          const int grc = bind_gate(h->n, &gates[i], pr, n_params, true, &out[(size_t)i], &err);
-          if (grc != SV_OK) {
-            row_rc[(size_t)r] = grc;
-            row_err[(size_t)r] = "gate " + std::to_string(i) + ": " + err;
-            break;
-          }
-        }
-      }
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
-    work(0);
-    for (std::thread& th : pool) th.join();
-    for (int32_t r = 1; r < n_rows; ++r)
-      if (row_rc[(size_t)r] != SV_OK) return fail(row_rc[(size_t)r], std::string("row ") + std::to_string(r) + ": " + row_err[(size_t)r]);
-  }
   PauliGroups G;
   rc = group_terms(h, terms, n_terms, &G);
   if (rc) return rc;
@@ -1055,8 +1026,41 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
   }
   const int64_t stride = mo;
   std::vector<Cx> mats((size_t)stride * n_rows);
-  for (int32_t r = 0; r < n_rows; ++r)
-    for (size_t k = 0; k < g0.size(); ++k) full(rows[(size_t)r][k], mats.data() + (size_t)r * stride + ops[k].mat_off);
+  for (size_t k = 0; k < g0.size(); ++k) full(g0[k], mats.data() + ops[k].mat_off);
+  std::vector<int64_t> pgates;  // the row-dependent (parametrised) gates
+  for (size_t k = 0; k < g0.size(); ++k)
+    if (g0[k].param >= 0) pgates.push_back((int64_t)k);
+  {
+    std::vector<int> row_rc((size_t)n_rows, SV_OK);
+    std::vector<std::string> row_err((size_t)n_rows);
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int nt = std::max(1, std::min(hw, (n_rows - 1 + 255) / 256));
+    auto work = [&](int t) {
+      BoundGate b;
+      std::string err;
+      for (int32_t r = 1 + t; r < n_rows; r += nt) {
+        Cx* mr = mats.data() + (size_t)r * stride;
+        std::memcpy(mr, mats.data(), (size_t)stride * sizeof(Cx));  // row-independent gates
+        const double* pr = params ? params + (size_t)r * n_params : nullptr;
+        for (int64_t k : pgates) {
+          const int grc = bind_gate(h->n, &gates[k], pr, n_params, true, &b, &err);
+          if (grc != SV_OK) {
+            row_rc[(size_t)r] = grc;
+            row_err[(size_t)r] = "gate " + std::to_string(k) + ": " + err;
+            break;
+          }
+          full(b, mr + ops[(size_t)k].mat_off);
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (std::thread& th : pool) th.join();
+    for (int32_t r = 1; r < n_rows; ++r)
+      if (row_rc[(size_t)r] != SV_OK)
+        return fail(row_rc[(size_t)r], std::string("row ") + std::to_string(r) + ": " + row_err[(size_t)r]);
+  }
   std::vector<uint64_t> xs, zs;
   std::vector<double> cs;
   for (size_t gi = 0; gi < G.xs.size(); ++gi)
