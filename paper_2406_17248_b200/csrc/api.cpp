@@ -43,6 +43,26 @@ bool DevBuf::ensure(size_t bytes) {
   cap = want;
   return true;
 }
+bool PinnedBuf::ensure(size_t bytes) {
+  if (bytes <= cap) return true;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  cap = 0;
+  const size_t want = bytes < 65536 ? 65536 : bytes + bytes / 4;
+  if (cudaMallocHost(&p, want) != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return false;
+  }
+  cap = want;
+  return true;
+}
+void PinnedBuf::release() {
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  cap = 0;
+}
+
 void DevBuf::release() {
   if (p) cudaFree(p);
   p = nullptr;
@@ -523,6 +543,8 @@ sv_status sv_destroy(sv_handle h) {
   cudaStreamSynchronize(h->stream);
   h->state.release();
   h->promo.release();
+  h->pin_in.release();
+  h->pin_out.release();
   h->work_psi.release();
   h->work_lam.release();
   h->work_r.release();
@@ -1025,8 +1047,29 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
     }
   }
   const int64_t stride = mo;
-  std::vector<Cx> mats((size_t)stride * n_rows);
-  for (size_t k = 0; k < g0.size(); ++k) full(g0[k], mats.data() + ops[k].mat_off);
+  std::vector<uint64_t> xs, zs;
+  std::vector<double> cs;
+  for (size_t gi = 0; gi < G.xs.size(); ++gi)
+    for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
+      xs.push_back(G.xs[gi]);
+      zs.push_back(G.z[t]);
+      cs.push_back(G.c[2 * t]);
+      cs.push_back(G.c[2 * t + 1]);
+    }
+  // one upload from page-locked staging: [ops | gens | mats | x | z | c]; the per-row matrices are
+  // written straight into it
+  auto al = [](size_t v) { return (v + 63) & ~size_t(63); };
+  const size_t b_ops = ops.size() * sizeof(BatchOp), b_gen = gens.size() * 16,
+               b_mat = (size_t)stride * (size_t)n_rows * 16, b_x = xs.size() * 8, b_c = cs.size() * 8;
+  const size_t o_gen = al(b_ops), o_mat = o_gen + al(b_gen), o_x = o_mat + al(b_mat), o_z = o_x + al(b_x),
+               o_c = o_z + al(b_x), total = o_c + al(b_c) + 64;
+  if (!h->d_terms.ensure(total)) return fail(SV_E_OOM, "batch buffers");
+  const size_t nout = (size_t)n_rows * (1 + (size_t)std::max(n_params, 0));
+  if (!h->d_out.ensure(nout * 8 + 8)) return fail(SV_E_OOM, "batch outputs");
+  if (!h->pin_in.ensure(total) || !h->pin_out.ensure(nout * 8 + 8)) return fail(SV_E_OOM, "batch host staging");
+  char* hs = static_cast<char*>(h->pin_in.p);
+  Cx* mats = reinterpret_cast<Cx*>(hs + o_mat);
+  for (size_t k = 0; k < g0.size(); ++k) full(g0[k], mats + ops[k].mat_off);
   std::vector<int64_t> pgates;  // the row-dependent (parametrised) gates
   for (size_t k = 0; k < g0.size(); ++k)
     if (g0[k].param >= 0) pgates.push_back((int64_t)k);
@@ -1039,8 +1082,8 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
       BoundGate b;
       std::string err;
       for (int32_t r = 1 + t; r < n_rows; r += nt) {
-        Cx* mr = mats.data() + (size_t)r * stride;
-        std::memcpy(mr, mats.data(), (size_t)stride * sizeof(Cx));  // row-independent gates
+        Cx* mr = mats + (size_t)r * stride;
+        std::memcpy(mr, mats, (size_t)stride * sizeof(Cx));  // row-independent gates
         const double* pr = params ? params + (size_t)r * n_params : nullptr;
         for (int64_t k : pgates) {
           const int grc = bind_gate(h->n, &gates[k], pr, n_params, true, &b, &err);
@@ -1061,29 +1104,8 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
       if (row_rc[(size_t)r] != SV_OK)
         return fail(row_rc[(size_t)r], std::string("row ") + std::to_string(r) + ": " + row_err[(size_t)r]);
   }
-  std::vector<uint64_t> xs, zs;
-  std::vector<double> cs;
-  for (size_t gi = 0; gi < G.xs.size(); ++gi)
-    for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
-      xs.push_back(G.xs[gi]);
-      zs.push_back(G.z[t]);
-      cs.push_back(G.c[2 * t]);
-      cs.push_back(G.c[2 * t + 1]);
-    }
-  // one upload: [ops | gens | mats | x | z | c]
-  auto al = [](size_t v) { return (v + 63) & ~size_t(63); };
-  const size_t b_ops = ops.size() * sizeof(BatchOp), b_gen = gens.size() * 16, b_mat = mats.size() * 16,
-               b_x = xs.size() * 8, b_c = cs.size() * 8;
-  const size_t o_gen = al(b_ops), o_mat = o_gen + al(b_gen), o_x = o_mat + al(b_mat), o_z = o_x + al(b_x),
-               o_c = o_z + al(b_x), total = o_c + al(b_c) + 64;
-  if (!h->d_terms.ensure(total)) return fail(SV_E_OOM, "batch buffers");
-  const size_t nout = (size_t)n_rows * (1 + (size_t)std::max(n_params, 0));
-  if (!h->d_out.ensure(nout * 8 + 8)) return fail(SV_E_OOM, "batch outputs");
-  h->h_stage.assign(total, 0);
-  char* hs = h->h_stage.data();
   std::memcpy(hs, ops.data(), b_ops);
   std::memcpy(hs + o_gen, gens.data(), b_gen);
-  std::memcpy(hs + o_mat, mats.data(), b_mat);
   std::memcpy(hs + o_x, xs.data(), b_x);
   std::memcpy(hs + o_z, zs.data(), b_x);
   std::memcpy(hs + o_c, cs.data(), b_c);
@@ -1108,8 +1130,8 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
   e = launch_batch_grad(h->psi, h->n_local, a, n_rows, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "batch launch");
   h->stats.kernel_launches += 1;
-  std::vector<double> hv(nout);
-  e = cudaMemcpyAsync(hv.data(), dout, nout * 8, cudaMemcpyDeviceToHost, h->stream);
+  const double* hv = static_cast<const double*>(h->pin_out.p);
+  e = cudaMemcpyAsync(h->pin_out.p, dout, nout * 8, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "batch readback");
   for (int32_t r = 0; r < n_rows; ++r) out_values[r] = hv[(size_t)r];

@@ -17,6 +17,14 @@ struct DevBuf {
   void release();
 };
 
+// Page-locked host staging (async H2D / D2H at full PCIe rate); grow-only like DevBuf.
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool ensure(size_t bytes);
+  void release();
+};
+
 struct ShardState;  // shard.cpp
 
 // A built plan and its device copy ([ops | stages | mats | rops], one upload). Plans are cached
@@ -49,6 +57,7 @@ struct sv_state_s {
   sv::DevBuf promo;
   sv::DevBuf d_ops, d_mats, d_terms, d_partials, d_out;
   std::vector<char> h_stage;
+  sv::PinnedBuf pin_in, pin_out;  // batch-mode staging
   std::vector<sv::CachedPlan*> plan_cache;  // owned, LRU (small)
   uint64_t plan_clock = 0;
   sv::PlanOptions opts;
