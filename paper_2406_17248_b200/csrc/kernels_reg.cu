@@ -559,12 +559,6 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ double lds64(const double* p) {
-  double r;
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(r) : "r"(a));
-  return r;
-}
 
 // A operand of a dense stage: this warp's variant matrix (global, L2-resident), 8 entries per lane.
 __device__ __forceinline__ void dense_load_a(const StageDesc& S, const double2* __restrict__ gmats2, uint64_t base,
