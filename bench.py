@@ -174,21 +174,35 @@ def run_grad_config(args, P, torch):
     if args.config == "C1":
         rows = np.random.default_rng(1).uniform(-np.pi, np.pi, (4096, len(w.params)))
 
-    def step():
-        if rows is not None:
-            return P.sv_expectation_with_grad_batch(sv.h, ga, rows, pa)
-        return P.sv_expectation_with_grad(sv.h, ga, w.params, pa)
+    # an optimiser loop: the parameters change every step (as in VQE / QAOA training), so every
+    # evaluation binds and plans its circuit afresh (no plan-cache hits); C1's rows are new too
+    prng = np.random.default_rng(7)
 
-    for _ in range(args.warmup):
-        step()
+    def step(i, moving=True):
+        if rows is not None:
+            r = rows + (1e-3 * i if moving else 0.0)
+            return P.sv_expectation_with_grad_batch(sv.h, ga, r, pa)
+        p = w.params + (1e-3 * prng.standard_normal(len(w.params)) if moving else 0.0)
+        return P.sv_expectation_with_grad(sv.h, ga, p, pa)
+
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize()
     P.sv_reset_stats(sv.h)
     with ClockSampler(0) as clk:
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            out = step()
+        for i in range(args.steps):
+            out = step(args.warmup + i)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / args.steps
+    # the same evaluation with unchanged parameters (plans reused from the handle's cache)
+    step(0, moving=False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(0, moving=False)
+    torch.cuda.synchronize()
+    dt_fixed = (time.perf_counter() - t0) / args.steps
     st = P.sv_get_stats(sv.h)
     evals = rows.shape[0] if rows is not None else 1
     line = {"metric": "expectation + adjoint-gradient evaluations per second", "value": evals / dt,
@@ -196,7 +210,9 @@ def run_grad_config(args, P, torch):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic", "config": {"workload": args.config, "n_qubits": w.n, "gates": len(w.gates),
                                             "params": len(w.params), "ham_terms": len(w.ham),
-                                            "rows_per_step": evals},
+                                            "rows_per_step": evals,
+                                            "param_updates": "parameters changed every step (optimiser loop)"},
+            "fixed_params_value": evals / dt_fixed,
             "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
             "e2e": {"value": evals / dt, "unit": "grad evals/s (host call incl.)",
                     "h2d_bytes_per_step": int(ga.nbytes + pa.nbytes + (rows.nbytes if rows is not None else w.params.nbytes)),
@@ -416,11 +432,13 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         reps = 2
-        for _ in range(reps):
-            Eg, gg = P.sv_expectation_with_grad(sv.h, gag, wg.params, pag)
+        prng = np.random.default_rng(11)
+        for _ in range(reps):  # parameters change every evaluation (optimiser loop)
+            Eg, gg = P.sv_expectation_with_grad(sv.h, gag, wg.params + 1e-3 * prng.standard_normal(len(wg.params)), pag)
         dtg = (time.perf_counter() - t0) / reps
         grad = {"workload": "C4g: 30q HEA 2 layers RY/RZ + CNOT ladder, 120 params, 50-term JW H",
-                "grad_evals_per_s": 1.0 / dtg, "ms_per_eval": 1e3 * dtg, "E": Eg}
+                "grad_evals_per_s": 1.0 / dtg, "ms_per_eval": 1e3 * dtg, "E": Eg,
+                "param_updates": "parameters changed every evaluation"}
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1 and shards == 1:

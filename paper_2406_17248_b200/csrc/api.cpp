@@ -5,6 +5,7 @@
 // in shard.cpp.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <thread>
@@ -63,10 +64,30 @@ void PinnedBuf::release() {
   cap = 0;
 }
 
+bool DevBuf::ensure_async(size_t bytes, cudaStream_t s) {
+  if (bytes <= cap) return true;
+  if (p) {
+    if (async) cudaFreeAsync(p, s);
+    else cudaFree(p);
+  }
+  p = nullptr;
+  cap = 0;
+  const size_t want = bytes < 65536 ? 65536 : bytes + bytes / 2;
+  if (cudaMallocAsync(&p, want, s) != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return false;
+  }
+  async = true;
+  cap = want;
+  return true;
+}
+
 void DevBuf::release() {
   if (p) cudaFree(p);
   p = nullptr;
   cap = 0;
+  async = false;
 }
 
 int check_handle(sv_state_s* h) {
@@ -100,46 +121,74 @@ void release_plan_cache(sv_state_s* h) {
   h->plan_cache.clear();
 }
 
-int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, const CachedPlan** out) {
-  const int kCacheEntries = 8;
+static uint64_t plan_key(const sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse) {
   uint64_t key = 1469598103934665603ull;
   key = fnv1a(gates.data(), gates.size() * sizeof(BoundGate), key);
   const int meta[9] = {h->n_local, reverse ? 1 : 0, h->opts.tile_qubits, h->opts.low_qubits, h->opts.fusion ? 1 : 0,
                        h->opts.kernel, h->opts.dense, h->opts.da_cost, (int)gates.size()};
-  key = fnv1a(meta, sizeof(meta), key);
+  return fnv1a(meta, sizeof(meta), key);
+}
+
+static constexpr int kCacheEntries = 8;
+
+// A cache slot for a new plan: a fresh entry, or the least recently used one.
+static CachedPlan* plan_slot(sv_state_s* h) {
+  CachedPlan* c = nullptr;
+  if ((int)h->plan_cache.size() < kCacheEntries) {
+    c = new CachedPlan();
+    h->plan_cache.push_back(c);
+    return c;
+  }
+  for (CachedPlan* x : h->plan_cache)
+    if (!c || x->stamp < c->stamp) c = x;
+  return c;
+}
+
+static int upload_plan(sv_state_s* h, CachedPlan* c, uint64_t key, const CachedPlan** out);
+
+int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, const CachedPlan** out) {
+  const uint64_t key = plan_key(h, gates, reverse);
   for (CachedPlan* c : h->plan_cache)
     if (c->key == key) {
       c->stamp = ++h->plan_clock;
       *out = c;
       return SV_OK;
     }
-  CachedPlan* c = nullptr;
-  if ((int)h->plan_cache.size() < kCacheEntries) {
-    c = new CachedPlan();
-    h->plan_cache.push_back(c);
-  } else {
-    c = *std::min_element(h->plan_cache.begin(), h->plan_cache.end(),
-                          [](const CachedPlan* x, const CachedPlan* y) { return x->stamp < y->stamp; });
-  }
+  CachedPlan* c = plan_slot(h);
   c->key = 0;
   build_plan(gates, h->n_local, h->opts, reverse, &c->plan);
+  return upload_plan(h, c, key, out);
+}
+
+static int upload_plan(sv_state_s* h, CachedPlan* c, uint64_t key, const CachedPlan** out) {
   // one buffer: [ops | stages | mats | rops], each section 64-byte aligned; one H2D copy
   const Plan& plan = c->plan;
   auto al = [](size_t x) { return (x + 63) & ~size_t(63); };
   const size_t ob = plan.ops.size() * sizeof(DevOp), sb = plan.stages.size() * sizeof(StageDesc),
                mb = plan.mats.size() * sizeof(double), rb = plan.rops.size() * sizeof(RegOp);
   const size_t so = al(ob), mo = so + al(sb), ro = mo + al(mb), total = ro + al(rb);
-  if (!c->buf.ensure(total + 64)) return fail(SV_E_OOM, "plan buffers");
-  h->h_stage.assign(total, 0);
-  std::memcpy(h->h_stage.data(), plan.ops.data(), ob);
-  std::memcpy(h->h_stage.data() + so, plan.stages.data(), sb);
-  std::memcpy(h->h_stage.data() + mo, plan.mats.data(), mb);
-  std::memcpy(h->h_stage.data() + ro, plan.rops.data(), rb);
+  if (!c->buf.ensure_async(total + 64, h->stream)) return fail(SV_E_OOM, "plan buffers");
+  // page-locked staging: the copy is truly asynchronous (a pageable source would hold the host
+  // until the stream reaches it); the previous upload from the same buffer must have completed
+  cudaError_t e = cudaSuccess;
+  if (h->plan_upload_done) {
+    e = cudaEventSynchronize(h->plan_upload_done);
+    if (e != cudaSuccess) return cuda_fail(h, e, "plan upload");
+  } else {
+    e = cudaEventCreateWithFlags(&h->plan_upload_done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(h, e, "plan upload event");
+  }
+  if (!h->pin_plan.ensure(total + 64)) return fail(SV_E_OOM, "plan staging");
+  char* hs = static_cast<char*>(h->pin_plan.p);
+  std::memcpy(hs, plan.ops.data(), ob);
+  std::memcpy(hs + so, plan.stages.data(), sb);
+  std::memcpy(hs + mo, plan.mats.data(), mb);
+  std::memcpy(hs + ro, plan.rops.data(), rb);
   c->so = so;
   c->mo = mo;
   c->ro = ro;
-  cudaError_t e = cudaSuccess;
-  if (total) e = cudaMemcpyAsync(c->buf.p, h->h_stage.data(), total, cudaMemcpyHostToDevice, h->stream);
+  if (total) e = cudaMemcpyAsync(c->buf.p, hs, total, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(h->plan_upload_done, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "plan upload");
   c->key = key;
   c->stamp = ++h->plan_clock;
@@ -545,6 +594,8 @@ sv_status sv_destroy(sv_handle h) {
   h->promo.release();
   h->pin_in.release();
   h->pin_out.release();
+  h->pin_plan.release();
+  if (h->plan_upload_done) cudaEventDestroy(h->plan_upload_done);
   h->work_psi.release();
   h->work_lam.release();
   h->work_r.release();

@@ -12,9 +12,11 @@
 // used here: the qubits on which either acts non-diagonally are disjoint from all qubits of the
 // other (operators block-diagonal on shared qubits commute). Controls act diagonally.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 #include "sv.h"
 #include "sv_internal.h"
@@ -53,6 +55,25 @@ struct PassGroup {
 // Swizzled 16-byte slot of tile index t (bank-conflict-free for 8 lanes spanning three tile
 // positions with distinct residues mod 3). XOR-linear: sw(a ^ b) = sw(a) ^ sw(b).
 uint32_t swz(uint32_t t) { return t ^ ((t >> 3 ^ t >> 6 ^ t >> 9 ^ t >> 12) & 7u); }
+
+// Runs f(0 .. n-1) on host threads (n independent work items; small n runs inline).
+template <class F>
+void parallel_for(int n, F f) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  static const int force1 = std::getenv("SV_PLAN_SERIAL") ? 1 : 0;
+  const int nt = force1 ? 1 : std::min(hw, n / 64);  // thread spawn costs ~ one small variant batch
+  if (nt <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      for (int i = t; i < n; i += nt) f(i);
+    });
+  for (int i = 0; i < n; i += nt) f(i);
+  for (std::thread& th : pool) th.join();
+}
 
 bool op_is_diag(const DevOp& o) { return o.type == OP_D1 || o.type == OP_D2; }
 
@@ -327,6 +348,83 @@ void dense_apply(Cx* u, const DevOp& o, const double* m, const int* reg_new, uin
 }
 
 
+// U <- op U for a whole 16 x 16 register-space matrix (row-major U[j * 16 + c]): the same
+// arithmetic as dense_apply column by column, with the control / variant decode done once.
+void dense_apply_cols(Cx* U, const DevOp& o, const double* m, const int* reg_new, uint32_t tbits, uint64_t obits) {
+  uint32_t cj = 0, cthr = 0;
+  for (int p = 0; p < 32; ++p)
+    if ((o.ctile >> p) & 1ull) {
+      if (reg_new[p] >= 0) cj |= 1u << reg_new[p];
+      else cthr |= 1u << p;
+    }
+  if ((cthr & tbits) != cthr) return;
+  if ((o.couter & obits) != o.couter) return;
+  auto bit_of = [&](int pos, int q, int j) -> uint32_t {
+    if (pos >= 0 && reg_new[pos] >= 0) return ((uint32_t)j >> reg_new[pos]) & 1u;
+    if (pos >= 0) return (tbits >> pos) & 1u;
+    return (uint32_t)((obits >> q) & 1ull);
+  };
+  auto cm = [](Cx a, Cx b) { return Cx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; };
+  auto ca = [](Cx a, Cx b) { return Cx{a.re + b.re, a.im + b.im}; };
+  const Cx* M = reinterpret_cast<const Cx*>(m);
+  switch (o.type) {
+    case OP_M1: case OP_AX1: {
+      const int r = reg_new[o.pa];
+      Cx mm[4];
+      if (o.type == OP_M1) { mm[0] = M[0]; mm[1] = M[1]; mm[2] = M[2]; mm[3] = M[3]; }
+      else { mm[0] = Cx{0, 0}; mm[1] = M[0]; mm[2] = M[1]; mm[3] = Cx{0, 0}; }
+      for (int j = 0; j < 16; ++j) {
+        if ((j >> r) & 1) continue;
+        if (((uint32_t)j & cj) != cj) continue;
+        Cx* a = U + j * 16;
+        Cx* b = U + (j | (1 << r)) * 16;
+        for (int c = 0; c < 16; ++c) {
+          const Cx x = a[c], y = b[c];
+          a[c] = ca(cm(mm[0], x), cm(mm[1], y));
+          b[c] = ca(cm(mm[2], x), cm(mm[3], y));
+        }
+      }
+      break;
+    }
+    case OP_M2: case OP_SWAP: {
+      const int ra = reg_new[o.pa], rb = reg_new[o.pb];
+      for (int j = 0; j < 16; ++j) {
+        if (((j >> ra) & 1) || ((j >> rb) & 1)) continue;
+        if (((uint32_t)j & cj) != cj) continue;
+        Cx* row[4] = {U + j * 16, U + (j | (1 << ra)) * 16, U + (j | (1 << rb)) * 16,
+                      U + (j | (1 << ra) | (1 << rb)) * 16};
+        for (int c = 0; c < 16; ++c) {
+          Cx x[4], y[4];
+          for (int k = 0; k < 4; ++k) x[k] = row[k][c];
+          if (o.type == OP_SWAP) { y[0] = x[0]; y[1] = x[2]; y[2] = x[1]; y[3] = x[3]; }
+          else
+            for (int rr = 0; rr < 4; ++rr) {
+              Cx acc{0, 0};
+              for (int k = 0; k < 4; ++k) acc = ca(acc, cm(M[rr * 4 + k], x[k]));
+              y[rr] = acc;
+            }
+          for (int k = 0; k < 4; ++k) row[k][c] = y[k];
+        }
+      }
+      break;
+    }
+    case OP_D1:
+      for (int j = 0; j < 16; ++j) {
+        if (((uint32_t)j & cj) != cj) continue;
+        const Cx f = M[bit_of(o.pa, o.qa, j)];
+        for (int c = 0; c < 16; ++c) U[j * 16 + c] = cm(f, U[j * 16 + c]);
+      }
+      break;
+    case OP_D2:
+      for (int j = 0; j < 16; ++j) {
+        if (((uint32_t)j & cj) != cj) continue;
+        const Cx f = M[bit_of(o.pa, o.qa, j) | (bit_of(o.pb, o.qb, j) << 1)];
+        for (int c = 0; c < 16; ++c) U[j * 16 + c] = cm(f, U[j * 16 + c]);
+      }
+      break;
+  }
+}
+
 // u <- (Pi_C (x) G) u in register space: the generator of a parametrised op restricted to the
 // control-satisfied subspace (zero elsewhere). G: op's generator (diagonal entries if gen_diag).
 void dense_gen_apply(Cx* u, const DevOp& o, const double* gm, const int* reg_new, uint32_t tbits, uint64_t obits) {
@@ -409,7 +507,8 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     if (!((regmask >> p) & 1u) && !((vt >> p) & 1u)) regmask |= 1u << p;
   if (__builtin_popcount(regmask) != 4) return false;
   const int m_tile = __builtin_popcount(vt), m_outer = __builtin_popcountll(vo);
-  if (std::getenv("SV_PLAN_DEBUG"))
+  static const bool plan_debug = std::getenv("SV_PLAN_DEBUG") != nullptr;
+  if (plan_debug)
     std::fprintf(stderr, "stage: ops %d cost %d m_tile %d m_outer %d\n", (int)sp->ops.size(), cost, m_tile, m_outer);
   if (adjoint) {
     // adjoint dense stage: per-warp R accumulators need warp-uniform variants (no outer bits);
@@ -471,28 +570,33 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
   std::vector<int> olist;
   for (int q = 0; q < 64; ++q)
     if ((vo >> q) & 1ull) olist.push_back(q);
-  // variant matrices U_v = G_n ... G_1 (register space), row stride kDenseStride
+  // variant matrices U_v = G_n ... G_1 (register space), row stride kDenseStride; the variants
+  // are independent, so they are generated on host threads (QAOA-like passes carry up to 64)
   const size_t off = plan->mats.size() - pd.mat_begin;
-  for (int v = 0; v < nvar; ++v) {
-    uint32_t tbits = 0;
-    for (int b = 0; b < m_tile; ++b)
-      if ((v >> b) & 1) tbits |= 1u << vlist[b];
-    uint64_t obits = 0;
-    for (int b = 0; b < m_outer; ++b)
-      if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
-    Cx U[256];
-    for (int c = 0; c < 16; ++c) {
-      Cx u[16];
-      for (int j = 0; j < 16; ++j) u[j] = Cx{j == c ? 1.0 : 0.0, 0.0};
-      for (const DevOp& o : sp->ops) dense_apply(u, o, plan->mats.data() + pd.mat_begin + o.mat_off, reg_new, tbits, obits);
-      for (int j = 0; j < 16; ++j) U[j * 16 + c] = u[j];
-    }
-    for (int j = 0; j < 16; ++j)
-      for (int c = 0; c < kDenseStride; ++c) {
-        const Cx e = c < 16 ? U[j * 16 + c] : Cx{0, 0};
-        plan->mats.push_back(e.re);
-        plan->mats.push_back(e.im);
-      }
+  const size_t vdoubles = 2 * 16 * (size_t)kDenseStride;
+  plan->mats.resize(plan->mats.size() + (size_t)nvar * vdoubles);
+  {
+    const double* opm = plan->mats.data() + pd.mat_begin;
+    double* dst = plan->mats.data() + pd.mat_begin + off;
+    parallel_for(nvar, [&](int v) {
+      uint32_t tbits = 0;
+      for (int b = 0; b < m_tile; ++b)
+        if ((v >> b) & 1) tbits |= 1u << vlist[b];
+      uint64_t obits = 0;
+      for (int b = 0; b < m_outer; ++b)
+        if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
+      Cx U[256];
+      for (int j = 0; j < 16; ++j)
+        for (int c = 0; c < 16; ++c) U[j * 16 + c] = Cx{j == c ? 1.0 : 0.0, 0.0};
+      for (const DevOp& o : sp->ops) dense_apply_cols(U, o, opm + o.mat_off, reg_new, tbits, obits);
+      double* d = dst + (size_t)v * vdoubles;
+      for (int j = 0; j < 16; ++j)
+        for (int c = 0; c < kDenseStride; ++c) {
+          const Cx e = c < 16 ? U[j * 16 + c] : Cx{0, 0};
+          *d++ = e.re;
+          *d++ = e.im;
+        }
+    });
   }
   StageDesc& S = sp->sd;
   std::memset(&S, 0, sizeof(S));
@@ -836,7 +940,14 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
     pd.op_end = (int)plan->ops.size();
     if (o.kernel == 1 && k - 3 >= 5) {
       pd.R = 3;
-      plan_pass_stages(plan, &pd, !reverse, o.dense != 0, n_local, o.da_cost);
+      {
+        static const bool tm = std::getenv("SV_PLAN_TIMING") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        plan_pass_stages(plan, &pd, !reverse, o.dense != 0, n_local, o.da_cost);
+        if (tm)
+          std::fprintf(stderr, "pass %zu stages %.3f ms\n", plan->passes.size(),
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      }
     } else {
       pd.R = 0;
       pd.seq_mats = (int32_t)(plan->mats.size() - pd.mat_begin);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sv.h"
@@ -13,7 +14,11 @@ namespace sv {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool async = false;  // allocated with cudaMallocAsync (stream-ordered, no device-wide sync)
   bool ensure(size_t bytes);
+  // Grow-only like ensure, but stream-ordered (cudaFreeAsync / cudaMallocAsync on `s`) with 1.5x
+  // headroom: replacing a plan buffer never stalls the device.
+  bool ensure_async(size_t bytes, cudaStream_t s);
   void release();
 };
 
@@ -58,6 +63,8 @@ struct sv_state_s {
   sv::DevBuf d_ops, d_mats, d_terms, d_partials, d_out;
   std::vector<char> h_stage;
   sv::PinnedBuf pin_in, pin_out;  // batch-mode staging
+  sv::PinnedBuf pin_plan;         // plan upload staging
+  cudaEvent_t plan_upload_done = nullptr;
   std::vector<sv::CachedPlan*> plan_cache;  // owned, LRU (small)
   uint64_t plan_clock = 0;
   sv::PlanOptions opts;
