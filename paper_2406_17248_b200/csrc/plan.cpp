@@ -12,6 +12,10 @@
 // used here: the qubits on which either acts non-diagonally are disjoint from all qubits of the
 // other (operators block-diagonal on shared qubits commute). Controls act diagonally.
 #include <algorithm>
+#include <mutex>
+#include <functional>
+#include <condition_variable>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -57,22 +61,81 @@ struct PassGroup {
 uint32_t swz(uint32_t t) { return t ^ ((t >> 3 ^ t >> 6 ^ t >> 9 ^ t >> 12) & 7u); }
 
 // Runs f(0 .. n-1) on host threads (n independent work items; small n runs inline).
+// Persistent host worker pool for independent planning work items (dense variant matrices):
+// workers sleep on a condition variable; a job hands out indices through an atomic counter and the
+// calling thread participates. Spawning threads per call cost more than the work it split.
+class PlanPool {
+ public:
+  static PlanPool& get() {
+    static PlanPool pool;
+    return pool;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  void run(int n, const std::function<void(int)>& f) {
+    if (workers_.empty() || n < 8) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    job_ = &f;
+    n_ = n;
+    next_.store(0);
+    active_ = (int)workers_.size();
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) f(i);
+    lk.lock();
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  PlanPool() {
+    static const bool serial = std::getenv("SV_PLAN_SERIAL") != nullptr;
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int nw = serial ? 0 : std::min(hw, 16) - 1;
+    for (int t = 0; t < nw; ++t) workers_.emplace_back([this] { loop(); });
+  }
+  ~PlanPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (std::thread& t : workers_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(m_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+      const std::function<void(int)>* f = job_;
+      const int n = n_;
+      lk.unlock();
+      if (f)
+        for (int i = next_.fetch_add(1); i < n; i = next_.fetch_add(1)) (*f)(i);
+      lk.lock();
+      if (--active_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  std::atomic<int> next_{0};
+};
+
 template <class F>
 void parallel_for(int n, F f) {
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  static const int force1 = std::getenv("SV_PLAN_SERIAL") ? 1 : 0;
-  const int nt = force1 ? 1 : std::min(hw, n / 64);  // thread spawn costs ~ one small variant batch
-  if (nt <= 1) {
-    for (int i = 0; i < n; ++i) f(i);
-    return;
-  }
-  std::vector<std::thread> pool;
-  for (int t = 1; t < nt; ++t)
-    pool.emplace_back([&, t] {
-      for (int i = t; i < n; i += nt) f(i);
-    });
-  for (int i = 0; i < n; i += nt) f(i);
-  for (std::thread& th : pool) th.join();
+  const std::function<void(int)> fn(f);
+  PlanPool::get().run(n, fn);
 }
 
 bool op_is_diag(const DevOp& o) { return o.type == OP_D1 || o.type == OP_D2; }
