@@ -422,7 +422,18 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
         if ((G.xs[gi] >> q) & 1ull) xt |= 1u << pos_of[q];
       pp.xtile[g] = xt;
       pp.tbeg[g] = (int)z_all.size() - pp.term_base;
-      for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
+      // terms ordered by the tile-position Z bits above the kernel's thread bits (k_pauli_tile sums
+      // runs of equal element-part masks once)
+      std::vector<int> ts;
+      for (int t = G.begin[gi]; t < G.end[gi]; ++t) ts.push_back(t);
+      auto zhi = [&](int t) {
+        uint32_t zt = 0;
+        for (int q = 0; q < nl; ++q)
+          if (((G.z[t] >> q) & 1ull) && ((T >> q) & 1ull)) zt |= 1u << pos_of[q];
+        return zt >> 9;
+      };
+      std::stable_sort(ts.begin(), ts.end(), [&](int x, int y) { return zhi(x) < zhi(y); });
+      for (int t : ts) {
         z_all.push_back(G.z[t]);
         c_all.push_back(G.c[2 * t]);
         c_all.push_back(G.c[2 * t + 1]);

@@ -538,21 +538,40 @@ __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __rest
           }
           continue;
         }
+        // the host sorts a group's terms by their element-part mask zh = zt >> tid bits: a run of
+        // equal zh is summed once (per-thread signs folded), then spread over the 8 elements
+        // with compile-time Walsh signs (one switch per run instead of per-element selects)
         double2 C[EPT];
 #pragma unroll
         for (int j = 0; j < EPT; ++j) C[j] = make_double2(0.0, 0.0);
+        double2 S = make_double2(0.0, 0.0);
+        uint32_t cur = s_zt[tb] >> kPauliTidBits;
+        auto flush = [&](uint32_t zh) {
+#define SV_SPREAD(H)                                                  \
+  case H:                                                             \
+    _Pragma("unroll") for (int j = 0; j < EPT; ++j) {                 \
+      if (__builtin_popcount(j & H) & 1) { C[j].x -= S.x; C[j].y -= S.y; } \
+      else { C[j].x += S.x; C[j].y += S.y; }                           \
+    }                                                                 \
+    break;
+          switch (zh & 7u) {
+            SV_SPREAD(0) SV_SPREAD(1) SV_SPREAD(2) SV_SPREAD(3) SV_SPREAD(4) SV_SPREAD(5) SV_SPREAD(6) SV_SPREAD(7)
+          }
+#undef SV_SPREAD
+        };
         for (int t = tb; t < te; ++t) {
           const uint32_t zt = s_zt[t];
-          double2 c = s_c[t];
-          if (__popc(tid & zt & (uint32_t)(kPauliThreads - 1)) & 1) c = make_double2(-c.x, -c.y);
-          const uint32_t wr = walsh16(zt >> kPauliTidBits);
-#pragma unroll
-          for (int j = 0; j < EPT; ++j) {
-            const bool neg = (wr >> j) & 1u;
-            C[j].x += neg ? -c.x : c.x;
-            C[j].y += neg ? -c.y : c.y;
+          const uint32_t zh = zt >> kPauliTidBits;
+          if (zh != cur) {
+            flush(cur);
+            S = make_double2(0.0, 0.0);
+            cur = zh;
           }
+          const double2 c = s_c[t];
+          if (__popc(tid & zt & (uint32_t)(kPauliThreads - 1)) & 1) { S.x -= c.x; S.y -= c.y; }
+          else { S.x += c.x; S.y += c.y; }
         }
+        flush(cur);
 #pragma unroll
         for (int j = 0; j < EPT; ++j) {
           const double2 w = cmul(C[j], amp(tp[(tid + (uint32_t)j * (uint32_t)kPauliThreads) ^ xt]));
