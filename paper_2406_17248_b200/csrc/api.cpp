@@ -293,7 +293,7 @@ static int run_plan_c64(sv_state_s* h, const CachedPlan& cp) {
     L.d_partials = nullptr;
     L.nmats = next_mat - pd.mat_begin;
     const int64_t ntiles = int64_t(1) << (h->n_local - pd.k);
-    L.grid = (int)std::min<int64_t>(ntiles, (int64_t)pauli_tile_grid(30, 12) * 3);  // SMs x 3
+    L.grid = (int)std::min<int64_t>(ntiles, (int64_t)device_sm_count() * 3);
     L.n_local = h->n_local;
     L.rank_bits = 0;
     cudaError_t e = launch_pass_c64(h->psi32, L, h->stream);

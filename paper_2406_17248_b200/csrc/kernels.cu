@@ -738,6 +738,8 @@ int num_sms() {
 
 }  // namespace
 
+int device_sm_count() { return num_sms(); }
+
 int pass_grid(int n_local, int k, bool dual) {
   const int64_t ntiles = 1ll << (n_local - k);
   const int64_t want = (int64_t)num_sms() * 2 * ((k <= 10) ? 2 : 1);

@@ -1366,23 +1366,12 @@ cudaError_t launch_pass_c64(float* psi, const PassLaunch& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-static int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
 cudaError_t launch_widen(const float* a, double* b, int64_t n, cudaStream_t s) {
-  k_widen<<<sm_count() * 4, 256, 0, s>>>(reinterpret_cast<const float2*>(a), reinterpret_cast<double2*>(b), n);
+  k_widen<<<device_sm_count() * 4, 256, 0, s>>>(reinterpret_cast<const float2*>(a), reinterpret_cast<double2*>(b), n);
   return cudaGetLastError();
 }
 cudaError_t launch_narrow(const double* a, float* b, int64_t n, cudaStream_t s) {
-  k_narrow<<<sm_count() * 4, 256, 0, s>>>(reinterpret_cast<const double2*>(a), reinterpret_cast<float2*>(b), n);
+  k_narrow<<<device_sm_count() * 4, 256, 0, s>>>(reinterpret_cast<const double2*>(a), reinterpret_cast<float2*>(b), n);
   return cudaGetLastError();
 }
 

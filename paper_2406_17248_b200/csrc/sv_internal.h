@@ -211,6 +211,7 @@ cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStrea
 cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaStream_t s);
 // complex64 state (NEXT-3)
 bool c64_pass_ok(const PassDesc& pd);
+int device_sm_count();  // SMs of the current device (cached)
 cudaError_t launch_pass_c64(float* psi, const PassLaunch& L, cudaStream_t s);
 cudaError_t launch_widen(const float* a, double* b, int64_t n, cudaStream_t s);
 cudaError_t launch_narrow(const double* a, float* b, int64_t n, cudaStream_t s);
