@@ -939,11 +939,11 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
   if ((int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
   double2 ue[2][4];
   int it = 0;
+  if ((int64_t)blockIdx.x < a.ntiles) dense_load_a(s_st[0], gm2, tile_base(blockIdx.x), warp, lane, ue);
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
     const int cur = it & 1;
     const uint64_t base = tile_base(tile);
     const int64_t next = tile + gridDim.x;
-    dense_load_a(s_st[0], gm2, base, warp, lane, ue);
     if (next < a.ntiles) {
       issue_load(next, cur ^ 1);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -954,7 +954,10 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
     double2* tp = smem_tiles + (size_t)cur * N;
     for (int st = 0; st < a.nstages; ++st) {
       dense_apply_a(tp, s_st[st], ue, warp, lane);
+      // the next A operand: this tile's next stage, or the next tile's first stage (its L2
+      // latency then overlaps the barrier, the store and the next tile's wait)
       if (st + 1 < a.nstages) dense_load_a(s_st[st + 1], gm2, base, warp, lane, ue);
+      else if (next < a.ntiles) dense_load_a(s_st[0], gm2, tile_base(next), warp, lane, ue);
       __syncthreads();
     }
     {
