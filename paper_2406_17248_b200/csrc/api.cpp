@@ -4,6 +4,7 @@
 // (plan.cpp), uploads plan data and launches. Sharding (sv_create_sharded / virtual shards) lives
 // in shard.cpp.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -456,10 +457,21 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
   }
   const size_t zb = (z_all.size() * 8 + 15) & ~size_t(15), cb = c_all.size() * 8;
   if (!h->d_terms.ensure(zb + cb + 16)) return fail(SV_E_OOM, "term buffers");
-  h->h_stage.assign(zb + cb + 16, 0);
-  std::memcpy(h->h_stage.data(), z_all.data(), z_all.size() * 8);
-  std::memcpy(h->h_stage.data() + zb, c_all.data(), cb);
-  cudaError_t e = cudaMemcpyAsync(h->d_terms.p, h->h_stage.data(), zb + cb, cudaMemcpyHostToDevice, h->stream);
+  // page-locked staging: the upload does not hold the host until the stream drains (the gradient
+  // plans its reverse sweep meanwhile); the previous upload from this buffer must be complete
+  cudaError_t e = cudaSuccess;
+  if (h->terms_upload_done) {
+    e = cudaEventSynchronize(h->terms_upload_done);
+  } else {
+    e = cudaEventCreateWithFlags(&h->terms_upload_done, cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_fail(h, e, "term upload");
+  if (!h->pin_terms.ensure(zb + cb + 16)) return fail(SV_E_OOM, "term staging");
+  char* hs = static_cast<char*>(h->pin_terms.p);
+  std::memcpy(hs, z_all.data(), z_all.size() * 8);
+  std::memcpy(hs + zb, c_all.data(), cb);
+  e = cudaMemcpyAsync(h->d_terms.p, hs, zb + cb, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(h->terms_upload_done, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "term upload");
   const uint64_t* dz = static_cast<const uint64_t*>(h->d_terms.p);
   const double* dc = reinterpret_cast<const double*>(static_cast<const char*>(h->d_terms.p) + zb);
@@ -606,7 +618,10 @@ sv_status sv_destroy(sv_handle h) {
   h->pin_in.release();
   h->pin_out.release();
   h->pin_plan.release();
+  h->pin_terms.release();
+  h->pin_e.release();
   if (h->plan_upload_done) cudaEventDestroy(h->plan_upload_done);
+  if (h->terms_upload_done) cudaEventDestroy(h->terms_upload_done);
   h->work_psi.release();
   h->work_lam.release();
   h->work_r.release();
@@ -866,11 +881,18 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   if (e != cudaSuccess) return cuda_fail(h, e, "copy psi0");
   h->stats.algorithmic_bytes += 2.0 * (double)bytes;
   // 1. forward
+  static const bool tmg = std::getenv("SV_PLAN_TIMING") != nullptr;
+  const auto tg0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (tmg) std::fprintf(stderr, "grad %s at %.3f ms\n", what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count());
+  };
   const CachedPlan* fwdp = nullptr;
   rc = get_plan(h, bg, false, &fwdp);
   if (rc) return rc;
+  lap("fwd plan");
   rc = run_plan(h, *fwdp, psi, nullptr, nullptr, 0, nullptr, nullptr);
   if (rc) return rc;
+  lap("fwd launched");
   h->stats.gates_applied += (int64_t)bg.size();
   // 2. lambda = H psi, E
   double E = 0.0;
@@ -886,20 +908,26 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
     if (rc) return rc;
     e = launch_reduce_slots(static_cast<double*>(h->d_partials.p), nslots, pgrid, static_cast<double*>(h->d_out.p),
                             h->stream);
-    std::vector<double> ev((size_t)nslots);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(ev.data(), h->d_out.p, (size_t)nslots * 8, cudaMemcpyDeviceToHost, h->stream);
+    // page-locked destination: the copy stays asynchronous (a pageable one would hold the host
+    // until the forward passes finish, serialising the reverse plan behind them)
+    if (!h->pin_e.ensure((size_t)nslots * 8 + 8)) return fail(SV_E_OOM, "energy staging");
+    const double* ev = static_cast<const double*>(h->pin_e.p);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h->pin_e.p, h->d_out.p, (size_t)nslots * 8, cudaMemcpyDeviceToHost, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "energy");
     h->stats.kernel_launches += 1;
     // (the copy completes at the synchronisation inside run_reverse)
     std::vector<double> d;
     const CachedPlan* revp = nullptr;
+    lap("lambda launched");
     rc = get_plan(h, bg, true, &revp);
     if (rc) return rc;
+    lap("rev plan");
     rc = run_reverse(h, *revp, psi, lam, &d);
     if (rc) return rc;
+    lap("reverse done");
     e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "energy");
-    for (double v : ev) E += v;
+    for (int i = 0; i < nslots; ++i) E += ev[i];
     *out_value = E;
     for (int32_t p = 0; p < n_params; ++p) out_grad[p] = 0.0;
     for (size_t sl = 0; sl < d.size(); ++sl) out_grad[revp->plan.slot_param[sl]] += revp->plan.slot_coeff[sl] * 2.0 * d[sl];

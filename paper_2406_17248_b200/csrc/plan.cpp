@@ -860,6 +860,11 @@ int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual) {
 }
 
 void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOptions& o, bool reverse, Plan* plan) {
+  static const bool tmg = std::getenv("SV_PLAN_TIMING") != nullptr;
+  const auto tb0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (tmg) std::fprintf(stderr, "build_plan %s at %.3f ms\n", what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb0).count());
+  };
   const int k = choose_tile_qubits(n_local, o, reverse);
   const int L = std::min(o.low_qubits, k);
   const uint64_t lowmask = (L >= 64) ? ~0ull : ((1ull << L) - 1);
@@ -920,6 +925,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
     pending.swap(skipped);
   }
 
+  lap("grouped");
   // ---- 2. emit passes (forward order, or reversed with daggered ops for the adjoint sweep) ----
   plan->passes.clear();
   plan->reverse = reverse;
@@ -1021,6 +1027,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
     }
     plan->passes.push_back(pd);
   }
+  lap("emitted");
   // compact register-kernel ops
   plan->rops.assign(plan->ops.size(), RegOp{});
   for (const PassDesc& pd : plan->passes) {

@@ -65,6 +65,9 @@ struct sv_state_s {
   sv::PinnedBuf pin_in, pin_out;  // batch-mode staging
   sv::PinnedBuf pin_plan;         // plan upload staging
   cudaEvent_t plan_upload_done = nullptr;
+  sv::PinnedBuf pin_terms;        // Pauli term upload staging
+  sv::PinnedBuf pin_e;            // energy partials read-back (gradient)
+  cudaEvent_t terms_upload_done = nullptr;
   std::vector<sv::CachedPlan*> plan_cache;  // owned, LRU (small)
   uint64_t plan_clock = 0;
   sv::PlanOptions opts;
