@@ -639,6 +639,9 @@ sv_status sv_destroy(sv_handle h) {
 
 sv_status sv_set_stream(sv_handle h, void* stream) {
   if (!h) return fail(SV_E_ARG, "null handle");
+  // work already queued on the previous stream must finish before buffers it uses can be replaced
+  // stream-ordered on the new one
+  if (h->stream) cudaStreamSynchronize(h->stream);
   h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
   return SV_OK;
 }
