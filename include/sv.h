@@ -168,7 +168,8 @@ sv_status sv_create_c64(int32_t n_qubits, sv_handle* out);
 sv_status sv_destroy(sv_handle h);
 
 /* Use this CUDA stream (a cudaStream_t passed as void*) for all subsequent work; NULL = the
- * handle's own stream. The caller keeps the stream alive while the handle uses it. */
+ * handle's own stream. Work already queued on the previous stream is waited for first. The caller
+ * keeps the stream alive while the handle uses it. */
 sv_status sv_set_stream(sv_handle h, void* cuda_stream);
 
 sv_status sv_set_option(sv_handle h, int32_t key, int64_t value);
