@@ -873,7 +873,8 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
         if (DUAL) lam[gi] = tl[sl];
       }
     }
-    __syncthreads();
+    // no barrier: every thread reloads (cp.async) exactly the slots it just stored from, and the
+    // last stage ended with one
   }
   if (DUAL) {
     for (int i = tid; i < a.n_da * nwarps * 512; i += nthr)
@@ -965,7 +966,8 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
 #pragma unroll
       for (int i = 0; i < 8; ++i) psi[bt | a.hsub[i]] = tp[swz_t ^ a.zsub[i]];
     }
-    __syncthreads();
+    // no barrier: every thread reloads (cp.async) exactly the slots it just stored from, and the
+    // last stage ended with one
   }
 }
 
@@ -1191,7 +1193,8 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_c64(float2* __restric
 #pragma unroll
       for (int i = 0; i < 8; ++i) psi[bt | a.hsub[i]] = tp[swz_t ^ a.zsub[i]];
     }
-    __syncthreads();
+    // no barrier: every thread reloads (cp.async) exactly the slots it just stored from, and the
+    // last stage ended with one
   }
 }
 
