@@ -311,3 +311,28 @@ def test_determinism(P):
     b = sv.expectation_with_grad(w.gates, w.params, w.ham)
     sv.close()
     assert a[0] == b[0] and np.array_equal(a[1], b[1])
+
+
+def test_user_streams(P):
+    """Work on caller-provided CUDA streams (switched between calls, and back to the handle's own)
+    gives the same results as the default stream (sv_set_stream, include/sv.h)."""
+    import torch
+    n = 14
+    w = W.random_complex(n, 5, seed=77, n_params=3, extra_kinds=("PS", "MAT2"))
+    ham = W.jw_hamiltonian(n, 12, seed=3)
+    ref_psi = oracle.apply_circuit(n, w.gates, w.params)
+    E0, g0 = oracle.adjoint_grad(n, w.gates, w.params, ham)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    sv = P.StateVector(n)
+    P.sv_set_stream(sv.h, s1.cuda_stream)
+    sv.apply_circuit(w.gates, w.params)
+    P.sv_set_stream(sv.h, s2.cuda_stream)
+    assert np.max(np.abs(sv.get_state() - ref_psi)) <= AMP_TOL
+    sv.reset()
+    E, g = sv.expectation_with_grad(w.gates, w.params, ham)
+    P.sv_set_stream(sv.h, None)
+    E2, g2 = sv.expectation_with_grad(w.gates, w.params, ham)
+    sv.close()
+    assert abs(E - E0) < E_TOL and abs(E2 - E0) < E_TOL
+    np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
+    assert np.array_equal(g, g2)
