@@ -39,7 +39,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_TFLOPS = 36.9  # measured FP64 tensor (DMMA) peak = DMMA+DFMA mixed peak on this pool's B200
 # dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
 # --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
-TRAFFIC_PER_LAUNCH = {"C4": (17.182704 + 17.548224) * 1e9}  # profiles/r01_ncu_pass30_full.txt (k_pass_dense)
+TRAFFIC_PER_LAUNCH = {"C4": (17.181665 + 17.543235) * 1e9}  # profiles/r01_ncu_pass30_full.txt (k_pass_dense)
 TRAFFIC_PER_LAUNCH_C64 = None  # complex64 pass: not captured yet
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
