@@ -37,10 +37,11 @@ import workloads as W  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_TFLOPS = 36.9  # measured FP64 tensor (DMMA) peak = DMMA+DFMA mixed peak on this pool's B200
+TF32_SPLIT_PEAK_TFLOPS = 277.3 / 3  # measured mma.sync TF32 peak / 3 products (complex64 dense stages)
 # dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
 # --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
 TRAFFIC_PER_LAUNCH = {"C4": (17.181665 + 17.543235) * 1e9}  # profiles/r01_ncu_pass30_full.txt (k_pass_dense)
-TRAFFIC_PER_LAUNCH_C64 = None  # complex64 pass: not captured yet
+TRAFFIC_PER_LAUNCH_C64 = (8.614921 + 8.540025) * 1e9  # profiles/r01_ncu_c64_pass30_full.txt (k_pass_c64)
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
 
@@ -381,15 +382,21 @@ def main():
         plan = P.sv_plan_info(n, ga, w.params)
         fma_per_amp = sum(p["fma_per_amp"] for p in plan)
         fp64_flops = 2.0 * fma_per_amp * amps  # algorithmic FP64 work of the executed plan
+        c64 = args.precision == "c64"
+        # complex64: the dense stages run TF32 MMAs with a 3-term split, so the peak for the
+        # algorithmic (complex matrix-vector) flops is the measured TF32 mma.sync rate / 3
+        peak = TF32_SPLIT_PEAK_TFLOPS if c64 else FP64_PEAK_TFLOPS
         roof = {
             "bound": "tensor",
-            "kernel": ("k_pass_c64 (complex64 tiles widened to FP64 for DMMA dense stages + register stages)"
-                       if args.precision == "c64" else
+            "kernel": ("k_pass_c64 (complex64 tiles; dense stages on TF32 tensor cores, 3-term split; register stages)"
+                       if c64 else
                        "k_pass_dense / k_pass_reg<3,false> (fused forward tile passes: FP64 DMMA dense stages + register stages)"),
-            "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
-            "peak_source": "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
-                           "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)",
-            "unit": "TFLOP/s", "frac": fp64_flops / passes / (pass_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+            "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": peak,
+            "peak_source": ("measured legacy mma.sync TF32 277 TF (tools/microbench/mma_legacy.cu, "
+                            "profiles/r01_mma_legacy_microbench.jsonl) / 3 for the 3-term split" if c64 else
+                            "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
+                            "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)"),
+            "unit": "TFLOP/s", "frac": fp64_flops / passes / (pass_ms / 1e3) / 1e12 / peak,
             "traffic": TRAFFIC_PER_LAUNCH.get(args.config) if args.precision == "c128" else TRAFFIC_PER_LAUNCH_C64,
             "algorithmic_flops_per_launch": fp64_flops / passes, "avg_launch_ms": pass_ms,
             "hbm": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src,
