@@ -985,6 +985,8 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 
+__constant__ uint32_t kPerm24[24] = {228, 180, 216, 120, 156, 108, 225, 177, 201, 57, 141, 45, 210, 114, 198, 54, 78, 30, 147, 99, 135, 39, 75, 27};  // plan.cpp make_dense order
+
 // ---- complex64 dense stage on TF32 tensor cores with a 3-term split ("3xTF32") ----
 // Y = [[Ur, -Ui], [Ui, Ur]] [Xr; Xi] as mma.sync m16n8k8 (TF32 in, FP32 accumulate): per warp
 // 2 M-tiles (Re / Im out) x 2 N-tiles (its 16 vectors) x 4 K-steps. Every FP32 operand v is split
@@ -1027,21 +1029,24 @@ __device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S,
   // slot parts (swz is XOR-linear): vector n = 8 nt + col (col bits -> thrpos[0..2], nt -> thrpos[3]),
   // register index r (bit i -> regpos[i])
   auto sp = [&](int pos) { return swz8(1u << pos); };
+  // the warp's four vector positions in the host-chosen order (StageDesc::c64_perm)
+  const uint32_t pc = kPerm24[S.c64_perm];
+  const int X[4] = {S.thrpos[pc & 3], S.thrpos[(pc >> 2) & 3], S.thrpos[(pc >> 4) & 3], S.thrpos[(pc >> 6) & 3]};
   uint32_t wsw = 0;
   for (int b = 0; b < 3; ++b)
     if (((warp >> b) & 1) && S.thrpos[4 + b] >= 0) wsw ^= sp(S.thrpos[4 + b]);
   uint32_t bB = wsw, bD = wsw;
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
-    if ((g >> b) & 1) bB ^= sp(S.thrpos[b]);   // B: n col = g
+    if ((g >> b) & 1) bB ^= sp(X[b]);   // B: n col = g
     if ((g >> b) & 1) bD ^= sp(S.regpos[b]);   // D: out amp o = g (+8)
   }
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
     if ((t >> b) & 1) bB ^= sp(S.regpos[b]);      // B: in amp r = t (+4, +8)
-    if ((t >> b) & 1) bD ^= sp(S.thrpos[b + 1]);  // D: n col = 2 t (+1)
+    if ((t >> b) & 1) bD ^= sp(X[b + 1]);  // D: n col = 2 t (+1)
   }
-  const uint32_t sN = sp(S.thrpos[3]), sR2 = sp(S.regpos[2]), sR3 = sp(S.regpos[3]), sC0 = sp(S.thrpos[0]);
+  const uint32_t sN = sp(X[3]), sR2 = sp(S.regpos[2]), sR3 = sp(S.regpos[3]), sC0 = sp(X[0]);
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     // B fragments: in amps r = t + 4 c + 8 kh of vector (8 nt + g): Re for K-steps 0-1, Im for 2-3

@@ -692,6 +692,29 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     for (int kt = 0; kt < 4; ++kt)
       S.off_r[mt * 4 + kt] = (uint16_t)swz((mt ? p3 : 0u) | ((kt & 1) ? bc2 : 0u) | ((kt & 2) ? n0 : 0u));
   S.da_index = da_index;
+  {
+    // complex64 tiles (8-byte slots, 4-bit XOR fold: position p lands in bank class bit p mod 4):
+    // pick the order of the warp's four vector positions whose TF32 fragment lanes (B: three
+    // vector bits + register bits 0, 1; D: register bits 0..2 + vector bits 1, 2) spread over
+    // the most bank classes
+    static const int perms[24][4] = {{0,1,2,3},{0,1,3,2},{0,2,1,3},{0,2,3,1},{0,3,1,2},{0,3,2,1},
+                                     {1,0,2,3},{1,0,3,2},{1,2,0,3},{1,2,3,0},{1,3,0,2},{1,3,2,0},
+                                     {2,0,1,3},{2,0,3,1},{2,1,0,3},{2,1,3,0},{2,3,0,1},{2,3,1,0},
+                                     {3,0,1,2},{3,0,2,1},{3,1,0,2},{3,1,2,0},{3,2,0,1},{3,2,1,0}};
+    auto classes = [](std::initializer_list<int> pos) {
+      int m = 0;
+      for (int p : pos) m |= 1 << (p & 3);
+      return __builtin_popcount(m);
+    };
+    int best = 0, best_score = -1;
+    for (int pi = 0; pi < 24; ++pi) {
+      int X[4];
+      for (int b = 0; b < 4; ++b) X[b] = order[perms[pi][b]];
+      const int sc = classes({X[0], X[1], X[2], newreg[0], newreg[1]}) + classes({newreg[0], newreg[1], newreg[2], X[1], X[2]});
+      if (sc > best_score) { best_score = sc; best = pi; }
+    }
+    S.c64_perm = best;
+  }
   if (adjoint) {
     S.dense = 2;
     Plan::DAStage ds;

@@ -83,7 +83,8 @@ struct StageDesc {
   uint16_t lane_r[32];       // swz(lane part of the R-fragment load address)
   uint16_t off_r[8];         // swz(uniform part) for (mt, kt), index mt * 4 + kt
   int32_t da_index;          // first R accumulator slot of this adjoint dense stage in its pass (+ outer variant)
-  int32_t pad1;
+  int32_t c64_perm;          // complex64 dense stage: permutation (0..23) of thrpos[0..3] for the
+                             // TF32 fragment lanes, chosen on the host for few bank conflicts
 };
 static_assert(sizeof(StageDesc) == 312, "StageDesc layout");
 
