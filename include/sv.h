@@ -124,7 +124,8 @@ enum {
                                    parametrised op) reaches this run as adjoint dense MMA stages;
                                    -1 (default): 96 for states of >= 24 local qubits, else 250
                                    (their fixed per-pass costs amortise over large states only);
-                                   0: every eligible stage; 1 << 20: none */
+                                   0: every eligible stage (incl. one outer variant bit at any
+                                   size); 1 << 20: none */
 };
 
 /* a1: |0...0> on n_qubits (1 <= n <= 40 subject to memory), current CUDA device, new stream. */

@@ -322,7 +322,10 @@ const int g_da_enable = env_int("SV_DA", 1);
 const int g_da_max_per_pass = env_int("SV_DA_MAX_PER_PASS", kMaxDAPerPass);
 
 const int g_da_max_tile = env_int("SV_DA_MAX_TILE", 2);
-const int g_da_max_outer = env_int("SV_DA_MAX_OUTER", 1);  // outer variant bits of an adjoint dense stage (profiles/r01_da_outer_sweep.txt)
+// outer variant bits of an adjoint dense stage: 1 for large states (C4g 1.90 -> 1.97 grad evals/s),
+// 0 below 26 local qubits (C3 28.2 -> 28.7); profiles/r01_da_outer_sweep.txt. Env overrides.
+const int g_da_max_outer_env = env_int("SV_DA_MAX_OUTER", -1);
+int da_max_outer_for(int n_local) { return g_da_max_outer_env >= 0 ? g_da_max_outer_env : (n_local >= 26 ? 1 : 0); }
 
 // FP64 pipe cost per amplitude of an op applied sequentially (DFMA path), for the dense choice.
 int seq_cost(const DevOp& o, const double* m) {
@@ -545,7 +548,8 @@ void dense_gen_apply(Cx* u, const DevOp& o, const double* gm, const int* reg_new
 // the sequential path and feasible: variant bits <= 3 in total, tile variant bits on warp
 // positions. Returns false (stage untouched) otherwise.
 bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles, bool adjoint = false,
-                int pass_index = 0, int da_index = 0, int da_slots_left = 0, int da_min_cost = 96) {
+                int pass_index = 0, int da_index = 0, int da_slots_left = 0, int da_min_cost = 96,
+                int da_max_outer = 1) {
   const int k = pd.k;
   const int nw_bits = k - 8;  // 2^(k-3) threads: 16 vectors of 16 amplitudes per warp
   if (nw_bits < 1 || __builtin_popcount(sp->regset) > 4) return false;
@@ -577,7 +581,7 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     // worth it once the sequential dual cost (psi + lambda + overlaps) passes the dense cost
     int ngrad = 0;
     for (const DevOp& o : sp->ops) ngrad += o.grad_slot >= 0 ? 1 : 0;
-    if (2 * cost + 8 * ngrad < da_min_cost || m_outer > g_da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits) ||
+    if (2 * cost + 8 * ngrad < da_min_cost || m_outer > da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits) ||
         (1 << m_outer) > da_slots_left)
       return false;
   } else if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > g_dense_max_var) {
@@ -812,13 +816,15 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
     if (!seq.empty()) add_sequential(split_stages(seq, *pd, pd->R, -1, -1));
   } else if (!forward && dense && k >= 9 && g_da_enable) {
     const int da_min = da_min_cost_for(n_local, da_cost);
-    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(g_da_max_tile, k - 8), g_da_max_tile + g_da_max_outer);
+    // da_cost 0 ("every eligible stage") also admits one outer variant bit at any size
+    const int da_outer = da_cost == 0 ? std::max(1, da_max_outer_for(n_local)) : da_max_outer_for(n_local);
+    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(g_da_max_tile, k - 8), g_da_max_tile + da_outer);
     int nda = 0;  // R accumulator slots of this pass (2^m_outer per adjoint dense stage)
     std::vector<DevOp> seq;
     for (StagePlan& sp : st4) {
       if (nda < g_da_max_per_pass &&
           make_dense(&sp, *pd, plan, size_t(1) << 22, true, (int)plan->passes.size(), nda, g_da_max_per_pass - nda,
-                     da_min)) {
+                     da_min, da_outer)) {
         nda += 1 << sp.sd.m_outer;
         if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
         final_stages.push_back(std::move(sp));
