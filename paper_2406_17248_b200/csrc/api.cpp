@@ -1169,8 +1169,8 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
   {
     std::vector<int> row_rc((size_t)n_rows, SV_OK);
     std::vector<std::string> row_err((size_t)n_rows);
-    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-    const int nt = std::max(1, std::min(hw, (n_rows - 1 + 255) / 256));
+    // row chunks on the persistent host pool (no thread spawn per call)
+    const int nt = std::max(1, std::min(64, (n_rows - 1 + 63) / 64));
     auto work = [&](int t) {
       BoundGate b;
       std::string err;
@@ -1189,10 +1189,7 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
         }
       }
     };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
-    work(0);
-    for (std::thread& th : pool) th.join();
+    host_parallel_for(nt, work);
     for (int32_t r = 1; r < n_rows; ++r)
       if (row_rc[(size_t)r] != SV_OK)
         return fail(row_rc[(size_t)r], std::string("row ") + std::to_string(r) + ": " + row_err[(size_t)r]);

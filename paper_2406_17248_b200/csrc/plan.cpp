@@ -868,6 +868,8 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
 
 }  // namespace
 
+void host_parallel_for(int n, const std::function<void(int)>& f) { PlanPool::get().run(n, f); }
+
 int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual) {
   // forward passes: 2^11-amplitude tiles (256 threads, three double-buffered CTAs per SM);
   // adjoint (psi + lambda) passes: 2^10 (128 threads, two register-heavy CTAs per SM — measured

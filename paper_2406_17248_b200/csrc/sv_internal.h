@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -184,6 +185,8 @@ struct PlanOptions {
   int da_cost = -1;  // adjoint dense stage cost threshold (SV_OPT_ADJOINT_DENSE_COST; -1 auto by size)
 };
 int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual);
+// f(0 .. n-1) on the library's persistent host worker pool (plan.cpp)
+void host_parallel_for(int n, const std::function<void(int)>& f);
 void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOptions& o, bool reverse_for_adjoint,
                 Plan* plan);
 // FP64 FMAs per amplitude of pass i of a plan (dense stages 64, sequential ops by class).
