@@ -183,7 +183,16 @@ static int upload_plan(sv_state_s* h, CachedPlan* c, uint64_t key, const CachedP
   char* hs = static_cast<char*>(h->pin_plan.p);
   std::memcpy(hs, plan.ops.data(), ob);
   std::memcpy(hs + so, plan.stages.data(), sb);
-  std::memcpy(hs + mo, plan.mats.data(), mb);
+  {
+    // the variant matrices dominate (16 MB for C3): copied in parallel chunks on the host pool
+    constexpr size_t kChunk = size_t(1) << 20;
+    const int nch = (int)((mb + kChunk - 1) / kChunk);
+    const char* src = reinterpret_cast<const char*>(plan.mats.data());
+    host_parallel_for(nch, [&](int i) {
+      const size_t b = (size_t)i * kChunk;
+      std::memcpy(hs + mo + b, src + b, std::min(kChunk, mb - b));
+    });
+  }
   std::memcpy(hs + ro, plan.rops.data(), rb);
   c->so = so;
   c->mo = mo;

@@ -544,11 +544,76 @@ void dense_gen_apply(Cx* u, const DevOp& o, const double* gm, const int* reg_new
   for (int j = 0; j < 16; ++j) u[j] = out[j];
 }
 
+// One dense stage's variant matrices, deferred: U_v = G_n ... G_1 in register space for every
+// variant v (tile variant bits vlist, outer bits olist), written to plan->mats at dst (row stride
+// kDenseStride). The op matrices are read at opm + op.mat_off (pass-relative offsets).
+struct DenseJob {
+  std::vector<DevOp> ops;
+  size_t opm = 0, dst = 0;
+  int reg_new[32];
+  std::vector<int> vlist, olist;
+  int m_tile = 0, m_outer = 0;
+};
+
+void fill_dense_variants(Plan* plan, const std::vector<DenseJob>& jobs) {
+  std::vector<int> first(jobs.size() + 1, 0);
+  for (size_t j = 0; j < jobs.size(); ++j) first[j + 1] = first[j] + (1 << (jobs[j].m_tile + jobs[j].m_outer));
+  const size_t vdoubles = 2 * 16 * (size_t)kDenseStride;
+  parallel_for(first.back(), [&](int item) {
+    const size_t j = (size_t)(std::upper_bound(first.begin(), first.end(), item) - first.begin()) - 1;
+    const DenseJob& J = jobs[j];
+    const int v = item - first[j];
+    uint32_t tbits = 0;
+    for (int b = 0; b < J.m_tile; ++b)
+      if ((v >> b) & 1) tbits |= 1u << J.vlist[b];
+    uint64_t obits = 0;
+    for (int b = 0; b < J.m_outer; ++b)
+      if ((v >> (J.m_tile + b)) & 1) obits |= 1ull << J.olist[b];
+    const double* opm = plan->mats.data() + J.opm;
+    Cx U[256];
+    for (int r = 0; r < 16; ++r)
+      for (int c = 0; c < 16; ++c) U[r * 16 + c] = Cx{r == c ? 1.0 : 0.0, 0.0};
+    // runs of diagonal ops (QAOA phase layers) are collected into one diagonal and applied to the
+    // rows of U once, before the next non-diagonal op
+    Cx dg[16];
+    bool dg_pending = false;
+    auto flush = [&] {
+      if (!dg_pending) return;
+      for (int r = 0; r < 16; ++r)
+        for (int c = 0; c < 16; ++c) {
+          const Cx a = U[r * 16 + c];
+          U[r * 16 + c] = Cx{dg[r].re * a.re - dg[r].im * a.im, dg[r].re * a.im + dg[r].im * a.re};
+        }
+      dg_pending = false;
+    };
+    for (const DevOp& o : J.ops) {
+      if (op_is_diag(o)) {
+        if (!dg_pending) {
+          for (int r = 0; r < 16; ++r) dg[r] = Cx{1.0, 0.0};
+          dg_pending = true;
+        }
+        dense_apply(dg, o, opm + o.mat_off, J.reg_new, tbits, obits);
+      } else {
+        flush();
+        dense_apply_cols(U, o, opm + o.mat_off, J.reg_new, tbits, obits);
+      }
+    }
+    flush();
+    double* d = plan->mats.data() + J.dst + (size_t)v * vdoubles;
+    for (int r = 0; r < 16; ++r)
+      for (int c = 0; c < kDenseStride; ++c) {
+        const Cx e = c < 16 ? U[r * 16 + c] : Cx{0, 0};
+        *d++ = e.re;
+        *d++ = e.im;
+      }
+  });
+}
+
 // Folds a 4-register stage into dense variant matrices (appended to plan->mats) when cheaper than
 // the sequential path and feasible: variant bits <= 3 in total, tile variant bits on warp
 // positions. Returns false (stage untouched) otherwise.
-bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles, bool adjoint = false,
-                int pass_index = 0, int da_index = 0, int da_slots_left = 0, int da_min_cost = 96,
+bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles, std::vector<DenseJob>* jobs,
+                bool adjoint = false, int pass_index = 0, int da_index = 0, int da_slots_left = 0, int da_min_cost = 96,
                 int da_max_outer = 1) {
   const int k = pd.k;
   const int nw_bits = k - 8;  // 2^(k-3) threads: 16 vectors of 16 amplitudes per warp
@@ -636,33 +701,24 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
   std::vector<int> olist;
   for (int q = 0; q < 64; ++q)
     if ((vo >> q) & 1ull) olist.push_back(q);
-  // variant matrices U_v = G_n ... G_1 (register space), row stride kDenseStride; the variants
-  // are independent, so they are generated on host threads (QAOA-like passes carry up to 64)
+  // variant matrices U_v = G_n ... G_1 (register space), row stride kDenseStride: reserved here,
+  // computed by fill_dense_variants() for every stage of the plan at once (independent work items
+  // on the host pool; QAOA-like plans carry thousands of variants)
   const size_t off = plan->mats.size() - pd.mat_begin;
   const size_t vdoubles = 2 * 16 * (size_t)kDenseStride;
   plan->mats.resize(plan->mats.size() + (size_t)nvar * vdoubles);
   {
-    const double* opm = plan->mats.data() + pd.mat_begin;
-    double* dst = plan->mats.data() + pd.mat_begin + off;
-    parallel_for(nvar, [&](int v) {
-      uint32_t tbits = 0;
-      for (int b = 0; b < m_tile; ++b)
-        if ((v >> b) & 1) tbits |= 1u << vlist[b];
-      uint64_t obits = 0;
-      for (int b = 0; b < m_outer; ++b)
-        if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
-      Cx U[256];
-      for (int j = 0; j < 16; ++j)
-        for (int c = 0; c < 16; ++c) U[j * 16 + c] = Cx{j == c ? 1.0 : 0.0, 0.0};
-      for (const DevOp& o : sp->ops) dense_apply_cols(U, o, opm + o.mat_off, reg_new, tbits, obits);
-      double* d = dst + (size_t)v * vdoubles;
-      for (int j = 0; j < 16; ++j)
-        for (int c = 0; c < kDenseStride; ++c) {
-          const Cx e = c < 16 ? U[j * 16 + c] : Cx{0, 0};
-          *d++ = e.re;
-          *d++ = e.im;
-        }
-    });
+    DenseJob J;
+    J.ops = sp->ops;
+    J.opm = (size_t)pd.mat_begin;
+    J.dst = (size_t)pd.mat_begin + off;
+    std::memcpy(J.reg_new, reg_new, sizeof(reg_new));
+    J.vlist = vlist;
+    J.olist = olist;
+    J.m_tile = m_tile;
+    J.m_outer = m_outer;
+    if (jobs) jobs->push_back(std::move(J));
+    else fill_dense_variants(plan, std::vector<DenseJob>{std::move(J)});
   }
   StageDesc& S = sp->sd;
   std::memset(&S, 0, sizeof(S));
@@ -790,7 +846,8 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
 
 // Plans the register stages of pass `pd` (ops already emitted in pass order) and rewrites the
 // pass' op range in stage order.
-void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_local, int da_cost) {
+void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_local, int da_cost,
+                      std::vector<DenseJob>* jobs) {
   const int k = pd->k;
   std::vector<DevOp> pops(plan->ops.begin() + pd->op_begin, plan->ops.begin() + pd->op_end);
   std::vector<StagePlan> final_stages;
@@ -806,7 +863,7 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
     std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(3, k - 8), g_dense_max_var);
     std::vector<DevOp> seq;  // consecutive non-dense candidates are re-staged together
     for (StagePlan& sp : st4) {
-      if (make_dense(&sp, *pd, plan, budget)) {
+      if (make_dense(&sp, *pd, plan, budget, jobs)) {
         if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
         final_stages.push_back(std::move(sp));
       } else {
@@ -823,7 +880,7 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
     std::vector<DevOp> seq;
     for (StagePlan& sp : st4) {
       if (nda < g_da_max_per_pass &&
-          make_dense(&sp, *pd, plan, size_t(1) << 22, true, (int)plan->passes.size(), nda, g_da_max_per_pass - nda,
+          make_dense(&sp, *pd, plan, size_t(1) << 22, jobs, true, (int)plan->passes.size(), nda, g_da_max_per_pass - nda,
                      da_min, da_outer)) {
         nda += 1 << sp.sd.m_outer;
         if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
@@ -972,6 +1029,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
   plan->slot_param.clear();
   plan->slot_coeff.clear();
   plan->n_grad_slots = 0;
+  std::vector<DenseJob> jobs;  // dense-stage variant matrices, filled once every pass is planned
   std::vector<int> order(groups.size());
   for (size_t i = 0; i < groups.size(); ++i) order[i] = reverse ? (int)(groups.size() - 1 - i) : (int)i;
   for (int gidx : order) {
@@ -1043,7 +1101,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
       {
         static const bool tm = std::getenv("SV_PLAN_TIMING") != nullptr;
         const auto t0 = std::chrono::steady_clock::now();
-        plan_pass_stages(plan, &pd, !reverse, o.dense != 0, n_local, o.da_cost);
+        plan_pass_stages(plan, &pd, !reverse, o.dense != 0, n_local, o.da_cost, &jobs);
         if (tm)
           std::fprintf(stderr, "pass %zu stages %.3f ms\n", plan->passes.size(),
                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
@@ -1059,6 +1117,8 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
     plan->passes.push_back(pd);
   }
   lap("emitted");
+  fill_dense_variants(plan, jobs);
+  lap("dense variants");
   // compact register-kernel ops
   plan->rops.assign(plan->ops.size(), RegOp{});
   for (const PassDesc& pd : plan->passes) {

@@ -5,6 +5,8 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -127,11 +129,26 @@ struct PassDesc {
 };
 
 // A compiled plan: passes over one vector (forward) or two (adjoint).
+// Allocator whose value-construction leaves doubles uninitialised: resizing the plan's matrix
+// array does not zero (and page-fault) megabytes serially before the parallel fill writes them.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind { using other = NoInitAlloc<U>; };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept { ::new (static_cast<void*>(p)) U; }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) { ::new (static_cast<void*>(p)) U(std::forward<A>(a)...); }
+};
+
 struct Plan {
   std::vector<PassDesc> passes;
   std::vector<DevOp> ops;
   std::vector<RegOp> rops;  // compact copy of ops for register passes (same indexing)
-  std::vector<double> mats;
+  std::vector<double, NoInitAlloc<double>> mats;  // op matrices, generators, dense variants (per pass)
   std::vector<StageDesc> stages;
   int n_grad_slots = 0;
   std::vector<int32_t> slot_param;   // slot -> parameter index
