@@ -553,7 +553,48 @@ struct DenseJob {
   int reg_new[32];
   std::vector<int> vlist, olist;
   int m_tile = 0, m_outer = 0;
+  int da = -1;  // adjoint dense stage: index in plan->da whose B matrices this job also fills
 };
+
+// B_{j,v} = V^dagger (Pi_C G_j) V for variant v of an adjoint dense stage (V: product of the
+// stage's ops before its j-th parametrised op, register space).
+void fill_da_variant(const DenseJob& J, Plan::DAStage* ds, int v, uint32_t tbits, uint64_t obits, const double* opm) {
+  auto cm = [](Cx a, Cx b) { return Cx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; };
+  Cx V[256];  // columns c: V[j * 16 + c]
+  for (int j = 0; j < 16; ++j)
+    for (int c = 0; c < 16; ++c) V[j * 16 + c] = Cx{j == c ? 1.0 : 0.0, 0.0};
+  int gj = 0;
+  for (const DevOp& o : J.ops) {
+    if (o.grad_slot >= 0) {
+      Cx GV[256];
+      for (int c = 0; c < 16; ++c) {
+        Cx u[16];
+        for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
+        dense_gen_apply(u, o, opm + o.gen_off, J.reg_new, tbits, obits);
+        for (int j = 0; j < 16; ++j) GV[j * 16 + c] = u[j];
+      }
+      Cx* Bd = ds->B[(size_t)gj].data() + (size_t)v * 256;
+      for (int a = 0; a < 16; ++a)
+        for (int b = 0; b < 16; ++b) {
+          Cx acc{0, 0};
+          for (int j = 0; j < 16; ++j) {
+            const Cx vc = Cx{V[j * 16 + a].re, -V[j * 16 + a].im};
+            const Cx t = cm(vc, GV[j * 16 + b]);
+            acc.re += t.re;
+            acc.im += t.im;
+          }
+          Bd[a * 16 + b] = acc;
+        }
+      ++gj;
+    }
+    for (int c = 0; c < 16; ++c) {
+      Cx u[16];
+      for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
+      dense_apply(u, o, opm + o.mat_off, J.reg_new, tbits, obits);
+      for (int j = 0; j < 16; ++j) V[j * 16 + c] = u[j];
+    }
+  }
+}
 
 void fill_dense_variants(Plan* plan, const std::vector<DenseJob>& jobs) {
   std::vector<int> first(jobs.size() + 1, 0);
@@ -599,6 +640,7 @@ void fill_dense_variants(Plan* plan, const std::vector<DenseJob>& jobs) {
       }
     }
     flush();
+    if (J.da >= 0) fill_da_variant(J, &plan->da[(size_t)J.da], v, tbits, obits, opm);
     double* d = plan->mats.data() + J.dst + (size_t)v * vdoubles;
     for (int r = 0; r < 16; ++r)
       for (int c = 0; c < kDenseStride; ++c) {
@@ -717,8 +759,7 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     J.olist = olist;
     J.m_tile = m_tile;
     J.m_outer = m_outer;
-    if (jobs) jobs->push_back(std::move(J));
-    else fill_dense_variants(plan, std::vector<DenseJob>{std::move(J)});
+    jobs->push_back(std::move(J));
   }
   StageDesc& S = sp->sd;
   std::memset(&S, 0, sizeof(S));
@@ -783,55 +824,14 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     ds.m_tile = m_tile;
     ds.m_outer = m_outer;
     ds.global_slot = plan->da_slots_total + da_index;
-    // B_{j,var} = V^dagger (Pi_C G_j) V with V the product of the stage's ops before j
+    // B_{j,var} = V^dagger (Pi_C G_j) V with V the product of the stage's ops before j, filled
+    // per variant with the variant matrices (fill_dense_variants)
     for (size_t i = 0; i < sp->ops.size(); ++i)
       if (sp->ops[i].grad_slot >= 0) {
         ds.slots.push_back(sp->ops[i].grad_slot);
         ds.B.emplace_back((size_t)nvar * 256);
       }
-    auto cm = [](Cx a, Cx b) { return Cx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; };
-    for (int v = 0; v < nvar; ++v) {
-      uint32_t tbits = 0;
-      for (int b = 0; b < m_tile; ++b)
-        if ((v >> b) & 1) tbits |= 1u << vlist[b];
-      uint64_t obits = 0;
-      for (int b = 0; b < m_outer; ++b)
-        if ((v >> (m_tile + b)) & 1) obits |= 1ull << olist[b];
-      Cx V[256];  // columns c: V[j * 16 + c]
-      for (int j = 0; j < 16; ++j)
-        for (int c = 0; c < 16; ++c) V[j * 16 + c] = Cx{j == c ? 1.0 : 0.0, 0.0};
-      int gj = 0;
-      for (const DevOp& o : sp->ops) {
-        if (o.grad_slot >= 0) {
-          Cx GV[256];
-          for (int c = 0; c < 16; ++c) {
-            Cx u[16];
-            for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
-            dense_gen_apply(u, o, plan->mats.data() + pd.mat_begin + o.gen_off, reg_new, tbits, obits);
-            for (int j = 0; j < 16; ++j) GV[j * 16 + c] = u[j];
-          }
-          Cx* Bd = ds.B[(size_t)gj].data() + (size_t)v * 256;
-          for (int a = 0; a < 16; ++a)
-            for (int b = 0; b < 16; ++b) {
-              Cx acc{0, 0};
-              for (int j = 0; j < 16; ++j) {
-                const Cx vc = Cx{V[j * 16 + a].re, -V[j * 16 + a].im};
-                const Cx t = cm(vc, GV[j * 16 + b]);
-                acc.re += t.re;
-                acc.im += t.im;
-              }
-              Bd[a * 16 + b] = acc;
-            }
-          ++gj;
-        }
-        for (int c = 0; c < 16; ++c) {
-          Cx u[16];
-          for (int j = 0; j < 16; ++j) u[j] = V[j * 16 + c];
-          dense_apply(u, o, plan->mats.data() + pd.mat_begin + o.mat_off, reg_new, tbits, obits);
-          for (int j = 0; j < 16; ++j) V[j * 16 + c] = u[j];
-        }
-      }
-    }
+    jobs->back().da = (int)plan->da.size();
     plan->da.push_back(std::move(ds));
   }
   for (int nt = 0; nt < 2; ++nt)
