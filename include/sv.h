@@ -30,8 +30,10 @@
  * the next synchronous call as SV_E_CUDA / SV_E_NCCL and poison the handle (SV_E_POISONED after).
  *
  * Ownership: the caller owns every array it passes; nothing is retained after a call returns.
- * A handle owns its device memory (cudaMalloc on the device current at creation). Handles are
- * single-owner (not thread-safe); distinct handles may be used concurrently.
+ * A handle owns its device memory (cudaMalloc on the device current at creation); every entry point
+ * makes that device current for the call and restores the caller's current device on return.
+ * Handles are single-owner (not thread-safe); distinct handles, also on different devices, may be
+ * used concurrently from different threads.
  *
  * Synchrony: sv_apply_* enqueue work on the handle's stream and return (asynchronous to the host,
  * stream-ordered). sv_expectation*, sv_get_state* synchronize the stream before returning.
@@ -120,12 +122,16 @@ enum {
   SV_OPT_LOW_QUBITS = 3,         /* qubits 0..L-1 always in a tile (coalescing granule), default 3 */
   SV_OPT_DENSE = 4,              /* 1 (default): fold register stages into dense FP64-MMA stages  */
   SV_OPT_KERNEL = 5,             /* 1 (default): register-blocked kernel; 0: shared-memory kernel */
-  SV_OPT_ADJOINT_DENSE_COST = 6 /* reverse-sweep stages whose sequential cost (2 x FMA/amp + 8 per
+  SV_OPT_ADJOINT_DENSE_COST = 6, /* reverse-sweep stages whose sequential cost (2 x FMA/amp + 8 per
                                    parametrised op) reaches this run as adjoint dense MMA stages;
                                    -1 (default): 96 for states of >= 24 local qubits, else 250
                                    (their fixed per-pass costs amortise over large states only);
                                    0: every eligible stage (incl. one outer variant bit at any
                                    size); 1 << 20: none */
+  SV_OPT_C64_SPLIT = 7           /* complex64 dense stages: 3 (default) TF32 products of the hi/lo
+                                   split (~2^-21 relative per product); 1: the single hi x hi TF32
+                                   product (~2^-11) — kept only to show the tests' tolerance
+                                   detects a precision loss */
 };
 
 /* a1: |0...0> on n_qubits (1 <= n <= 40 subject to memory), current CUDA device, new stream. */
@@ -184,6 +190,13 @@ sv_status sv_reset(sv_handle h);
  * For sharded handles every rank passes the full array (set) / receives it (get, gathered). */
 sv_status sv_set_state(sv_handle h, const double* host_amps);
 sv_status sv_get_state(sv_handle h, double* host_amps);
+
+/* Sampled-amplitude readout (parity checks at sizes where the full state does not fit a host
+ * buffer, e.g. 34 qubits sharded): out[2j], out[2j+1] = (re, im) of amplitude idx[j] (LOGICAL
+ * index, qubit 0 = LSB; remaps of a sharded state are undone). count >= 0; idx[j] < 2^n
+ * (SV_E_QUBIT_RANGE otherwise). Sharded handles: every rank passes the same indices and receives all
+ * values (one all-reduce). complex64 states return their values widened. Synchronous. */
+sv_status sv_get_amplitudes(sv_handle h, const uint64_t* idx, int64_t count, double* out);
 
 /* Same, from / to DEVICE memory (device pointer on the handle's device), single-GPU handles
  * (complex64 handles: 2*2^n floats). */

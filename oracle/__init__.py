@@ -60,6 +60,10 @@ def lib():
         L.or_adjoint_grad.restype = ctypes.c_int
         L.or_shift_grad.argtypes = [P, ctypes.c_int, i64] + circ + [P, i32, i64, P, P, P]
         L.or_shift_grad.restype = ctypes.c_int
+        L.or_splitmix64.argtypes = [u64]
+        L.or_splitmix64.restype = u64
+        L.or_sample.argtypes = [P, ctypes.c_int, i64, u64, P]
+        L.or_sample.restype = None
         L.or_state_zero.argtypes = [P, ctypes.c_int]
         L.or_state_zero.restype = None
         _lib = L
@@ -200,6 +204,28 @@ def shift_grad(n: int, gates, params, ham, psi0: Optional[np.ndarray] = None) ->
     if rc != 0:
         raise ValueError("non-differentiable gate carries a parameter")
     return g[:P]
+
+
+def splitmix64(x: int) -> int:
+    return int(lib().or_splitmix64(int(x) & ((1 << 64) - 1)))
+
+
+def sample_indices(psi: np.ndarray, shots: int, seed: int) -> np.ndarray:
+    """Basis index of every shot by the inverse CDF of |psi|^2 (or_sample, Fig. 1)."""
+    psi = np.ascontiguousarray(psi, dtype=np.complex128)
+    n = int(psi.size).bit_length() - 1
+    out = np.zeros(max(int(shots), 1), dtype=np.int64)
+    lib().or_sample(_p(psi), n, int(shots), int(seed) & ((1 << 64) - 1), _p(out))
+    return out[: int(shots)]
+
+
+def sample(psi: np.ndarray, qubits: Sequence[int], shots: int, seed: int) -> np.ndarray:
+    """Per shot, bit j = measured value of qubits[j] (the library's sv_sample output format)."""
+    idx = sample_indices(psi, shots, seed).astype(np.uint64)
+    out = np.zeros(idx.size, dtype=np.uint64)
+    for j, q in enumerate(qubits):
+        out |= ((idx >> np.uint64(q)) & np.uint64(1)) << np.uint64(j)
+    return out
 
 
 def energy(n: int, gates, params, ham, psi0=None) -> float:

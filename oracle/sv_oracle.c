@@ -30,6 +30,8 @@
  *                         reverse sweep un-applying U_k^dagger from psi and lambda, in that order.
  *   or_shift_grad       — exact parameter-shift rules per gate occurrence (2-term / 4-term,
  *                         reading c2.10), a second, independent gradient definition.
+ *   or_sample           — "Sampling Measurement" (Fig. 1): inverse CDF of
+ *                         |psi_i|^2 with SplitMix64 counter-based uniforms (sv.h contract).
  * Reductions: Neumaier compensated sums over fixed chunks combined in fixed order, so results do
  * not depend on the OpenMP thread count (reading c2.16).
  *
@@ -433,4 +435,43 @@ int or_shift_grad(const double* psi0, int n, int64_t ngates, const int32_t* kind
 void or_state_zero(double* psi, int n) {
   memset(psi, 0, sizeof(double) * 2 * ((size_t)1 << n));
   psi[0] = 1.0;
+}
+
+/* ---- sampling measurement ("Sampling Measurement", Fig. 1) ----
+ * The plain inverse-CDF definition: with p_i = |psi_i|^2 and the running sums F_i = p_0 + ... + p_i
+ * (left to right), shot s draws the basis index
+ *     i_s = min { i : F_i >= u_s * F_{N-1} }   (N - 1 if no such i),
+ * u_s = (splitmix64(seed + s) >> 11) * 2^-53 in [0, 1) — the counter-based uniform the library's
+ * contract fixes (include/sv.h sv_sample), implemented here on its own: SplitMix64's published
+ * output function (golden constant 0x9E3779B97F4A7C15, shifts 30/27/31, multipliers
+ * 0xBF58476D1CE4E5B9 / 0x94D049BB133111EB). Marginals over measured qubits are read off i_s by the
+ * caller. One binary search per shot over F (no sorting, no blocking). */
+uint64_t or_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void or_sample(const double* psi_, int n, int64_t shots, uint64_t seed, int64_t* out_index) {
+  const cplx* psi = (const cplx*)psi_;
+  const int64_t N = (int64_t)1 << n;
+  double* F = (double*)malloc(sizeof(double) * N);
+  double run = 0.0;
+  for (int64_t i = 0; i < N; ++i) {
+    double p = creal(psi[i]) * creal(psi[i]) + cimag(psi[i]) * cimag(psi[i]);
+    run += p;
+    F[i] = run;
+  }
+  const double total = F[N - 1];
+  for (int64_t s = 0; s < shots; ++s) {
+    const double u = (double)(or_splitmix64(seed + (uint64_t)s) >> 11) * (1.0 / 9007199254740992.0) * total;
+    int64_t lo = 0, hi = N - 1; /* smallest i in [lo, hi] with F_i >= u (hi if none) */
+    while (lo < hi) {
+      int64_t mid = lo + (hi - lo) / 2;
+      if (F[mid] >= u) hi = mid; else lo = mid + 1;
+    }
+    out_index[s] = lo;
+  }
+  free(F);
 }

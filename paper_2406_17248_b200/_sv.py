@@ -21,6 +21,7 @@ STATUS = {0: "SV_OK", 1: "SV_E_ARG", 2: "SV_E_QUBIT_RANGE", 3: "SV_E_TARGET_CONT
           8: "SV_E_OOM", 9: "SV_E_CUDA", 10: "SV_E_NCCL", 11: "SV_E_POISONED"}
 SV_OPT_TILE_QUBITS, SV_OPT_FUSION, SV_OPT_LOW_QUBITS, SV_OPT_DENSE, SV_OPT_KERNEL = 1, 2, 3, 4, 5
 SV_OPT_ADJOINT_DENSE_COST = 6
+SV_OPT_C64_SPLIT = 7
 
 
 class SvError(RuntimeError):
@@ -80,6 +81,7 @@ def _load():
         "sv_reset": [H],
         "sv_set_state": [H, P],
         "sv_get_state": [H, P],
+        "sv_get_amplitudes": [H, P, i64, P],
         "sv_set_state_device": [H, P],
         "sv_get_state_device": [H, P],
         "sv_apply_gate": [H, ctypes.POINTER(sv_gate), P, i32],
@@ -252,6 +254,14 @@ def sv_get_state(h, n: int, out: Optional[np.ndarray] = None) -> np.ndarray:
     return out
 
 
+def sv_get_amplitudes(h, idx) -> np.ndarray:
+    """Amplitudes at logical indices idx (sampled readout; sharded states un-permuted)."""
+    i = np.ascontiguousarray(np.asarray(idx, dtype=np.uint64).reshape(-1))
+    out = np.empty(max(i.size, 1), dtype=np.complex128)
+    _check(lib.sv_get_amplitudes(h, _ptr(i), int(i.size), _ptr(out)))
+    return out[: i.size]
+
+
 def sv_set_state_device(h, dev_ptr: int) -> None:
     _check(lib.sv_set_state_device(h, ctypes.c_void_p(dev_ptr)))
 
@@ -392,6 +402,9 @@ class StateVector:
 
     def get_state(self):
         return sv_get_state(self.h, self.n)
+
+    def get_amplitudes(self, idx):
+        return sv_get_amplitudes(self.h, idx)
 
     def apply_circuit(self, gates, params=None):
         sv_apply_circuit(self.h, gates, params)

@@ -140,12 +140,24 @@ void release_plan_cache(sv_state_s* h) {
   h->plan_cache.clear();
 }
 
-static uint64_t plan_key(const sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse) {
+struct PlanMeta {
+  int v[9];
+};
+static PlanMeta plan_meta(const sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse) {
+  return PlanMeta{{h->n_local, reverse ? 1 : 0, h->opts.tile_qubits, h->opts.low_qubits, h->opts.fusion ? 1 : 0,
+                   h->opts.kernel, h->opts.dense, h->opts.da_cost, (int)gates.size()}};
+}
+
+static uint64_t plan_key(const std::vector<BoundGate>& gates, const PlanMeta& meta) {
   uint64_t key = 1469598103934665603ull;
   key = hash_bytes(gates.data(), gates.size() * sizeof(BoundGate), key);
-  const int meta[9] = {h->n_local, reverse ? 1 : 0, h->opts.tile_qubits, h->opts.low_qubits, h->opts.fusion ? 1 : 0,
-                       h->opts.kernel, h->opts.dense, h->opts.da_cost, (int)gates.size()};
-  return hash_bytes(meta, sizeof(meta), key);
+  return hash_bytes(&meta, sizeof(meta), key);
+}
+
+static bool plan_ident_equal(const CachedPlan& c, const std::vector<BoundGate>& gates, const PlanMeta& meta) {
+  const size_t gb = gates.size() * sizeof(BoundGate);
+  return c.ident.size() == gb + sizeof(meta) && std::memcmp(c.ident.data(), gates.data(), gb) == 0 &&
+         std::memcmp(c.ident.data() + gb, &meta, sizeof(meta)) == 0;
 }
 
 static constexpr int kCacheEntries = 8;
@@ -166,15 +178,22 @@ static CachedPlan* plan_slot(sv_state_s* h) {
 static int upload_plan(sv_state_s* h, CachedPlan* c, uint64_t key, const CachedPlan** out);
 
 int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, const CachedPlan** out) {
-  const uint64_t key = plan_key(h, gates, reverse);
+  const PlanMeta meta = plan_meta(h, gates, reverse);
+  const uint64_t key = plan_key(gates, meta);
   for (CachedPlan* c : h->plan_cache)
-    if (c->key == key) {
+    if (c->key == key && plan_ident_equal(*c, gates, meta)) {
       c->stamp = ++h->plan_clock;
       *out = c;
       return SV_OK;
     }
   CachedPlan* c = plan_slot(h);
   c->key = 0;
+  {
+    const size_t gb = gates.size() * sizeof(BoundGate);
+    c->ident.resize(gb + sizeof(meta));
+    std::memcpy(c->ident.data(), gates.data(), gb);
+    std::memcpy(c->ident.data() + gb, &meta, sizeof(meta));
+  }
   build_plan(gates, h->n_local, h->opts, reverse, &c->plan);
   return upload_plan(h, c, key, out);
 }
@@ -324,6 +343,7 @@ static int run_plan_c64(sv_state_s* h, const CachedPlan& cp) {
     L.grid = (int)std::min<int64_t>(ntiles, (int64_t)device_sm_count() * 3);
     L.n_local = h->n_local;
     L.rank_bits = 0;
+    L.c64_terms = h->c64_split;
     cudaError_t e = launch_pass_c64(h->psi32, L, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "complex64 pass launch");
     h->stats.kernel_launches += 1;
@@ -639,6 +659,7 @@ sv_status sv_create_c64(int32_t n_qubits, sv_handle* out) {
 
 sv_status sv_destroy(sv_handle h) {
   if (!h) return SV_OK;
+  DeviceGuard dev_guard(h->device);
   cudaStreamSynchronize(h->stream);
   h->state.release();
   h->promo.release();
@@ -691,6 +712,10 @@ sv_status sv_set_option(sv_handle h, int32_t key, int64_t value) {
       if (value < -1 || value > (1 << 20)) return fail(SV_E_ARG, "adjoint dense cost threshold out of range");
       h->opts.da_cost = (int)value;
       return SV_OK;
+    case SV_OPT_C64_SPLIT:
+      if (value != 1 && value != 3) return fail(SV_E_ARG, "complex64 split must be 1 or 3");
+      h->c64_split = (int)value;
+      return SV_OK;
     default: return fail(SV_E_ARG, "unknown option");
   }
 }
@@ -704,6 +729,7 @@ sv_status sv_get_num_qubits(sv_handle h, int32_t* out) {
 sv_status sv_reset(sv_handle h) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (h->world > 1) return shard_reset(h);
   if (h->c64) {
     cudaError_t e = init_c64(h);
@@ -719,6 +745,7 @@ sv_status sv_reset(sv_handle h) {
 sv_status sv_set_state(sv_handle h, const double* host) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (!host) return fail(SV_E_ARG, "null host buffer");
   if (h->world > 1) return shard_set_state(h, host);
   if (h->c64) {  // complex128 host values rounded to complex64
@@ -751,6 +778,7 @@ sv_status sv_set_state(sv_handle h, const double* host) {
 sv_status sv_get_state(sv_handle h, double* host) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (!host) return fail(SV_E_ARG, "null host buffer");
   if (h->world > 1) return shard_get_state(h, host);
   if (h->c64) {
@@ -780,9 +808,50 @@ sv_status sv_get_state(sv_handle h, double* host) {
   return SV_OK;
 }
 
+}  // extern "C"
+
+int sv::gather_amplitudes(sv_state_s* h, const void* psi, bool c64, const std::vector<uint64_t>& idx, double* out,
+                          bool accumulate) {
+  const size_t cnt = idx.size();
+  if (!cnt) return SV_OK;
+  const size_t ib = (cnt * 8 + 63) & ~size_t(63);
+  if (!h->d_terms.ensure(ib + cnt * 16 + 64)) return fail(SV_E_OOM, "amplitude readout buffers");
+  char* db = static_cast<char*>(h->d_terms.p);
+  std::vector<double> tmp(2 * cnt);
+  cudaError_t e = cudaMemcpyAsync(db, idx.data(), cnt * 8, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess)
+    e = launch_gather(psi, c64, reinterpret_cast<const uint64_t*>(db), (int64_t)cnt, reinterpret_cast<double*>(db + ib),
+                      h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(tmp.data(), db + ib, cnt * 16, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "amplitude readout");
+  h->stats.kernel_launches += 1;
+  for (size_t j = 0; j < 2 * cnt; ++j) out[j] = accumulate ? out[j] + tmp[j] : tmp[j];
+  return SV_OK;
+}
+
+extern "C" {
+
+sv_status sv_get_amplitudes(sv_handle h, const uint64_t* idx, int64_t count, double* out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
+  if (count < 0 || (count > 0 && (!idx || !out))) return fail(SV_E_ARG, "bad amplitude readout arguments");
+  if (h->density) return fail(SV_E_ARG, "amplitude readout is for state vectors (use sv_get_state)");
+  const uint64_t lim = h->n >= 64 ? ~0ull : (1ull << h->n);
+  for (int64_t j = 0; j < count; ++j)
+    if (idx[j] >= lim) return fail(SV_E_QUBIT_RANGE, "amplitude index >= 2^n");
+  if (count == 0) return SV_OK;
+  if (h->world > 1) return shard_get_amplitudes(h, idx, count, out);
+  std::vector<uint64_t> v(idx, idx + count);
+  return gather_amplitudes(h, h->c64 ? static_cast<const void*>(h->psi32) : static_cast<const void*>(h->psi), h->c64, v,
+                           out, false);
+}
+
 sv_status sv_set_state_device(sv_handle h, const void* dev) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (!dev) return fail(SV_E_ARG, "null device buffer");
   if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
   cudaError_t e = h->c64 ? cudaMemcpyAsync(h->psi32, dev, size_t(8) << h->n_local, cudaMemcpyDeviceToDevice, h->stream)
@@ -794,6 +863,7 @@ sv_status sv_set_state_device(sv_handle h, const void* dev) {
 sv_status sv_get_state_device(sv_handle h, void* dev) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (!dev) return fail(SV_E_ARG, "null device buffer");
   if (h->world > 1) return fail(SV_E_ARG, "device-pointer state transfer is single-GPU only");
   cudaError_t e = h->c64 ? cudaMemcpyAsync(dev, h->psi32, size_t(8) << h->n_local, cudaMemcpyDeviceToDevice, h->stream)
@@ -810,6 +880,7 @@ sv_status sv_apply_gate(sv_handle h, const sv_gate* g, const double* params, int
 sv_status sv_apply_circuit(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params, int32_t n_params) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   std::vector<BoundGate> bg;
   rc = bind_circuit(h, gates, n_gates, params, n_params, false, &bg);
   if (rc) return rc;
@@ -821,6 +892,7 @@ sv_status sv_apply_circuit(sv_handle h, const sv_gate* gates, int64_t n_gates, c
 sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, double* out_value) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (!out_value) return fail(SV_E_ARG, "null out_value");
   PauliGroups G;
   rc = group_terms(h, terms, n_terms, &G);
@@ -890,6 +962,7 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
                                    double* out_grad) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (!out_value || (n_params > 0 && !out_grad)) return fail(SV_E_ARG, "null output");
   if (h->density) return fail(SV_E_ARG, "gradients are not available on density-matrix handles");
   if (h->c64) {  // complex64 state: this operation reads a complex128 copy (the state is unchanged)
@@ -1105,6 +1178,7 @@ extern "C" sv_status sv_expectation_with_grad_batch(sv_handle h, const sv_gate* 
                                                     double* out_grads) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (n_rows < 0 || !out_values || (n_rows > 0 && n_params > 0 && (!params || !out_grads)))
     return fail(SV_E_ARG, "bad batch arguments");
   if (n_rows == 0) return SV_OK;
@@ -1269,6 +1343,7 @@ extern "C" sv_status sv_sample(sv_handle h, const int32_t* qubits, int32_t n_mea
                                uint64_t* out) {
   int rc = check_handle(h);
   if (rc) return rc;
+  DeviceGuard dev_guard(h->device);
   if (shots < 0 || n_measured < 0 || n_measured > 64 || (shots > 0 && !out) || (n_measured > 0 && !qubits))
     return fail(SV_E_ARG, "bad sampling arguments");
   if (h->world > 1) return fail(SV_E_ARG, "sampling is single-GPU in this version");

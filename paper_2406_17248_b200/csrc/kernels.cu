@@ -297,6 +297,19 @@ __global__ void k_pack_half(double2* __restrict__ shard, double2* __restrict__ b
   }
 }
 
+// Sampled-amplitude readout: out[j] = psi[idx[j]] for idx[j] != ~0, else 0 (an index another shard
+// holds). T: double2 (complex128 state) or float2 (complex64 state).
+template <typename T>
+__global__ void k_gather(const T* __restrict__ psi, const uint64_t* __restrict__ idx, int64_t count,
+                         double2* __restrict__ out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = idx[j];
+    if (i == ~0ull) { out[j] = make_double2(0.0, 0.0); continue; }
+    const T v = psi[i];
+    out[j] = make_double2((double)v.x, (double)v.y);
+  }
+}
+
 __global__ void k_init(double2* psi, int64_t n, bool one) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -725,15 +738,16 @@ size_t pass_smem_bytes(int k, int low, int nops, int nmats, bool dual) {
   return b;
 }
 
-int g_num_sms = 0;
+std::atomic<int> g_num_sms[64];  // per device id (zero-initialised: static storage)
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  const int dev = current_device() & 63;
+  int v = g_num_sms[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    g_num_sms[dev].store(v, std::memory_order_relaxed);
   }
-  return g_num_sms;
+  return v;
 }
 
 }  // namespace
@@ -810,12 +824,13 @@ cudaError_t launch_pass(double* psi, double* lam, const PassLaunch& L, cudaStrea
   a.grid = L.pstride > 0 ? L.pstride : L.grid;  // slot-row stride of the partials
   const bool dual = lam != nullptr;
   const size_t smem = pass_smem_bytes(a.k, a.low, a.nops, a.nmats, dual);
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[dual]) {
-    cudaError_t e = dual ? cudaFuncSetAttribute(k_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
-                         : cudaFuncSetAttribute(k_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static std::atomic<uint64_t> attr_set{0};
+  {
+    cudaError_t e = once_per_device(attr_set, [] {
+      cudaError_t r = cudaFuncSetAttribute(k_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      return r == cudaSuccess ? cudaFuncSetAttribute(k_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) : r;
+    });
     if (e != cudaSuccess) return e;
-    attr_set[dual] = true;
   }
   if (dual)
     k_pass<true><<<L.grid, kThreads, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
@@ -860,6 +875,17 @@ static int elementwise_grid(int64_t n) {
   const int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   return (int)(blocks < 1 ? 1 : blocks);
+}
+
+cudaError_t launch_gather(const void* psi, bool c64, const uint64_t* idx, int64_t count, double* out, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  if (c64)
+    k_gather<float2><<<elementwise_grid(count), kThreads, 0, s>>>(static_cast<const float2*>(psi), idx, count,
+                                                                  reinterpret_cast<double2*>(out));
+  else
+    k_gather<double2><<<elementwise_grid(count), kThreads, 0, s>>>(static_cast<const double2*>(psi), idx, count,
+                                                                   reinterpret_cast<double2*>(out));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_swap_halves(double* a, double* b, int nl, int l, cudaStream_t s) {
@@ -917,12 +943,13 @@ static cudaError_t pauli_tile_impl(const void* psi, bool c64, double* lam, int m
   a.c = reinterpret_cast<const double2*>(d_c) + pp.term_base;
   a.partials = d_partials;
   const size_t smem = (size_t(c64 ? 16 : 32) << pp.k) + (size_t)pp.nterms * 28 + 8 + (size_t(8) << (pp.k - pp.low));
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_pauli_tile<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pauli_tile<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  static std::atomic<uint64_t> attr{0};
+  {
+    cudaError_t e = once_per_device(attr, [] {
+      cudaError_t r = cudaFuncSetAttribute(k_pauli_tile<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      return r == cudaSuccess ? cudaFuncSetAttribute(k_pauli_tile<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) : r;
+    });
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   if (c64) {
     if (lam || mode != 0 || pp.tq[0] != 0) return cudaErrorInvalidValue;  // E only; pairs need qubit 0 at position 0

@@ -153,11 +153,11 @@ __global__ void __launch_bounds__(kBT) k_batch_grad(const double2* __restrict__ 
 
 cudaError_t launch_batch_grad(const double* psi0, int n, const BatchArgs& a, int rows, cudaStream_t s) {
   const size_t smem = (size_t(32) << n);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_batch_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  static std::atomic<uint64_t> attr{0};
+  {
+    cudaError_t e = once_per_device(
+        attr, [] { return cudaFuncSetAttribute(k_batch_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   k_batch_grad<<<rows, kBT, smem, s>>>(reinterpret_cast<const double2*>(psi0), n, a);
   return cudaGetLastError();

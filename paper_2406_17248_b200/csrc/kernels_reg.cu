@@ -62,6 +62,7 @@ __device__ __forceinline__ double2 cneg(double2 a) { return make_double2(-a.x, -
 struct RegArgs {
   int32_t k, low, nops, nstages, n_outer, nmats, ngrad, grid;
   int32_t n_da, pstride;  // pstride: slot-row stride of partials (>= grid)
+  int32_t c64_terms, pad_;  // complex64 dense stages: 3 = hi/lo split products (default), 1 = hi only
   double* r_partials;  // adjoint dense stages: [da][warp][16 * 32][grid]
   int8_t tq[kMaxTileQubits + 3];
   int8_t oq[64];
@@ -1009,7 +1010,7 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
 }
 
 __device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S, const double2* __restrict__ gm2,
-                                                 uint64_t base, int warp, int lane) {
+                                                 uint64_t base, int warp, int lane, bool split) {
   const int g = lane >> 2, t = lane & 3;
   uint32_t var = S.warp_var[warp];
   for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
@@ -1073,6 +1074,7 @@ __device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S,
       mma_tf32(dim, aih, xr_h[kh][0], xr_h[kh][1]);
       mma_tf32(dre, nih, xi_h[kh][0], xi_h[kh][1]);
       mma_tf32(dim, arh, xi_h[kh][0], xi_h[kh][1]);
+      if (!split) continue;  // SV_OPT_C64_SPLIT = 1: one TF32 product (test of the tolerance's power)
       mma_tf32(dre, arh, xr_l[kh][0], xr_l[kh][1]);
       mma_tf32(dim, aih, xr_l[kh][0], xr_l[kh][1]);
       mma_tf32(dre, nih, xi_l[kh][0], xi_l[kh][1]);
@@ -1157,7 +1159,7 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_c64(float2* __restric
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
       if (S.dense) {
-        dense_stage_tf32(tp, S, gm2, base, warp, lane);
+        dense_stage_tf32(tp, S, gm2, base, warp, lane, a.c64_terms != 1);
         __syncthreads();
         continue;
       }
@@ -1242,13 +1244,13 @@ bool pass_all_dense(const Plan& plan, const PassDesc& pd) {
 }
 
 static cudaError_t set_reg_attrs() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e == cudaSuccess) done = true;
-  return e;
+  static std::atomic<uint64_t> done{0};
+  return once_per_device(done, [] {
+    cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return e;
+  });
 }
 
 // Resident CTAs per SM for the register passes of a plan: the largest pass' shared memory decides
@@ -1364,13 +1366,14 @@ cudaError_t launch_pass_c64(float* psi, const PassLaunch& L, cudaStream_t s) {
   a.ops = L.d_rops + pd.op_begin;
   a.mats = L.d_mats + pd.mat_begin;
   a.stages = L.d_stages + pd.stage_begin;
+  a.c64_terms = L.c64_terms;
   const int nthr = 1 << tb;
   const size_t smem = c64_pass_smem_bytes(a.k, a.nops, a.nstages, a.nmats);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_pass_c64, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static std::atomic<uint64_t> attr{0};
+  {
+    cudaError_t e = once_per_device(
+        attr, [] { return cudaFuncSetAttribute(k_pass_c64, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   k_pass_c64<<<L.grid, nthr, smem, s>>>(reinterpret_cast<float2*>(psi), a);

@@ -72,7 +72,10 @@ class PlanPool {
   }
   int size() const { return (int)workers_.size() + 1; }
   void run(int n, const std::function<void(int)>& f) {
-    if (workers_.empty() || n < 8) {
+    // one job at a time: a second thread planning concurrently (distinct handles may be driven
+    // from different threads, sv.h) runs its items inline instead of sharing the counter
+    std::unique_lock<std::mutex> job_lock(run_m_, std::try_to_lock);
+    if (workers_.empty() || n < 8 || !job_lock.owns_lock()) {
       for (int i = 0; i < n; ++i) f(i);
       return;
     }
@@ -123,6 +126,7 @@ class PlanPool {
     }
   }
   std::vector<std::thread> workers_;
+  std::mutex run_m_;  // held for a whole job
   std::mutex m_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* job_ = nullptr;

@@ -471,6 +471,25 @@ int shard_get_state(sv_state_s* h, double* host) {
   return SV_OK;
 }
 
+// Sampled amplitudes in logical order: every held shard gathers the indices it owns (others read
+// as 0), the NCCL transport sums the per-rank vectors with one all-reduce (x + 0 = x: exact).
+int shard_get_amplitudes(sv_state_s* h, const uint64_t* idx, int64_t count, double* out) {
+  ShardState& S = *h->shard;
+  const int nl = h->n_local;
+  std::fill(out, out + 2 * count, 0.0);
+  for (size_t a = 0; a < S.ranks.size(); ++a) {
+    std::vector<uint64_t> loc((size_t)count);
+    for (int64_t j = 0; j < count; ++j) {
+      uint64_t sh, lo;
+      locate(idx[j], S.perm, nl, &sh, &lo);
+      loc[(size_t)j] = sh == (uint64_t)S.ranks[a] ? lo : ~0ull;
+    }
+    int rc = gather_amplitudes(h, S.bufs[a].p, false, loc, out, true);
+    if (rc) return rc;
+  }
+  return allreduce_host(h, out, (size_t)(2 * count));
+}
+
 int shard_apply(sv_state_s* h, const std::vector<BoundGate>& bg) {
   ShardState& S = *h->shard;
   std::vector<Step> steps = schedule(bg, S.perm, h->n_local);

@@ -37,6 +37,8 @@ struct ShardState;  // shard.cpp
 // benchmark loop, a repeated evaluation) skips planning and the upload.
 struct CachedPlan {
   uint64_t key = 0;
+  std::vector<unsigned char> ident;  // the bound gates' bytes + planning meta: a hash hit is verified
+                                     // by comparing these (no silent reuse on a 64-bit collision)
   uint64_t stamp = 0;
   Plan plan;
   DevBuf buf;
@@ -71,6 +73,7 @@ struct sv_state_s {
   std::vector<sv::CachedPlan*> plan_cache;  // owned, LRU (small)
   uint64_t plan_clock = 0;
   sv::PlanOptions opts;
+  int c64_split = 3;  // SV_OPT_C64_SPLIT
   sv_stats stats{};
   sv::ShardState* shard = nullptr;
 };
@@ -105,6 +108,11 @@ void destroy_sharding(sv_state_s* h);
 int shard_reset(sv_state_s* h);
 int shard_set_state(sv_state_s* h, const double* host);
 int shard_get_state(sv_state_s* h, double* host);
+int shard_get_amplitudes(sv_state_s* h, const uint64_t* idx, int64_t count, double* out);
+// gathers psi[dev_idx[j]] (local indices, ~0 = not held) into host out (2 * count doubles), adding
+// into out when accumulate (exact: other shards contribute 0)
+int gather_amplitudes(sv_state_s* h, const void* psi, bool c64, const std::vector<uint64_t>& idx, double* out,
+                      bool accumulate);
 int shard_apply(sv_state_s* h, const std::vector<BoundGate>& bg);
 int shard_expectation(sv_state_s* h, const PauliGroups& G, double* out);
 int shard_expectation_with_grad(sv_state_s* h, const std::vector<BoundGate>& bg, int32_t n_params,

@@ -2,6 +2,7 @@
 // kernels (kernels.cu). Not part of the ABI (include/sv.h is).
 #pragma once
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <functional>
@@ -13,6 +14,35 @@
 #include <cuda_runtime.h>
 
 namespace sv {
+
+// Per-device one-time setup (function attributes such as the dynamic shared-memory opt-in are per
+// device): f() runs until it succeeds once on each device; a mask bit per device id, thread-safe
+// (a race runs f twice, which is harmless for attribute setters).
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+template <class F>
+cudaError_t once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = f();
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+// Makes the handle's device current for the duration of an entry point (restores the caller's).
+struct DeviceGuard {
+  int prev = -1, want = -1;
+  explicit DeviceGuard(int dev) : want(dev) {
+    cudaGetDevice(&prev);
+    if (prev != want) cudaSetDevice(want);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
 
 struct Cx {
   double re, im;
@@ -224,6 +254,7 @@ struct PassLaunch {
   int grid;                // CTAs
   int pstride = 0;         // stride of d_partials' slot rows (>= grid; 0: grid)
   bool all_dense = false;  // forward register pass of dense stages only (k_pass_dense)
+  int c64_terms = 3;       // complex64 dense stages: TF32 split products (3) or one product (1)
   int n_local;
   uint64_t rank_bits;      // (sharded) global index bits of this shard, for controls/diagonals on
                            // global qubits folded by the planner (0 single-GPU)
@@ -242,6 +273,8 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual);
 bool pass_all_dense(const Plan& plan, const PassDesc& pd);  // k_pass_dense eligible  // resident CTAs/SM of a register pass
 
 cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
+// out[j] = psi[idx[j]] (complex128 out; idx[j] == ~0 -> 0); psi complex128, or complex64 if c64
+cudaError_t launch_gather(const void* psi, bool c64, const uint64_t* idx, int64_t count, double* out, cudaStream_t s);
 // Sharding: swap halves of two virtual shards (a[y0|2^l] <-> b[y0]); pack / unpack the half of a
 // shard with local bit l == h (elements off .. off+count of that half) to / from a buffer.
 cudaError_t launch_swap_halves(double* a, double* b, int nl, int l, cudaStream_t s);

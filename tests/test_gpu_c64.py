@@ -1,10 +1,15 @@
 """NEXT-3 complex64 mode ("single-precision and double-precision
 simulation modes") vs the complex128 CPU oracle.
 
-Tolerance 1e-4: a complex64 amplitude carries a relative rounding of 2^-24 ~ 6e-8
-per stored value; every stage rounds once, a dense stage adds 16-term FP32 dot products, so after
-~100 stages the absolute error per amplitude of a unit-norm state stays ~1e-5. Energies are
-FP64-accumulated over complex64 inputs: |dE| <= 2 sum|c_t| * max|d psi| << 1e-4 for the sums here.
+Tolerances are RELATIVE to the state (an absolute 1e-4 on amplitudes of size 2^(-n/2) would let a
+5% error per amplitude through). Derivation: a stored complex64 value carries 2^-24 ~ 6e-8
+relative rounding; a dense stage's 16-term products use the 3-product TF32 hi/lo split
+(hi = top 10 mantissa bits, lo = the rest, read by the tensor core to 10 bits) whose per-product
+error is ~2^-21 ~ 5e-7 relative, FP32 accumulation adds ~2^-24 per term. Over the <= ~30 stages of
+these circuits, independent errors add in quadrature: ||d psi||_2 / ||psi||_2 ~ sqrt(30) * 6e-7
+~ 3e-6, so REL = 1e-5 holds with margin. A single hi x hi TF32 product (2^-11 ~ 5e-4 relative)
+gives ~1e-3: `test_c64_tolerance_detects_single_tf32` shows the bound catches it. Energies are
+FP64-accumulated over complex64 inputs: |dE| <= 2 * sum|c_t| * ||d psi||_2.
 """
 import numpy as np
 import pytest
@@ -13,7 +18,15 @@ import oracle
 import workloads as W
 
 pytestmark = pytest.mark.gpu
-TOL = 1e-4
+REL = 1e-5   # ||psi_gpu - psi_oracle||_2 <= REL * ||psi_oracle||_2 (module docstring)
+
+
+def rel_err(got, ref):
+    return float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+
+
+def e_tol(ham):
+    return 2.0 * REL * sum(abs(c) for c, _ in ham) + 1e-12
 
 
 @pytest.fixture(scope="module")
@@ -36,7 +49,7 @@ def test_c64_dense_circuit(P, n, depth, native):
     got = sv.get_state()
     st = P.sv_get_stats(sv.h)
     sv.close()
-    assert np.max(np.abs(got - ref)) <= TOL
+    assert rel_err(got, ref) <= REL
     # native complex64 passes: 16 bytes per amplitude per pass, no widen/narrow traffic
     if native:
         assert st["algorithmic_bytes"] == pytest.approx(16.0 * (1 << n) * st["gate_passes"])
@@ -56,7 +69,7 @@ def test_c64_controlled_random(P, n):
     sv.apply_circuit(w.gates)
     got = sv.get_state()
     sv.close()
-    assert np.max(np.abs(got - ref)) <= TOL
+    assert rel_err(got, ref) <= REL
 
 
 @pytest.mark.parametrize("n", [10, 14])
@@ -69,7 +82,7 @@ def test_c64_expectation(P, n):
     sv.apply_circuit(w.gates)
     E = sv.expectation(ham)
     sv.close()
-    assert abs(E - ref) <= TOL
+    assert abs(E - ref) <= e_tol(ham)
 
 
 def test_c64_promoted_paths(P):
@@ -79,7 +92,7 @@ def test_c64_promoted_paths(P):
     w = W.random_complex(5, 4, seed=3)
     sv = P.StateVectorC64(5)
     sv.apply_circuit(w.gates)
-    assert np.max(np.abs(sv.get_state() - oracle.apply_circuit(5, w.gates))) <= TOL
+    assert rel_err(sv.get_state(), oracle.apply_circuit(5, w.gates)) <= REL
     sv.close()
     # wide x-mask (X on every qubit of 16)
     n = 16
@@ -88,7 +101,7 @@ def test_c64_promoted_paths(P):
     sv = P.StateVectorC64(n)
     sv.apply_circuit(w.gates)
     psi = oracle.apply_circuit(n, w.gates)
-    assert abs(sv.expectation(ham) - oracle.expectation(psi, ham)[0]) <= TOL
+    assert abs(sv.expectation(ham) - oracle.expectation(psi, ham)[0]) <= e_tol(ham)
     sv.close()
     # gradient on a complex64 handle (complex128 copy of the complex64 start state)
     h = W.hea(10, 2, seed=4, nterms=12)
@@ -96,8 +109,9 @@ def test_c64_promoted_paths(P):
     E, g = sv.expectation_with_grad(h.gates, h.params, h.ham)
     Er, gr = oracle.adjoint_grad(10, h.gates, h.params, h.ham)
     sv.close()
-    assert abs(E - Er) <= TOL
-    assert np.max(np.abs(g - gr)) <= TOL
+    # the gradient runs in complex128 on the widened complex64 start state |0..0> (exact)
+    assert abs(E - Er) <= 1e-9
+    assert np.max(np.abs(g - gr)) <= 1e-9
 
 
 def test_c64_sampling_and_reset(P):
@@ -122,7 +136,26 @@ def test_c64_matches_c128_path(P):
     b = P.StateVectorC64(n)
     a.apply_circuit(w.gates)
     b.apply_circuit(w.gates)
-    assert np.max(np.abs(a.get_state() - b.get_state())) <= TOL
-    assert abs(a.expectation(ham) - b.expectation(ham)) <= TOL
+    assert rel_err(b.get_state(), a.get_state()) <= REL
+    assert abs(a.expectation(ham) - b.expectation(ham)) <= e_tol(ham)
     a.close()
     b.close()
+
+
+def test_c64_tolerance_detects_single_tf32(P):
+    """The relative bound has the power to catch a precision bug: the same 19-qubit dense circuit
+    with the dense stages reduced to the single hi x hi TF32 product (SV_OPT_C64_SPLIT = 1, ~2^-11
+    relative per product) exceeds REL by orders of magnitude, while the default 3-product split
+    stays inside it."""
+    n = 19
+    w = W.random_circuit(n, 8, seed=100 + n)
+    ref = oracle.apply_circuit(n, w.gates)
+    errs = {}
+    for split in (3, 1):
+        sv = P.StateVectorC64(n)
+        sv.set_option(P.SV_OPT_C64_SPLIT, split)
+        sv.apply_circuit(w.gates)
+        errs[split] = rel_err(sv.get_state(), ref)
+        sv.close()
+    assert errs[3] <= REL, errs
+    assert errs[1] > 10 * REL, errs

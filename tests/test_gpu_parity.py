@@ -336,3 +336,33 @@ def test_user_streams(P):
     assert abs(E - E0) < E_TOL and abs(E2 - E0) < E_TOL
     np.testing.assert_allclose(g, g0, atol=E_TOL, rtol=0)
     assert np.array_equal(g, g2)
+
+
+def test_concurrent_handles_two_threads(P):
+    """Distinct handles may be driven concurrently (include/sv.h): two threads evaluate gradients of
+    different circuits with changing parameters at once (each call plans on the shared host worker
+    pool and launches on its own stream; ctypes releases the GIL); every result equals the
+    oracle's."""
+    import threading
+
+    cases = [W.qaoa(12, 3, seed_graph=5, seed_angles=6), W.hea(11, 3, seed=9, nterms=20)]
+    refs = [[oracle.adjoint_grad(w.n, w.gates, w.params + 0.01 * r, w.ham) for r in range(4)] for w in cases]
+    errs = [[], []]
+
+    def worker(i):
+        w = cases[i]
+        sv = P.StateVector(w.n)
+        try:
+            for r in range(4):
+                E, g = sv.expectation_with_grad(w.gates, w.params + 0.01 * r, w.ham)
+                errs[i].append(max(abs(E - refs[i][r][0]), float(np.max(np.abs(g - refs[i][r][1])))))
+        finally:
+            sv.close()
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert len(errs[0]) == 4 and len(errs[1]) == 4
+    assert max(errs[0] + errs[1]) <= 1e-9, errs

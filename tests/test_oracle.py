@@ -374,3 +374,60 @@ def test_density_oracle_pins():
     # Pauli matrices vs Kronecker products (independent construction)
     term = {0: "X", 2: "Y"}
     np.testing.assert_allclose(oracle.pauli_matrix(n, term), B.kron_list({0: B.PX, 2: B.PY}, n), atol=1e-15)
+
+
+# ----------------------------------------------------------------------------- sampling (NEXT-2)
+# "Sampling Measurement" (Fig. 1): or_sample is the plain inverse
+# CDF of |psi|^2 driven by the counter-based SplitMix64 uniforms of the sv_sample contract.
+
+SPLITMIX = json.load(open(os.path.join(GOLD, "splitmix64.json")))
+
+
+def test_splitmix64_reference_outputs():
+    g = int(SPLITMIX["golden"], 16)
+    for k, ref in enumerate(SPLITMIX["stream_from_state_0"]):
+        assert oracle.splitmix64((k * g) % (1 << 64)) == int(ref, 16)
+
+
+def test_sample_spec_examples():
+    """|0> -> all 0; |+> -> count of 0 within 5 sigma of 50000 at 1e5 shots; Bell state
+    -> only 00 and 11 appear (zero-probability outcomes are never drawn)."""
+    zero = oracle.zero_state(1)
+    assert np.all(oracle.sample(zero, [0], 100, seed=1) == 0)
+    plus = np.array([1, 1], dtype=np.complex128) / np.sqrt(2)
+    ones = int(np.sum(oracle.sample(plus, [0], 100000, seed=2)))
+    assert abs(ones - 50000) < 5 * np.sqrt(100000 * 0.25)
+    bell = np.array([1, 0, 0, 1], dtype=np.complex128) / np.sqrt(2)
+    assert set(np.unique(oracle.sample(bell, [0, 1], 10000, seed=3)).tolist()) == {0, 3}
+
+
+def test_sample_worked_draws():
+    """Hand-worked: probabilities (1/4, 0, 3/4, 0). With seed 0 the uniforms are the published
+    SplitMix64 outputs / 2^64 (u_0 = 0xe220a8397b1dcdaf >> 11 / 2^53 = 0.8833...): a draw lands on
+    index 0 iff u <= 1/4, else on index 2; indices 1 and 3 (probability 0) never appear."""
+    psi = np.array([0.5, 0, np.sqrt(0.75), 0], dtype=np.complex128)
+    g = int(SPLITMIX["golden"], 16)
+    # seed = k * golden makes shot 0 of each call the k-th published output
+    for k, ref in enumerate(SPLITMIX["stream_from_state_0"]):
+        u = (int(ref, 16) >> 11) / 2.0 ** 53
+        idx = oracle.sample_indices(psi, 1, seed=(k * g) % (1 << 64))[0]
+        assert idx == (0 if u * 1.0 <= 0.25 else 2), (k, u, idx)
+    idx = oracle.sample_indices(psi, 20000, seed=5)
+    assert set(np.unique(idx).tolist()) <= {0, 2}
+    assert abs(np.mean(idx == 0) - 0.25) < 5 * np.sqrt(0.25 * 0.75 / 20000)
+
+
+def test_sample_frequencies_match_probabilities():
+    """Empirical frequencies of 2e5 shots on a random 4-qubit state match |psi_i|^2 (every outcome
+    within 5 sigma); the marginal over a qubit subset is the bits of the full draw."""
+    psi = W.random_state(4, 77)
+    p = np.abs(psi) ** 2
+    shots = 200000
+    idx = oracle.sample_indices(psi, shots, seed=11)
+    freq = np.bincount(idx, minlength=16) / shots
+    assert np.all(np.abs(freq - p) < 5 * np.sqrt(p * (1 - p) / shots) + 1e-12)
+    sub = oracle.sample(psi, [3, 1], shots, seed=11)
+    assert np.array_equal(sub, ((idx >> 3) & 1) | (((idx >> 1) & 1) << 1))
+    # deterministic under the seed, different under another seed
+    assert np.array_equal(idx, oracle.sample_indices(psi, shots, seed=11))
+    assert not np.array_equal(idx, oracle.sample_indices(psi, shots, seed=12))

@@ -329,6 +329,25 @@ def config(name: str) -> Workload:
     raise KeyError(name)
 
 
+def fullsize_case(name: str) -> Workload:
+    """Full-size oracle parity cases (tests/golden/fullsize_<name>.npz, tools/gen_golden_fullsize.py):
+    C3 / C3dc as benched; the C4 generator at 26q full depth; C4 itself truncated to its first 4
+    layers (30q, 178 gates); the C4g generator at 26q."""
+    if name in ("C3", "C3dc"):
+        return config(name)
+    if name == "C4_26":
+        w = random_circuit(26, 40, seed=3040)
+        w.ham = jw_hamiltonian(26, 50, 3030)
+        return w
+    if name == "C4_30d4":
+        w = config("C4")
+        w.gates = w.gates[: 2 * (30 + 15 + 30 + 14)]  # layers 0..3 (even: 15 CZ, odd: 14 CZ)
+        return w
+    if name == "C4g_26":
+        return hea(26, 2, seed=3030)
+    raise KeyError(name)
+
+
 # ----------------------------------------------------------------------------- neutral arrays
 
 def gate_arrays(gates: Sequence[Gate]) -> dict:
