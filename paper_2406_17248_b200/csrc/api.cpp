@@ -418,9 +418,14 @@ bool pauli_groups_all_tiled(const sv_state_s* h, const PauliGroups& G) {
 // Tiled evaluation of all Pauli groups: groups whose x-masks fit together in one 2^k tile (low
 // qubits + the x bits) share one pass (k_pauli_tile). Writes one partial slot (grid doubles) per
 // pass; *nslots receives the pass count. lam (optional) receives H psi.
-int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
-               int* nslots, const float* psi32) {
-  const int nl = h->n_local;
+// Plans the tiled Pauli passes of a Hamiltonian (k_pauli_tile): groups whose x-masks fit one 2^k tile
+// together (with the low qubits) share a pass. E only (lam == nullptr) emits one entry per
+// off-diagonal term and one diagonal entry; lambda passes one entry per x-group. Passes are first
+// minimised in number (greedy, widest x-masks first), then rebalanced by evaluation cost at that
+// pass count. The tile's register positions (9..11) get the three qubits that hit most off-diagonal
+// entries' x-masks (their pair-symmetric representatives then vary in registers, not threads).
+static void plan_pauli_passes(const PauliGroups& G, int nl, bool e_only, std::vector<PauliPassDesc>* passes,
+                              std::vector<uint64_t>* z_all, std::vector<double>* c_all, std::vector<int>* wide) {
   const int k = pauli_k(nl);
   const int L = std::min(3, k);
   const uint64_t lowmask = (1ull << L) - 1;
@@ -429,69 +434,213 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
     return __builtin_popcountll(G.xs[x]) > __builtin_popcountll(G.xs[y]);
   });
-  std::vector<PauliPassDesc> passes;
-  std::vector<uint64_t> z_all;
-  std::vector<double> c_all;
-  std::vector<int> remaining, wide;  // wide: x-mask does not fit a tile -> per-group pair kernel
+  std::vector<int> fit;  // groups that fit a tile
   for (int gi : order) {
-    if (__builtin_popcountll(lowmask | G.xs[gi]) <= k) remaining.push_back(gi);
-    else wide.push_back(gi);
+    if (__builtin_popcountll(lowmask | G.xs[gi]) <= k) fit.push_back(gi);
+    else wide->push_back(gi);
   }
-  while (!remaining.empty()) {
+  auto entries = [&](int gi) { return (e_only && G.xs[gi] != 0) ? G.end[gi] - G.begin[gi] : 1; };
+  // evaluation cost per element (units ~ one pair-symmetric off-diagonal term in E-only mode)
+  auto cost = [&](int gi) {
+    const int nt = G.end[gi] - G.begin[gi];
+    if (G.xs[gi] == 0) return 1.0 + 0.08 * nt;  // measured: the 20-term diagonal group ~ 2.5 off-diagonal terms
+    return e_only ? (double)nt : 1.0 + 0.25 * (nt - 1);
+  };
+  auto partition = [&](double cap) {
+    std::vector<std::vector<int>> out;
+    std::vector<int> remaining = fit;
+    while (!remaining.empty()) {
+      uint64_t T = lowmask;
+      std::vector<int> taken, rest;
+      int ne = 0, nterms = 0;
+      double c = 0.0;
+      for (int gi : remaining) {
+        const int nt = G.end[gi] - G.begin[gi];
+        const bool first = taken.empty();
+        if (ne + entries(gi) <= 32 && __builtin_popcountll(T | G.xs[gi]) <= k && nterms + nt <= 1024 &&
+            (first || c + cost(gi) <= cap)) {
+          T |= G.xs[gi];
+          taken.push_back(gi);
+          ne += entries(gi);
+          nterms += nt;
+          c += cost(gi);
+        } else {
+          rest.push_back(gi);
+        }
+      }
+      out.push_back(taken);
+      remaining.swap(rest);
+    }
+    return out;
+  };
+  std::vector<std::vector<int>> parts = partition(1e300);
+  if (parts.size() > 1) {
+    double total = 0.0, mx = 0.0;
+    for (int gi : fit) { total += cost(gi); mx = std::max(mx, cost(gi)); }
+    const size_t P0 = parts.size();
+    for (double cap = std::max(mx, total / (double)P0); cap < total; cap *= 1.1) {
+      std::vector<std::vector<int>> q = partition(cap);
+      if (q.size() <= P0) { parts.swap(q); break; }
+    }
+  }
+  for (const std::vector<int>& taken : parts) {
     PauliPassDesc pp;
     std::memset(&pp, 0, sizeof(pp));
     uint64_t T = lowmask;
-    std::vector<int> taken, rest;
-    int nterms = 0;
-    for (int gi : remaining) {
-      const int nt = G.end[gi] - G.begin[gi];
-      if ((int)taken.size() < 32 && __builtin_popcountll(T | G.xs[gi]) <= k && nterms + nt <= 1024) {
-        T |= G.xs[gi];
-        taken.push_back(gi);
-        nterms += nt;
-      } else {
-        rest.push_back(gi);
-      }
-    }
+    for (int gi : taken) T |= G.xs[gi];
     for (int q = 0; q < nl && __builtin_popcountll(T) < k; ++q) T |= 1ull << q;
     pp.k = k;
-    int low = 0;
-    while (low < k && ((T >> low) & 1ull)) ++low;
-    pp.low = low;
+    // tile position order (k = 12, k_pauli_tile geometry): low qubits 0..2, two more lane qubits,
+    // the warp-bit qubits, the register qubits J (positions TB..11). An off-diagonal entry evaluates
+    // only one element of each pair (e, e^x) when x has a register or warp bit: J is the set hitting
+    // most entries, the lane qubits the pair leaving fewest entries with x inside the lanes.
+    constexpr int TB = kPauliTileTidBits;
+    constexpr int NJ = 12 - TB;
+    std::vector<int> others;
+    for (int q = L; q < nl; ++q)
+      if ((T >> q) & 1ull) others.push_back(q);
+    uint64_t J = 0, lanes = 0;
+    if (k == 12 && others.size() == 9) {
+      std::vector<uint64_t> xs;
+      std::vector<int> wt;
+      for (int gi : taken)
+        if (G.xs[gi] != 0) { xs.push_back(G.xs[gi] & ~lowmask); wt.push_back(entries(gi)); }
+      int best = -1;
+      for (uint32_t sub = 0; sub < (1u << 9); ++sub) {
+        if (__builtin_popcount(sub) != NJ) continue;
+        uint64_t cand = 0;
+        for (int i = 0; i < 9; ++i)
+          if ((sub >> i) & 1u) cand |= 1ull << others[i];
+        int hit = 0;
+        for (size_t e = 0; e < xs.size(); ++e)
+          if (xs[e] & cand) hit += wt[e];
+        if (hit > best) { best = hit; J = cand; }
+      }
+      int worst = 1 << 30;
+      for (size_t i0 = 0; i0 < 9; ++i0)
+        for (size_t i1 = i0 + 1; i1 < 9; ++i1) {
+          const uint64_t cand = (1ull << others[i0]) | (1ull << others[i1]);
+          if (cand & J) continue;
+          int slow = 0;
+          for (size_t e = 0; e < xs.size(); ++e)
+            if ((xs[e] & ~cand) == 0) slow += wt[e];
+          if (slow < worst) { worst = slow; lanes = cand; }
+        }
+    }
+    int p = 0;
+    for (int q = 0; q < L; ++q) pp.tq[p++] = (int8_t)q;
+    for (int q : others)
+      if ((lanes >> q) & 1ull) pp.tq[p++] = (int8_t)q;
+    for (int q : others)
+      if (!((J >> q) & 1ull) && !((lanes >> q) & 1ull)) pp.tq[p++] = (int8_t)q;
+    for (int q : others)
+      if ((J >> q) & 1ull) pp.tq[p++] = (int8_t)q;
     int pos_of[64];
-    for (int q = 0, p = 0; q < nl; ++q)
-      if ((T >> q) & 1ull) { pp.tq[p] = (int8_t)q; pos_of[q] = p++; }
-    pp.term_base = (int)z_all.size();
-    for (int gi : taken) {
-      const int g = pp.ngroups++;
-      pp.xphys[g] = G.xs[gi];
-      uint32_t xt = 0;
+    for (int i = 0; i < k; ++i) pos_of[(int)pp.tq[i]] = i;
+    int low = 0;
+    while (low < k && pp.tq[low] == low) ++low;
+    pp.low = low;
+    pp.diag_g = -1;
+    pp.term_base = (int)z_all->size();
+    auto tile_mask = [&](uint64_t m) {
+      uint32_t t = 0;
       for (int q = 0; q < nl; ++q)
-        if ((G.xs[gi] >> q) & 1ull) xt |= 1u << pos_of[q];
+        if (((m >> q) & 1ull) && ((T >> q) & 1ull)) t |= 1u << pos_of[q];
+      return t;
+    };
+    auto rule_of = [&](uint32_t xt) {
+      int rule = PR_ALL, wb = 5;
+      if (k == 12) {
+        for (int bb = NJ - 1; bb >= 0; --bb)
+          if ((xt >> (TB + bb)) & 1u) rule = bb;
+        if (rule == PR_ALL)
+          for (int bb = 5; bb < TB; ++bb)
+            if ((xt >> bb) & 1u) { rule = PR_WARP; wb = bb; break; }
+      }
+      return std::make_pair(rule, wb);
+    };
+    auto emit = [&](uint64_t x, const std::vector<int>& ts, int type) {
+      const int g = pp.ngroups++;
+      pp.xphys[g] = x;
+      const uint32_t xt = tile_mask(x);
       pp.xtile[g] = xt;
-      pp.tbeg[g] = (int)z_all.size() - pp.term_base;
+      const auto rw = rule_of(xt);
+      pp.gkind[g] = (uint8_t)(rw.first | (type << 3) | ((rw.second - 5) << 5));
+      pp.zt_reg[g] = ts.empty() ? 0u : tile_mask(G.z[ts[0]]) >> TB;
+      pp.tbeg[g] = (int)z_all->size() - pp.term_base;
+      for (int t : ts) {
+        z_all->push_back(G.z[t]);
+        c_all->push_back(G.c[2 * t]);
+        c_all->push_back(G.c[2 * t + 1]);
+      }
+      pp.tend[g] = (int)z_all->size() - pp.term_base;
+    };
+    auto single_type = [&](int t) { return G.c[2 * t + 1] != 0.0 ? PG_SINGLE_IM : PG_SINGLE_RE; };
+    auto sorted_terms = [&](int gi) {
       // terms ordered by the tile-position Z bits above the kernel's thread bits (k_pauli_tile sums
       // runs of equal element-part masks once)
       std::vector<int> ts;
       for (int t = G.begin[gi]; t < G.end[gi]; ++t) ts.push_back(t);
-      auto zhi = [&](int t) {
-        uint32_t zt = 0;
-        for (int q = 0; q < nl; ++q)
-          if (((G.z[t] >> q) & 1ull) && ((T >> q) & 1ull)) zt |= 1u << pos_of[q];
-        return zt >> 9;
-      };
-      std::stable_sort(ts.begin(), ts.end(), [&](int x, int y) { return zhi(x) < zhi(y); });
-      for (int t : ts) {
-        z_all.push_back(G.z[t]);
-        c_all.push_back(G.c[2 * t]);
-        c_all.push_back(G.c[2 * t + 1]);
+      std::stable_sort(ts.begin(), ts.end(), [&](int x, int y) { return (tile_mask(G.z[x]) >> TB) < (tile_mask(G.z[y]) >> TB); });
+      return ts;
+    };
+    if (e_only) {
+      // off-diagonal terms first, one entry each, sorted by class (representative rule, c' type):
+      // entry g is term g of the pass; the diagonal entry last
+      std::vector<std::pair<int, int>> ents;  // (class, term)
+      int diag_gi = -1;
+      for (int gi : taken) {
+        if (G.xs[gi] == 0) { diag_gi = gi; continue; }
+        const int r = rule_of(tile_mask(G.xs[gi])).first;
+        const int ci = (r < NJ ? r : (r == PR_WARP ? 3 : 4)) * 2;
+        for (int t : sorted_terms(gi)) ents.push_back({ci + (single_type(t) == PG_SINGLE_IM ? 1 : 0), t});
       }
-      pp.tend[g] = (int)z_all.size() - pp.term_base;
+      std::stable_sort(ents.begin(), ents.end(), [](const std::pair<int, int>& u, const std::pair<int, int>& v) { return u.first < v.first; });
+      for (int c = 0; c <= 10; ++c) {
+        int cnt = 0;
+        for (const auto& e : ents) cnt += e.first < c ? 1 : 0;
+        pp.cls_beg[c] = cnt;
+      }
+      for (const auto& e : ents) {
+        int gi = 0;
+        while (!(e.second >= G.begin[gi] && e.second < G.end[gi])) ++gi;
+        emit(G.xs[gi], {e.second}, single_type(e.second));
+      }
+      if (diag_gi >= 0) {
+        const std::vector<int> ts = sorted_terms(diag_gi);
+        emit(0, ts, PG_DIAG);
+        pp.diag_g = pp.ngroups - 1;
+        // the kernel walks the diagonal terms by their register-part z mask h (sorted)
+        const int rel0 = pp.tbeg[pp.ngroups - 1];
+        for (int hh = 0; hh <= 16; ++hh) {
+          int r = rel0;
+          for (int t : ts)
+            if ((int)(tile_mask(G.z[t]) >> TB) < hh) ++r;
+          pp.diag_rb[hh] = r;
+        }
+      }
+    } else {
+      for (int gi : taken) {
+        const std::vector<int> ts = sorted_terms(gi);
+        const uint64_t x = G.xs[gi];
+        if (x == 0) emit(x, ts, PG_DIAG);
+        else if (ts.size() == 1) emit(x, ts, single_type(ts[0]));
+        else emit(x, ts, PG_MULTI);
+      }
     }
-    pp.nterms = (int)z_all.size() - pp.term_base;
-    passes.push_back(pp);
-    remaining.swap(rest);
+    pp.nterms = (int)z_all->size() - pp.term_base;
+    passes->push_back(pp);
   }
+}
+
+int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
+               int* nslots, const float* psi32) {
+  const int nl = h->n_local;
+  std::vector<PauliPassDesc> passes;
+  std::vector<uint64_t> z_all;
+  std::vector<double> c_all;
+  std::vector<int> wide;  // wide: x-mask does not fit a tile -> per-group pair kernel
+  plan_pauli_passes(G, nl, lam == nullptr, &passes, &z_all, &c_all, &wide);
   // wide groups' terms follow the passes' terms
   std::vector<int> wide_base;
   for (int gi : wide) {

@@ -408,6 +408,33 @@ __global__ void __launch_bounds__(kThreads) k_pauli_cross(const double2* __restr
 // One CTA loads a tile of 2^k amplitudes whose qubit set contains the x-masks of up to 32 Pauli
 // groups; every element evaluates all those groups from the on-chip tile: one HBM read of psi (and
 // one write / read-modify-write of lambda) for many groups instead of one pass per group.
+//
+// Geometry of the main path (2^12 tiles, 256 threads x 16 elements: the per-tile and per-entry setup
+// of a thread is amortised over 16 elements; 8 warps per SM with 8 independent pairs each per term):
+// element e = tid + 256 j of the tile, j < 16 in registers. The host orders the tile: positions 0..2
+// = qubits 0..2 (128-byte HBM chunks; lanes on them read conflict-free 16-byte smem phases), 3..4
+// (the other lane bits) = the two qubits least used by x-masks, 5..7 warp bits, 8..11 the register
+// index j.
+//
+// Sign algebra (P = c i^{popc(x&z)} X^x Z^z, so (P psi)[e] = c' (-1)^{popc((e^x)&z)} psi[e^x]): per
+// tile the outer-bit part (-1)^{popc(base & z_out)} and (-1)^{popc(x & z)} are folded into the
+// coefficient (s_c); per element (-1)^{popc(e & z_tile)} = (-1)^{popc(tid & z)} (-1)^{popc(j & z_j)}:
+// the first factor is a per-thread bit computed once per kernel (esg / dsg masks), the second is bit
+// j of the term's Walsh row walsh16(z_j) (uniform across the CTA).
+//
+// E only (mode 0): the host emits one entry per off-diagonal TERM (c' = c i^{popc(x&z)} is real or
+// imaginary) plus one diagonal entry (all x = 0 terms). Off-diagonal entries use the Hermitian pair
+// symmetry: the pair (e, e^x) contributes 2 Re[conj(psi_e) c' s(e) psi_{e^x}], so only one element
+// of each pair (the "representative") is evaluated, and c' real / imaginary leaves one real product
+// Re(conj(a) b) or Im(conj(a) b) per representative: 3 FP64 instructions and one 16-byte shared
+// load per pair. Representatives: x has register bit JB -> the j with bit JB clear; x has warp bit
+// w -> the j whose bit 0 equals bit w of tid (warp-uniform, no divergence, 8 of the 16 per thread);
+// x inside the lane bits -> all elements without the factor 2. The diagonal entry uses |psi_j|^2,
+// its 16-point Walsh-Hadamard transform W, and per register-part mask h one product
+// (sum_t c_t (-1)^{popc(tid & z_t)}) * W[h].
+// lambda modes (1: lam = H_pass psi, 2: lam += H_pass psi, 3: lam += H_pass psi and E = Re<psi|lam>):
+// every element accumulates sum_g C_g(e) psi[e^x_g]; single-term groups with real / imaginary c'
+// take 2 FMAs per element.
 struct PauliTileArgs {
   int32_t k, low, n_outer, ngroups, nterms, mode;  // 0: E only; 1: lam = H_pass psi (+E); 2: lam += H_pass psi;
                                                    // 3: lam += H_pass psi, E = Re<psi|lam> (last tiled pass)
@@ -417,6 +444,13 @@ struct PauliTileArgs {
   uint64_t xphys[32];
   uint32_t xtile[32];
   int32_t tbeg[32], tend[32];
+  uint8_t gkind[32];    // bits 0-2: representative rule (PR_*); bits 3-4: PG_* type; bits 5-7: warp bit - 5
+  int32_t diag_rb[17];  // E only: the diagonal entry's terms with register-part z mask h are [rb[h], rb[h+1])
+  int32_t diag_g;       // E only: index of the diagonal entry (-1: none)
+  int32_t cls_beg[11];  // E only: off-diagonal entries sorted by class (rule * 2 + imaginary): [cls_beg[c], cls_beg[c+1])
+  uint32_t x16[32];     // E only: 16 * x_tile (byte-offset XOR of the partner element)
+  uint32_t wrow[32];    // E only: Walsh row of the entry's register-part z mask
+  uint64_t hsub[16];    // dep(i * 256 * PER): HBM offset of the copy / element index bits above the thread bits
   const uint64_t* z;
   const double2* c;
   double* partials;
@@ -425,141 +459,276 @@ struct PauliTileArgs {
 __device__ __forceinline__ double2 amp(double2 v) { return v; }
 __device__ __forceinline__ double2 amp(float2 v) { return make_double2((double)v.x, (double)v.y); }
 
-// Walsh row of a 4-bit mask h: bit j (j < 16) = parity(j & h).
-// k_pauli_tile geometry: 2^12-amplitude tiles, 512 threads (16 warps: the kernel is latency-bound
-// with one 8-warp CTA per SM), 8 elements per thread
-constexpr int kPauliThreads = 512, kPauliTidBits = 9;
+constexpr int kPauliThreads = 1 << kPauliTileTidBits, kPauliTidBits = kPauliTileTidBits, kPauliEPT = 4096 / kPauliThreads;
 
+// Walsh row of a 4-bit mask h: bit j (j < 16) = parity(j & h).
 __device__ __forceinline__ uint32_t walsh16(uint32_t h) {
   uint32_t r = 0;
-  if (h & 1u) r ^= 0xAAAAu;  // bit 0 of j
-  if (h & 2u) r ^= 0xCCCCu;  // bit 1
-  if (h & 4u) r ^= 0xF0F0u;  // bit 2
-  if (h & 8u) r ^= 0xFF00u;  // bit 3
+  if (h & 1u) r ^= 0xAAAAu;
+  if (h & 2u) r ^= 0xCCCCu;
+  if (h & 4u) r ^= 0xF0F0u;
+  if (h & 8u) r ^= 0xFF00u;
   return r;
+}
+
+__device__ __forceinline__ double flip(double v, uint32_t neg) {  // neg ? -v : v (sign-bit xor)
+  return __hiloint2double(__double2hiint(v) ^ (int)(neg << 31), __double2loint(v));
+}
+
+// Sum over the representatives j (bit JB of j == SEL; JB = 4: every j) of s_j Re(conj(v_j) p_j)
+// (IM: Im(conj(v_j) p_j)); p_j is the partner element (tid + 512 j) ^ x of the tile, at byte offset
+// q16 ^ (j * 16 * 512) with q16 = (16 tid) ^ (16 x); s_j = bit j of the Walsh row wr.
+template <int JB, int SEL, bool IM, typename T>
+__device__ __forceinline__ double pair_sum(const double2 (&v)[kPauliEPT], const char* __restrict__ tpb, uint32_t q16,
+                                           uint32_t wr) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int j = 0; j < kPauliEPT; ++j) {
+    if (JB < 4 && (((j >> JB) & 1) != SEL)) continue;
+    const double2 p = amp(*reinterpret_cast<const T*>(tpb + (q16 ^ ((uint32_t)j * (uint32_t)(sizeof(T) * kPauliThreads)))));
+    const double q = flip(IM ? fma(v[j].x, p.y, -v[j].y * p.x) : fma(v[j].x, p.x, v[j].y * p.y), (wr >> j) & 1u);
+    switch (j & 3) {
+      case 0: s0 += q; break;
+      case 1: s1 += q; break;
+      case 2: s2 += q; break;
+      default: s3 += q; break;
+    }
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+// The off-diagonal entries of one class [gb, ge) (compile-time representative rule and c' type).
+// Entry g's term is term g of the pass (E-only layout); its coefficient s_c[g] is tile-folded.
+template <int RULE, bool IM, typename T>
+__device__ __forceinline__ double entry_class(const PauliTileArgs& a, int gb, int ge, const double2 (&v)[kPauliEPT],
+                                              const char* __restrict__ tpb, const double2* __restrict__ s_c, uint32_t tid,
+                                              uint32_t esg) {
+  double acc = 0.0;
+  for (int g = gb; g < ge; ++g) {
+    const uint32_t q16 = (tid * (uint32_t)sizeof(T)) ^ (a.x16[g] >> (sizeof(T) == 16 ? 0 : 1));
+    const uint32_t wr = a.wrow[g];
+    const uint32_t nt = (esg >> g) & 1u;
+    double q;
+    if (RULE < 4) {
+      q = 2.0 * pair_sum<RULE, 0, IM, T>(v, tpb, q16, wr);
+    } else if (RULE == PR_WARP) {
+      const uint32_t sel = (tid >> (5 + (a.gkind[g] >> 5))) & 1u;
+      q = 2.0 * (sel ? pair_sum<0, 1, IM, T>(v, tpb, q16, wr) : pair_sum<0, 0, IM, T>(v, tpb, q16, wr));
+    } else {
+      q = pair_sum<4, 0, IM, T>(v, tpb, q16, wr);
+    }
+    // Re(c' q) = c'.x q (real c') or -c'.y q_im (imaginary c')
+    acc = fma(IM ? flip(s_c[g].y, nt ^ 1u) : flip(s_c[g].x, nt), q, acc);
+  }
+  return acc;
 }
 
 template <typename T>  // T: double2 (complex128 state) or float2 (complex64 state, E only)
 __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __restrict__ psi, double2* __restrict__ lam,
                                                          PauliTileArgs a) {
-  // Per tile the rank / outer-bit part of every term's sign is folded into its coefficient; per
-  // element only the tile bits remain: sign_t(e) = (-1)^{popc(e & zt_t)} with zt_t the term's Z
-  // support in tile-position space. Loops run term-outer / element-inner (EPT elements per thread
-  // in registers) so each term's data is read once per thread per tile and the element updates are
-  // independent (ILP).
-  constexpr int EPT = 4096 / kPauliThreads;  // elements per thread of a 2^12 tile
+  constexpr int EPT = kPauliEPT;
+  constexpr uint32_t PER = sizeof(T) == 16 ? 1u : 2u;  // elements per 16-byte copy
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
   T* tile_buf = reinterpret_cast<T*>(smem_raw);  // two tiles
-  double2* s_c = reinterpret_cast<double2*>(tile_buf + 2 * N);                         // folded coefficients (per tile)
-  uint64_t* s_z = reinterpret_cast<uint64_t*>(s_c + a.nterms);  // physical Z masks
-  uint32_t* s_zt = reinterpret_cast<uint32_t*>(s_z + a.nterms); // tile-position Z masks
+  double2* s_c = reinterpret_cast<double2*>(tile_buf + 2 * N);   // folded coefficients (per tile)
+  uint64_t* s_zo = reinterpret_cast<uint64_t*>(s_c + a.nterms);  // Z masks outside the tile (physical)
+  uint32_t* s_zt = reinterpret_cast<uint32_t*>(s_zo + a.nterms); // tile-position Z masks | fixed fold parity << 31
   const int nhi = 1 << (a.k - a.low);
   uint64_t* s_hi = reinterpret_cast<uint64_t*>(s_zt + ((a.nterms + 1) & ~1));
+  __shared__ uint64_t s_ob[4 * 64];  // tile base = OR of four 64-entry deposit tables over the outer qubits
   __shared__ double s_red[kPauliThreads / 32];
   uint64_t tmask = 0;
   for (int p = 0; p < a.k; ++p) tmask |= 1ull << a.tq[p];
-  for (int i = threadIdx.x; i < a.nterms; i += blockDim.x) {
-    const uint64_t z = a.z[i];
-    s_z[i] = z;
-    uint32_t zt = 0;
-    for (int p = 0; p < a.k; ++p)
-      if ((z >> a.tq[p]) & 1ull) zt |= 1u << p;
-    s_zt[i] = zt;
-  }
+  for (int g = 0; g < a.ngroups; ++g)
+    for (int i = a.tbeg[g] + (int)threadIdx.x; i < a.tend[g]; i += blockDim.x) {
+      const uint64_t z = a.z[i];
+      s_zo[i] = z & ~tmask;
+      uint32_t zt = 0;
+      for (int p = 0; p < a.k; ++p)
+        if ((z >> a.tq[p]) & 1ull) zt |= 1u << p;
+      // the tile-independent part of the coefficient's sign, (-1)^{popc(x_tile & z_tile)}
+      s_zt[i] = zt | ((uint32_t)(__popc(a.xtile[g] & zt) & 1) << 31);
+    }
   for (int h = threadIdx.x; h < nhi; h += blockDim.x) {
     uint64_t off = 0;
     for (int b = 0; b < a.k - a.low; ++b)
       if ((h >> b) & 1) off |= 1ull << a.tq[a.low + b];
     s_hi[h] = off;
   }
+  for (int h = threadIdx.x; h < 4 * 64; h += blockDim.x) {
+    uint64_t off = 0;
+    for (int b = 0; b < 6; ++b) {
+      const int j = (h >> 6) * 6 + b;
+      if (((h >> b) & 1) && j < a.n_outer) off |= 1ull << a.oq[j];
+    }
+    s_ob[h] = off;
+  }
+  const uint32_t tid = threadIdx.x;
   const uint32_t lowmask = (1u << a.low) - 1u;
   const int per_thread = (int)(N / blockDim.x);  // == EPT for 2^12-amplitude tiles, else smaller
+  const bool fast = per_thread == EPT;
+  // HBM offset of this thread's copies / elements within a tile (tile positions of the thread bits)
+  uint64_t dep_t = 0;
+  {
+    const uint32_t e0 = tid * PER;
+    for (int p = 0; p < a.k; ++p)
+      if ((e0 >> p) & 1u) dep_t |= 1ull << a.tq[p];
+  }
+  __syncthreads();
+  // per-thread sign bits (-1)^{popc(tid & z)}: first term of each entry (esg), the diagonal entry's
+  // terms (dsg, up to 64; the rest are evaluated per tile)
+  uint32_t esg = 0;
+  uint64_t dsg = 0;
+  for (int g = 0; g < a.ngroups; ++g) esg |= (uint32_t)(__popc(tid & s_zt[a.tbeg[g]] & 0x7fffffffu) & 1) << g;
+  if (a.diag_g >= 0)
+    for (int t = a.tbeg[a.diag_g]; t < a.tend[a.diag_g] && t - a.tbeg[a.diag_g] < 64; ++t)
+      dsg |= (uint64_t)(__popc(tid & s_zt[t] & 0x7fffffffu) & 1) << (t - a.tbeg[a.diag_g]);
   double acc = 0.0;
-  // double-buffered tiles: cp.async streams tile i + gridDim.x while tile i is evaluated
   auto tile_base = [&](int64_t tile) {
-    uint64_t base = 0;
-    for (int j = 0; j < a.n_outer; ++j)
+    uint64_t base = s_ob[tile & 63] | s_ob[64 + ((tile >> 6) & 63)] | s_ob[128 + ((tile >> 12) & 63)] |
+                    s_ob[192 + ((tile >> 18) & 63)];
+    for (int j = 24; j < a.n_outer; ++j)
       if ((tile >> j) & 1) base |= 1ull << a.oq[j];
     return base;
   };
   // 16-byte copies: one complex128 amplitude, or a complex64 pair (e, e + 1) — tile position 0 is
-  // qubit 0, so the pair is contiguous in HBM too
-  constexpr uint32_t PER = sizeof(T) == 16 ? 1u : 2u;
-  auto issue = [&](int64_t tile, T* dst) {
-    const uint64_t base = tile_base(tile);
-    for (uint32_t e = threadIdx.x * PER; e < N; e += blockDim.x * PER) {
-      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(psi + (base | (e & lowmask) | s_hi[e >> a.low]))
-                   : "memory");
+  // qubit 0, so the pair is contiguous in HBM too; double-buffered (cp.async streams tile i +
+  // gridDim.x while tile i is evaluated)
+  auto issue = [&](uint64_t base, T* dst) {
+    if (fast) {
+      const T* src = psi + (base | dep_t);
+#pragma unroll
+      for (int i = 0; i < EPT / (int)PER; ++i) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + tid * PER + (uint32_t)i * (kPauliThreads * PER));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + a.hsub[i]) : "memory");
+      }
+    } else {
+      for (uint32_t e = threadIdx.x * PER; e < N; e += blockDim.x * PER) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(psi + (base | (e & lowmask) | s_hi[e >> a.low]))
+                     : "memory");
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  __syncthreads();
-  if ((int64_t)blockIdx.x < a.ntiles) issue(blockIdx.x, tile_buf);
+  uint64_t base_next = (int64_t)blockIdx.x < a.ntiles ? tile_base(blockIdx.x) : 0;
+  if ((int64_t)blockIdx.x < a.ntiles) issue(base_next, tile_buf);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-    const uint64_t base = tile_base(tile);
+    const uint64_t base = base_next;
     T* tp = tile_buf + (size_t)(it & 1) * N;
-    __syncthreads();  // the other buffer's previous tile is fully consumed
+    __syncthreads();  // the other buffer's previous tile (and s_c) is fully consumed
     const int64_t next = tile + gridDim.x;
     const bool more = next < a.ntiles;
-    if (more) issue(next, tile_buf + (size_t)((it + 1) & 1) * N);
-    // fold (-1)^{popc((base ^ x) & z)} (outer part) and (-1)^{popc(xt & zt)} into the coefficients
-    for (int g = 0; g < a.ngroups; ++g)
-      for (int t = a.tbeg[g] + (int)threadIdx.x; t < a.tend[g]; t += blockDim.x) {
-        const uint64_t z = s_z[t];
-        const int par = (__popcll(base & z & ~tmask) + __popc(a.xtile[g] & s_zt[t])) & 1;
-        const double2 c = a.c[t];
-        s_c[t] = par ? make_double2(-c.x, -c.y) : c;
-      }
+    if (more) {
+      base_next = tile_base(next);
+      issue(base_next, tile_buf + (size_t)((it + 1) & 1) * N);
+    }
+    // fold (-1)^{popc(base & z_out)} (outer part) and (-1)^{popc(xt & zt)} into the coefficients
+    for (int t = (int)tid; t < a.nterms; t += blockDim.x) {
+      const uint32_t neg = ((uint32_t)__popcll(base & s_zo[t]) ^ (s_zt[t] >> 31)) & 1u;
+      const double2 c = a.c[t];
+      s_c[t] = make_double2(flip(c.x, neg), flip(c.y, neg));
+    }
     if (more) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
-    if (per_thread == EPT) {
-      // modes 2 / 3 (lambda += this pass' groups): the old lambda values are loaded first, so
-      // their HBM latency overlaps the group evaluation, and the sum is stored once
-      double2 l[EPT];
+    if (fast && a.mode == 0) {
+      // ---- E only: representatives of off-diagonal terms + the diagonal entry ----
+      double2 v[EPT];
 #pragma unroll
-      for (int j = 0; j < EPT; ++j) {
-        if (a.mode >= 2) {
-          const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
-          l[j] = lam[base | (e & lowmask) | s_hi[e >> a.low]];
-        } else {
-          l[j] = make_double2(0.0, 0.0);
+      for (int j = 0; j < EPT; ++j) v[j] = amp(tp[tid + (uint32_t)j * kPauliThreads]);
+      if (a.diag_g >= 0) {
+        // diagonal terms: Walsh transform of |psi_j|^2 over j; the terms with z_j = h give
+        // (sum_t c_t (-1)^{popc(tid & z_t)}) * W[h]
+        const int tb = a.tbeg[a.diag_g];
+        double W[EPT];
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) W[j] = fma(v[j].x, v[j].x, v[j].y * v[j].y);
+#pragma unroll
+        for (int h = 1; h < EPT; h <<= 1)
+#pragma unroll
+          for (int j = 0; j < EPT; ++j)
+            if (!(j & h)) {
+              const double x0 = W[j], x1 = W[j | h];
+              W[j] = x0 + x1;
+              W[j | h] = x0 - x1;
+            }
+#pragma unroll
+        for (int h = 0; h < EPT; ++h) {
+          int t = a.diag_rb[h];
+          const int te = a.diag_rb[h + 1];
+          if (t == te) continue;
+          double S0 = 0.0, S1 = 0.0;
+          for (; t + 1 < te; t += 2) {
+            const uint32_t r = (uint32_t)(t - tb);
+            const uint32_t n0 = r < 64 ? (uint32_t)(dsg >> r) & 1u : __popc(tid & s_zt[t]) & 1u;
+            const uint32_t n1 = r + 1 < 64 ? (uint32_t)(dsg >> (r + 1)) & 1u : __popc(tid & s_zt[t + 1]) & 1u;
+            S0 += flip(s_c[t].x, n0);  // x = 0: c' = c real
+            S1 += flip(s_c[t + 1].x, n1);
+          }
+          if (t < te) {
+            const uint32_t r = (uint32_t)(t - tb);
+            S0 += flip(s_c[t].x, r < 64 ? (uint32_t)(dsg >> r) & 1u : __popc(tid & s_zt[t]) & 1u);
+          }
+          acc = fma(S0 + S1, W[h], acc);
         }
       }
-      // e = tid + kPauliThreads j: the sign (-1)^{popc(e & zt)} factors into a per-thread part
-      // (-1)^{popc(tid & zt)}, folded into the coefficient once per term, and a j part read from
-      // the term's Walsh row W(zt >> tid bits) (bit j = parity(j & (zt >> tid bits))). A single-term
-      // group needs no accumulation at all: its j sign goes onto the product.
-      const uint32_t tid = threadIdx.x;
+      const char* tpb = reinterpret_cast<const char*>(tp);
+      acc += entry_class<0, false, T>(a, a.cls_beg[0], a.cls_beg[1], v, tpb, s_c, tid, esg);
+      acc += entry_class<0, true, T>(a, a.cls_beg[1], a.cls_beg[2], v, tpb, s_c, tid, esg);
+      acc += entry_class<1, false, T>(a, a.cls_beg[2], a.cls_beg[3], v, tpb, s_c, tid, esg);
+      acc += entry_class<1, true, T>(a, a.cls_beg[3], a.cls_beg[4], v, tpb, s_c, tid, esg);
+      acc += entry_class<2, false, T>(a, a.cls_beg[4], a.cls_beg[5], v, tpb, s_c, tid, esg);
+      acc += entry_class<2, true, T>(a, a.cls_beg[5], a.cls_beg[6], v, tpb, s_c, tid, esg);
+      acc += entry_class<PR_WARP, false, T>(a, a.cls_beg[6], a.cls_beg[7], v, tpb, s_c, tid, esg);
+      acc += entry_class<PR_WARP, true, T>(a, a.cls_beg[7], a.cls_beg[8], v, tpb, s_c, tid, esg);
+      acc += entry_class<PR_ALL, false, T>(a, a.cls_beg[8], a.cls_beg[9], v, tpb, s_c, tid, esg);
+      acc += entry_class<PR_ALL, true, T>(a, a.cls_beg[9], a.cls_beg[10], v, tpb, s_c, tid, esg);
+    } else if (fast) {
+      // ---- lambda modes: every element accumulates sum_g C_g(e) psi[e ^ x_g] ----
+      // modes 2 / 3 (lambda += this pass' groups): the old lambda values are loaded first, so
+      // their HBM latency overlaps the group evaluation, and the sum is stored once
+      const double2* lsrc = lam + (base | dep_t);
+      double2 l[EPT];
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) l[j] = a.mode >= 2 ? lsrc[a.hsub[j]] : make_double2(0.0, 0.0);
       for (int g = 0; g < a.ngroups; ++g) {
+        const uint32_t gk = a.gkind[g];
         const uint32_t xt = a.xtile[g];
         const int tb = a.tbeg[g], te = a.tend[g];
-        if (te - tb == 1) {
-          const uint32_t zt = s_zt[tb];
-          double2 c = s_c[tb];
-          if (__popc(tid & zt & (uint32_t)(kPauliThreads - 1)) & 1) c = make_double2(-c.x, -c.y);
+        const uint32_t pb = tid ^ (xt & (kPauliThreads - 1u)), xj = xt >> kPauliTidBits;
+        const uint32_t type = (gk >> 3) & 3u;
+        if (type <= PG_SINGLE_IM) {
+          // one term, c' real (l += w s_j p) or imaginary (l += i w s_j p)
+          const uint32_t zt = s_zt[tb] & 0x7fffffffu;
           const uint32_t wr = walsh16(zt >> kPauliTidBits);
+          const bool im = type == PG_SINGLE_IM;
+          const double w = flip(im ? s_c[tb].y : s_c[tb].x, (esg >> g) & 1u);
 #pragma unroll
           for (int j = 0; j < EPT; ++j) {
-            const double2 w = cmul(c, amp(tp[(tid + (uint32_t)j * (uint32_t)kPauliThreads) ^ xt]));
-            const bool neg = (wr >> j) & 1u;
-            l[j].x += neg ? -w.x : w.x;
-            l[j].y += neg ? -w.y : w.y;
+            const double2 p = amp(tp[pb + (((uint32_t)j ^ xj) << kPauliTidBits)]);
+            const double ws = flip(w, (wr >> j) & 1u);
+            if (im) {
+              l[j].x = fma(-ws, p.y, l[j].x);
+              l[j].y = fma(ws, p.x, l[j].y);
+            } else {
+              l[j].x = fma(ws, p.x, l[j].x);
+              l[j].y = fma(ws, p.y, l[j].y);
+            }
           }
           continue;
         }
-        // the host sorts a group's terms by their element-part mask zh = zt >> tid bits: a run of
-        // equal zh is summed once (per-thread signs folded), then spread over the 8 elements
-        // with compile-time Walsh signs (one switch per run instead of per-element selects)
+        // several terms (or the diagonal group): the host sorts a group's terms by their
+        // element-part mask zh = zt >> tid bits; a run of equal zh is summed once (per-thread signs
+        // folded), then spread over the elements with compile-time Walsh signs
         double2 C[EPT];
 #pragma unroll
         for (int j = 0; j < EPT; ++j) C[j] = make_double2(0.0, 0.0);
         double2 S = make_double2(0.0, 0.0);
-        uint32_t cur = s_zt[tb] >> kPauliTidBits;
-        auto flush = [&](uint32_t zh) {
+        uint32_t cur = (s_zt[tb] & 0x7fffffffu) >> kPauliTidBits;
+        auto spread = [&](uint32_t zh) {
 #define SV_SPREAD(H)                                                  \
   case H:                                                             \
     _Pragma("unroll") for (int j = 0; j < EPT; ++j) {                 \
@@ -567,47 +736,52 @@ __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __rest
       else { C[j].x += S.x; C[j].y += S.y; }                           \
     }                                                                 \
     break;
-          switch (zh & 7u) {
+          switch (zh & 15u) {
             SV_SPREAD(0) SV_SPREAD(1) SV_SPREAD(2) SV_SPREAD(3) SV_SPREAD(4) SV_SPREAD(5) SV_SPREAD(6) SV_SPREAD(7)
+            SV_SPREAD(8) SV_SPREAD(9) SV_SPREAD(10) SV_SPREAD(11) SV_SPREAD(12) SV_SPREAD(13) SV_SPREAD(14) SV_SPREAD(15)
           }
 #undef SV_SPREAD
         };
         for (int t = tb; t < te; ++t) {
-          const uint32_t zt = s_zt[t];
+          const uint32_t zt = s_zt[t] & 0x7fffffffu;
           const uint32_t zh = zt >> kPauliTidBits;
           if (zh != cur) {
-            flush(cur);
+            spread(cur);
             S = make_double2(0.0, 0.0);
             cur = zh;
           }
           const double2 c = s_c[t];
-          if (__popc(tid & zt & (uint32_t)(kPauliThreads - 1)) & 1) { S.x -= c.x; S.y -= c.y; }
-          else { S.x += c.x; S.y += c.y; }
+          const uint32_t neg = __popc(tid & zt) & 1u;
+          S.x += flip(c.x, neg);
+          S.y += flip(c.y, neg);
         }
-        flush(cur);
+        spread(cur);
+        if (type == PG_DIAG) {  // the partner is the element itself
 #pragma unroll
-        for (int j = 0; j < EPT; ++j) {
-          const double2 w = cmul(C[j], amp(tp[(tid + (uint32_t)j * (uint32_t)kPauliThreads) ^ xt]));
-          l[j].x += w.x;
-          l[j].y += w.y;
+          for (int j = 0; j < EPT; ++j) l[j] = cfma(C[j], amp(tp[tid + (uint32_t)j * kPauliThreads]), l[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) l[j] = cfma(C[j], amp(tp[pb + (((uint32_t)j ^ xj) << kPauliTidBits)]), l[j]);
         }
       }
+      double2* ldst = lam + (base | dep_t);
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
-        const uint32_t e = threadIdx.x + (uint32_t)j * blockDim.x;
-        if (a.mode != 2) acc += re_conj_mul(amp(tp[e]), l[j]);  // mode 3: Re<psi|lambda> of all passes so far
-        if (a.mode != 0) lam[base | (e & lowmask) | s_hi[e >> a.low]] = l[j];
+        if (a.mode != 2) acc += re_conj_mul(amp(tp[tid + (uint32_t)j * kPauliThreads]), l[j]);  // mode 3: Re<psi|lambda> of all passes so far
+        ldst[a.hsub[j]] = l[j];
       }
     } else {
+      // small tiles (n < 12): one element at a time, every term of every group (mode 0 entries
+      // are single terms here as well; no pair symmetry)
       for (uint32_t e = threadIdx.x; e < N; e += blockDim.x) {
         double2 l = make_double2(0.0, 0.0);
         for (int g = 0; g < a.ngroups; ++g) {
           double2 C = make_double2(0.0, 0.0);
           for (int t = a.tbeg[g]; t < a.tend[g]; ++t) {
-            const bool neg = __popc(e & s_zt[t]) & 1;
+            const uint32_t neg = __popc(e & s_zt[t] & 0x7fffffffu) & 1u;
             const double2 c = s_c[t];
-            C.x += neg ? -c.x : c.x;
-            C.y += neg ? -c.y : c.y;
+            C.x += flip(c.x, neg);
+            C.y += flip(c.y, neg);
           }
           const double2 w = cmul(C, amp(tp[e ^ a.xtile[g]]));
           l.x += w.x;
@@ -938,6 +1112,27 @@ static cudaError_t pauli_tile_impl(const void* psi, bool c64, double* lam, int m
     a.xtile[g] = pp.xtile[g];
     a.tbeg[g] = pp.tbeg[g];
     a.tend[g] = pp.tend[g];
+    a.gkind[g] = pp.gkind[g];
+  }
+  for (int h = 0; h < 17; ++h) a.diag_rb[h] = pp.diag_rb[h];
+  a.diag_g = pp.diag_g;
+  for (int c = 0; c < 11; ++c) a.cls_beg[c] = pp.cls_beg[c];
+  for (int g = 0; g < pp.ngroups; ++g) {
+    a.x16[g] = pp.xtile[g] * 16u;
+    uint32_t h = 0;
+    for (int j = 0; j < 16; ++j)
+      if (__builtin_popcount((uint32_t)j & (pp.zt_reg[g])) & 1) h |= 1u << j;
+    a.wrow[g] = h;
+  }
+  {
+    const uint32_t per = c64 ? 2u : 1u;
+    for (int i = 0; i < 16; ++i) {
+      const uint32_t e = (uint32_t)i * kPauliThreads * per;
+      uint64_t off = 0;
+      for (int p = 0; p < pp.k; ++p)
+        if ((e >> p) & 1u) off |= 1ull << pp.tq[p];
+      a.hsub[i] = off;
+    }
   }
   a.z = d_z + pp.term_base;
   a.c = reinterpret_cast<const double2*>(d_c) + pp.term_base;

@@ -298,7 +298,20 @@ struct PauliPassDesc {
   uint64_t xphys[32];
   uint32_t xtile[32];
   int32_t tbeg[32], tend[32];  // relative to term_base
+  uint8_t gkind[32];           // bits 0-2: representative rule (PR_*); bits 3-4: PG_* type; bits 5-7: warp bit - 5
+  int32_t diag_rb[17];         // E only: diagonal entry terms with register-part z mask h: [rb[h], rb[h+1])
+  int32_t diag_g;              // E only: index of the diagonal entry, -1 none
+  int32_t cls_beg[11];         // E only: off-diagonal entries sorted by class rule * 2 + (c' imaginary)
+  uint32_t zt_reg[32];         // register-part (tile positions >= kPauliTileTidBits) z mask of entry g's first term
 };
+// Pauli pass entry types ((PauliPassDesc::gkind >> 2) & 3): one term with c' = c i^{popc(x&z)} real /
+// imaginary, several terms sharing x (lambda modes), the diagonal group (x = 0)
+enum { PG_SINGLE_RE = 0, PG_SINGLE_IM = 1, PG_MULTI = 2, PG_DIAG = 3 };
+// Representative rule of an E-only off-diagonal entry (gkind & 7), tile geometry of k_pauli_tile:
+// element e = tid + 512 j (tid = tile positions 0..8: lanes 0..4, warps 5..8; j = positions 9..11).
+// Rules 0..3: register bit JB of x; PR_WARP: a warp bit of x; PR_ALL: x inside the lane bits.
+enum { PR_WARP = 4, PR_ALL = 5 };
+constexpr int kPauliTileTidBits = 9;  // k_pauli_tile's E-only entry classes assume 3 register bits
 int pauli_tile_grid(int n_local, int k);
 cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_local, const PauliPassDesc& pp,
                               const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s);
