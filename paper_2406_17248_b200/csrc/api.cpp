@@ -443,7 +443,7 @@ static void plan_pauli_passes(const PauliGroups& G, int nl, bool e_only, std::ve
   // evaluation cost per element (units ~ one pair-symmetric off-diagonal term in E-only mode)
   auto cost = [&](int gi) {
     const int nt = G.end[gi] - G.begin[gi];
-    if (G.xs[gi] == 0) return 1.0 + 0.08 * nt;  // measured: the 20-term diagonal group ~ 2.5 off-diagonal terms
+    if (G.xs[gi] == 0) return 1.0 + 0.28 * nt;  // measured: the 20-term diagonal group ~ 6.5 off-diagonal terms
     return e_only ? (double)nt : 1.0 + 0.25 * (nt - 1);
   };
   auto partition = [&](double cap) {
@@ -605,6 +605,10 @@ static void plan_pauli_passes(const PauliGroups& G, int nl, bool e_only, std::ve
         int gi = 0;
         while (!(e.second >= G.begin[gi] && e.second < G.end[gi])) ++gi;
         emit(G.xs[gi], {e.second}, single_type(e.second));
+        if (e.first < 8) {  // pair-symmetric rule: each representative stands for its pair (factor 2)
+          (*c_all)[c_all->size() - 2] *= 2.0;
+          (*c_all)[c_all->size() - 1] *= 2.0;
+        }
       }
       if (diag_gi >= 0) {
         const std::vector<int> ts = sorted_terms(diag_gi);

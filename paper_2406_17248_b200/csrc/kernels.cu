@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_cross(const double2* __restr
 // Sign algebra (P = c i^{popc(x&z)} X^x Z^z, so (P psi)[e] = c' (-1)^{popc((e^x)&z)} psi[e^x]): per
 // tile the outer-bit part (-1)^{popc(base & z_out)} and (-1)^{popc(x & z)} are folded into the
 // coefficient (s_c); per element (-1)^{popc(e & z_tile)} = (-1)^{popc(tid & z)} (-1)^{popc(j & z_j)}:
-// the first factor is a per-thread bit computed once per kernel (esg / dsg masks), the second is bit
+// the first factor is a per-thread bit (computed once per kernel for each entry's first term), the second is bit
 // j of the term's Walsh row walsh16(z_j) (uniform across the CTA).
 //
 // E only (mode 0): the host emits one entry per off-diagonal TERM (c' = c i^{popc(x&z)} is real or
@@ -481,20 +481,18 @@ __device__ __forceinline__ double flip(double v, uint32_t neg) {  // neg ? -v : 
 template <int JB, int SEL, bool IM, typename T>
 __device__ __forceinline__ double pair_sum(const double2 (&v)[kPauliEPT], const char* __restrict__ tpb, uint32_t q16,
                                            uint32_t wr) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  double s[4];
+  int n = 0;
 #pragma unroll
   for (int j = 0; j < kPauliEPT; ++j) {
     if (JB < 4 && (((j >> JB) & 1) != SEL)) continue;
     const double2 p = amp(*reinterpret_cast<const T*>(tpb + (q16 ^ ((uint32_t)j * (uint32_t)(sizeof(T) * kPauliThreads)))));
     const double q = flip(IM ? fma(v[j].x, p.y, -v[j].y * p.x) : fma(v[j].x, p.x, v[j].y * p.y), (wr >> j) & 1u);
-    switch (j & 3) {
-      case 0: s0 += q; break;
-      case 1: s1 += q; break;
-      case 2: s2 += q; break;
-      default: s3 += q; break;
-    }
+    if (n < 4) s[n] = q;  // four independent chains, started from the first products
+    else s[n & 3] += q;
+    ++n;
   }
-  return (s0 + s1) + (s2 + s3);
+  return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
 // The off-diagonal entries of one class [gb, ge) (compile-time representative rule and c' type).
@@ -508,12 +506,13 @@ __device__ __forceinline__ double entry_class(const PauliTileArgs& a, int gb, in
     const uint32_t q16 = (tid * (uint32_t)sizeof(T)) ^ (a.x16[g] >> (sizeof(T) == 16 ? 0 : 1));
     const uint32_t wr = a.wrow[g];
     const uint32_t nt = (esg >> g) & 1u;
+    // the factor 2 of the pair-symmetric rules (representatives only) is in the host's coefficient
     double q;
     if (RULE < 4) {
-      q = 2.0 * pair_sum<RULE, 0, IM, T>(v, tpb, q16, wr);
+      q = pair_sum<RULE, 0, IM, T>(v, tpb, q16, wr);
     } else if (RULE == PR_WARP) {
       const uint32_t sel = (tid >> (5 + (a.gkind[g] >> 5))) & 1u;
-      q = 2.0 * (sel ? pair_sum<0, 1, IM, T>(v, tpb, q16, wr) : pair_sum<0, 0, IM, T>(v, tpb, q16, wr));
+      q = sel ? pair_sum<0, 1, IM, T>(v, tpb, q16, wr) : pair_sum<0, 0, IM, T>(v, tpb, q16, wr);
     } else {
       q = pair_sum<4, 0, IM, T>(v, tpb, q16, wr);
     }
@@ -576,14 +575,9 @@ __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __rest
       if ((e0 >> p) & 1u) dep_t |= 1ull << a.tq[p];
   }
   __syncthreads();
-  // per-thread sign bits (-1)^{popc(tid & z)}: first term of each entry (esg), the diagonal entry's
-  // terms (dsg, up to 64; the rest are evaluated per tile)
+  // per-thread sign bits (-1)^{popc(tid & z)} of the first term of each entry
   uint32_t esg = 0;
-  uint64_t dsg = 0;
   for (int g = 0; g < a.ngroups; ++g) esg |= (uint32_t)(__popc(tid & s_zt[a.tbeg[g]] & 0x7fffffffu) & 1) << g;
-  if (a.diag_g >= 0)
-    for (int t = a.tbeg[a.diag_g]; t < a.tend[a.diag_g] && t - a.tbeg[a.diag_g] < 64; ++t)
-      dsg |= (uint64_t)(__popc(tid & s_zt[t] & 0x7fffffffu) & 1) << (t - a.tbeg[a.diag_g]);
   double acc = 0.0;
   auto tile_base = [&](int64_t tile) {
     uint64_t base = s_ob[tile & 63] | s_ob[64 + ((tile >> 6) & 63)] | s_ob[128 + ((tile >> 12) & 63)] |
@@ -642,7 +636,6 @@ __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __rest
       if (a.diag_g >= 0) {
         // diagonal terms: Walsh transform of |psi_j|^2 over j; the terms with z_j = h give
         // (sum_t c_t (-1)^{popc(tid & z_t)}) * W[h]
-        const int tb = a.tbeg[a.diag_g];
         double W[EPT];
 #pragma unroll
         for (int j = 0; j < EPT; ++j) W[j] = fma(v[j].x, v[j].x, v[j].y * v[j].y);
@@ -660,19 +653,9 @@ __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __rest
           int t = a.diag_rb[h];
           const int te = a.diag_rb[h + 1];
           if (t == te) continue;
-          double S0 = 0.0, S1 = 0.0;
-          for (; t + 1 < te; t += 2) {
-            const uint32_t r = (uint32_t)(t - tb);
-            const uint32_t n0 = r < 64 ? (uint32_t)(dsg >> r) & 1u : __popc(tid & s_zt[t]) & 1u;
-            const uint32_t n1 = r + 1 < 64 ? (uint32_t)(dsg >> (r + 1)) & 1u : __popc(tid & s_zt[t + 1]) & 1u;
-            S0 += flip(s_c[t].x, n0);  // x = 0: c' = c real
-            S1 += flip(s_c[t + 1].x, n1);
-          }
-          if (t < te) {
-            const uint32_t r = (uint32_t)(t - tb);
-            S0 += flip(s_c[t].x, r < 64 ? (uint32_t)(dsg >> r) & 1u : __popc(tid & s_zt[t]) & 1u);
-          }
-          acc = fma(S0 + S1, W[h], acc);
+          double S = 0.0;
+          for (; t < te; ++t) S += flip(s_c[t].x, __popc(tid & s_zt[t]) & 1u);  // x = 0: c' = c real
+          acc = fma(S, W[h], acc);
         }
       }
       const char* tpb = reinterpret_cast<const char*>(tp);
@@ -1137,7 +1120,7 @@ static cudaError_t pauli_tile_impl(const void* psi, bool c64, double* lam, int m
   a.z = d_z + pp.term_base;
   a.c = reinterpret_cast<const double2*>(d_c) + pp.term_base;
   a.partials = d_partials;
-  const size_t smem = (size_t(c64 ? 16 : 32) << pp.k) + (size_t)pp.nterms * 28 + 8 + (size_t(8) << (pp.k - pp.low));
+  size_t smem = (size_t(c64 ? 16 : 32) << pp.k) + (size_t)pp.nterms * 28 + 8 + (size_t(8) << (pp.k - pp.low));
   static std::atomic<uint64_t> attr{0};
   {
     cudaError_t e = once_per_device(attr, [] {
