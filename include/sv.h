@@ -113,6 +113,10 @@ typedef struct {
   int64_t exchanges;             /* sharded: global<->local qubit swaps                           */
   double algorithmic_bytes;      /* HBM bytes the executed plan must move   */
   int64_t gates_applied;         /* gates of the user's circuits applied (forward only)           */
+  double exchange_bytes;         /* sharded: bytes this handle sent to peers in qubit swaps and
+                                    cross-shard Pauli streams (each direction counted once)      */
+  double exchange_ms;            /* sharded: device time of those exchanges (CUDA events around each
+                                    exchange on the handle's stream; summed at sv_get_stats)      */
 } sv_stats;
 
 /* Option keys for sv_set_option (A/B evidence; defaults are the tuned values). */

@@ -41,11 +41,12 @@ class sv_pauli(ctypes.Structure):
     _fields_ = [("x_mask", ctypes.c_uint64), ("z_mask", ctypes.c_uint64), ("coeff", ctypes.c_double)]
 
 
-class sv_stats(ctypes.Structure):
+class sv_stats(ctypes.Structure):  # include/sv.h
     _fields_ = [("kernel_launches", ctypes.c_int64), ("gate_passes", ctypes.c_int64),
                 ("adjoint_passes", ctypes.c_int64), ("expectation_passes", ctypes.c_int64),
                 ("exchanges", ctypes.c_int64), ("algorithmic_bytes", ctypes.c_double),
-                ("gates_applied", ctypes.c_int64)]
+                ("gates_applied", ctypes.c_int64), ("exchange_bytes", ctypes.c_double),
+                ("exchange_ms", ctypes.c_double)]
 
 
 class sv_pass_info(ctypes.Structure):

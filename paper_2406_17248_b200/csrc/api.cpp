@@ -638,7 +638,7 @@ static void plan_pauli_passes(const PauliGroups& G, int nl, bool e_only, std::ve
 }
 
 int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
-               int* nslots, const float* psi32) {
+               int* nslots, const float* psi32, bool lam_accumulate) {
   const int nl = h->n_local;
   std::vector<PauliPassDesc> passes;
   std::vector<uint64_t> z_all;
@@ -680,7 +680,7 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
   for (size_t p = 0; p < passes.size(); ++p, ++slot) {
     // lambda passes: the first writes (and gives its E), later ones accumulate; the last tiled
     // pass reports E = Re<psi|lambda> over all tiled groups (earlier accumulating passes report 0)
-    const int mode = lam == nullptr ? 0 : (slot == 0 ? 1 : (p + 1 == passes.size() ? 3 : 2));
+    const int mode = lam == nullptr ? 0 : lam_accumulate ? 2 : (slot == 0 ? 1 : (p + 1 == passes.size() ? 3 : 2));
     if (mode == 3) {  // its partial supersedes the first pass' one
       e = cudaMemsetAsync(d_partials, 0, (size_t)grid * 8, h->stream);
       if (e != cudaSuccess) return cuda_fail(h, e, "partials");
@@ -697,7 +697,7 @@ int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* l
     const int gi = wide[w];
     const int nt = G.end[gi] - G.begin[gi];
     // the pair kernel writes lambda when it is the first launch, else accumulates
-    e = launch_pauli_group(psi, lam, slot > 0, nl, G.xs[gi], dz + wide_base[w], dc + 2 * wide_base[w], nt,
+    e = launch_pauli_group(psi, lam, lam_accumulate || slot > 0, nl, G.xs[gi], dz + wide_base[w], dc + 2 * wide_base[w], nt,
                            d_partials + (size_t)slot * grid, std::min(grid, pauli_grid(nl)), h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "pauli group launch");
     if (pauli_grid(nl) < grid) {  // zero the unused tail of this slot (fixed-width reduction)
@@ -827,6 +827,11 @@ sv_status sv_destroy(sv_handle h) {
   h->work_lam.release();
   h->work_r.release();
   release_plan_cache(h);
+  for (auto& pr : h->xev) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  h->xev.clear();
   h->d_ops.release();
   h->d_mats.release();
   h->d_terms.release();
@@ -1269,12 +1274,28 @@ extern "C" {
 
 sv_status sv_get_stats(sv_handle h, sv_stats* out) {
   if (!h || !out) return fail(SV_E_ARG, "null argument");
+  DeviceGuard dev_guard(h->device);
+  for (auto& pr : h->xev) {  // exchange device time: events recorded around each exchange
+    float ms = 0.0f;
+    if (cudaEventSynchronize(pr.second) == cudaSuccess && cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess)
+      h->stats.exchange_ms += (double)ms;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  h->xev.clear();
   *out = h->stats;
   return SV_OK;
 }
 
 sv_status sv_reset_stats(sv_handle h) {
   if (!h) return fail(SV_E_ARG, "null argument");
+  DeviceGuard dev_guard(h->device);
+  for (auto& pr : h->xev) {
+    cudaEventSynchronize(pr.second);
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  h->xev.clear();
   std::memset(&h->stats, 0, sizeof(h->stats));
   return SV_OK;
 }

@@ -372,35 +372,40 @@ __global__ void __launch_bounds__(kThreads) k_pauli_group(const double2* __restr
 }
 
 
-// Cross-shard Pauli group (sharding, x-mask wider than a shard): E partials of
-// sum_i conj(psi[i]) C(i) partner[i ^ xl], C(i) = sum_j c_j (-1)^{popc((i ^ xl) & z_j)}; the
-// partner's rank-bit signs are folded into c_j by the host. lam (optional) += C(i) partner[i ^ xl].
+// Cross-shard Pauli group (sharding, x-mask wider than a shard), one streamed CHUNK of the partner
+// shard: partner[j - off] holds the partner's amplitudes j in [off, off + cnt) (cnt a power of two,
+// off a multiple of cnt); this kernel adds the E partials of
+//   sum_j conj(psi[j ^ xl]) C(j ^ xl) partner[j],  C(i) = sum_t c_t (-1)^{popc((i ^ xl) & z_t)},
+// the partner's rank-bit signs folded into c_t by the host (so only a chunk-sized buffer is needed:
+// a 34-qubit state on 2 GPUs leaves no room for a whole second shard). lam (optional) += C(i)
+// partner[j] at i = j ^ xl. Partials accumulate into partials[blockIdx.x] across chunks (same grid).
 __global__ void __launch_bounds__(kThreads) k_pauli_cross(const double2* __restrict__ psi,
                                                           const double2* __restrict__ partner, double2* __restrict__ lam,
-                                                          int n, uint64_t xl, const uint64_t* __restrict__ z,
-                                                          const double2* __restrict__ c, int nterms,
-                                                          double* __restrict__ partials) {
+                                                          int64_t off, int64_t cnt, uint64_t xl,
+                                                          const uint64_t* __restrict__ z, const double2* __restrict__ c,
+                                                          int nterms, double* __restrict__ partials, int first) {
   __shared__ uint64_t s_z[256];
   __shared__ double2 s_c[256];
   __shared__ double s_red[kThreads / 32];
   for (int i = threadIdx.x; i < nterms; i += blockDim.x) { s_z[i] = z[i]; s_c[i] = c[i]; }
   __syncthreads();
-  const int64_t N = 1ll << n, stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
-    const uint64_t ip = (uint64_t)i ^ xl;
+  for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < cnt; jj += stride) {
+    const uint64_t j = (uint64_t)(off + jj);
+    const uint64_t i = j ^ xl;
     double2 C = make_double2(0.0, 0.0);
-    for (int j = 0; j < nterms; ++j) {
-      const double sg = (__popcll(ip & s_z[j]) & 1) ? -1.0 : 1.0;
-      C.x = fma(sg, s_c[j].x, C.x);
-      C.y = fma(sg, s_c[j].y, C.y);
+    for (int t = 0; t < nterms; ++t) {
+      const double sg = (__popcll(j & s_z[t]) & 1) ? -1.0 : 1.0;
+      C.x = fma(sg, s_c[t].x, C.x);
+      C.y = fma(sg, s_c[t].y, C.y);
     }
-    const double2 w = cmul(C, partner[ip]);
+    const double2 w = cmul(C, partner[jj]);
     acc += re_conj_mul(psi[i], w);
     if (lam) { double2 l = lam[i]; l.x += w.x; l.y += w.y; lam[i] = l; }
   }
   acc = block_sum(acc, s_red);
-  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  if (threadIdx.x == 0) partials[blockIdx.x] = first ? acc : partials[blockIdx.x] + acc;
 }
 
 
@@ -875,6 +880,17 @@ __global__ void __launch_bounds__(kThreads) k_dm_trace(const double2* __restrict
 }
 
 // out[s] = sum_{j < per} partials[s*per + j], fixed order (strided per-thread sums, then a fixed tree).
+// Re<a|b> over n amplitudes: per-CTA partials (fixed order; reduced by k_reduce_slots).
+__global__ void __launch_bounds__(kThreads) k_redot(const double2* __restrict__ x, const double2* __restrict__ y, int64_t n,
+                                                    double* __restrict__ partials) {
+  __shared__ double s_red[kThreads / 32];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += re_conj_mul(x[i], y[i]);
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
 __global__ void __launch_bounds__(kThreads) k_reduce_slots(const double* __restrict__ partials, int per,
                                                            double* __restrict__ out) {
   __shared__ double s_red[kThreads / 32];
@@ -1021,6 +1037,11 @@ cudaError_t launch_pauli_group(const double* psi, double* lam, bool lam_accumula
   return cudaGetLastError();
 }
 
+cudaError_t launch_redot(const double* x, const double* y, int64_t n, double* d_partials, int grid, cudaStream_t s) {
+  k_redot<<<grid, kThreads, 0, s>>>(reinterpret_cast<const double2*>(x), reinterpret_cast<const double2*>(y), n, d_partials);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out, cudaStream_t s) {
   if (n_slots <= 0) return cudaSuccess;
   k_reduce_slots<<<n_slots, kThreads, 0, s>>>(d_partials, per_slot, d_out);
@@ -1059,12 +1080,12 @@ cudaError_t launch_pack_half(double* shard, double* buf, int l, int h, int64_t o
   return cudaGetLastError();
 }
 
-cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int n_local, uint64_t xl,
-                               const uint64_t* d_z, const double* d_c, int nterms, double* d_partials, int grid,
-                               cudaStream_t s) {
+cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int64_t off, int64_t cnt,
+                               uint64_t xl, const uint64_t* d_z, const double* d_c, int nterms, double* d_partials,
+                               int grid, bool first, cudaStream_t s) {
   k_pauli_cross<<<grid, kThreads, 0, s>>>(reinterpret_cast<const double2*>(psi), reinterpret_cast<const double2*>(partner),
-                                          reinterpret_cast<double2*>(lam), n_local, xl, d_z,
-                                          reinterpret_cast<const double2*>(d_c), nterms, d_partials);
+                                          reinterpret_cast<double2*>(lam), off, cnt, xl, d_z,
+                                          reinterpret_cast<const double2*>(d_c), nterms, d_partials, first ? 1 : 0);
   return cudaGetLastError();
 }
 

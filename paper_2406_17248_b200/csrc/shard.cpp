@@ -40,7 +40,13 @@ struct ShardState {
   std::vector<DevBuf> wpsi, wlam;  // gradient workspaces per held shard
   std::vector<int> perm;        // logical qubit -> physical position (the state's layout)
   ncclComm_t comm = nullptr;
-  DevBuf sendb, recvb, scalar;  // NCCL bounce buffers, all-reduce scratch
+  DevBuf scalar;                // all-reduce scratch
+  // pipelined exchanges: two bounce buffers per direction (this side; the partner side only for the
+  // virtual-shard emulation of the NCCL transport), a transfer stream, per-buffer events
+  DevBuf sendb[2], recvb[2], psend[2], precv[2];
+  cudaStream_t xstream = nullptr;
+  cudaEvent_t ev_pack[2] = {nullptr, nullptr}, ev_comm[2] = {nullptr, nullptr}, ev_unpack[2] = {nullptr, nullptr};
+  DevBuf eacc;                  // sharded expectation: one device double per evaluation unit
 };
 
 namespace {
@@ -232,39 +238,130 @@ uint64_t permute_mask(uint64_t m, const std::vector<int>& perm) {
 
 // ---- transports ----
 
+// Exchange timing: events around each exchange on the handle's stream (summed at sv_get_stats).
+struct XTimer {
+  sv_state_s* h;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  explicit XTimer(sv_state_s* hh) : h(hh) {
+    if (cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess) cudaEventRecord(e0, h->stream);
+    else { if (e0) cudaEventDestroy(e0); e0 = e1 = nullptr; }
+  }
+  ~XTimer() {
+    if (!e0) return;
+    cudaEventRecord(e1, h->stream);
+    h->xev.push_back({e0, e1});
+  }
+};
+
+int ensure_xstream(sv_state_s* h) {
+  ShardState& S = *h->shard;
+  if (S.xstream) return SV_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&S.xstream, cudaStreamNonBlocking);
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    e = cudaEventCreateWithFlags(&S.ev_pack[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&S.ev_comm[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&S.ev_unpack[b], cudaEventDisableTiming);
+  }
+  return e == cudaSuccess ? SV_OK : cuda_fail(h, e, "exchange stream");
+}
+
+// One side of a pairwise half-shard exchange: the shard, the half it sends (local bit L == hsend;
+// the received half lands in the same positions) and its two send / receive bounce buffers.
+struct XSide {
+  double* shard;
+  int hsend;
+  double* sendb[2];
+  double* recvb[2];
+};
+
+// Pipelined chunked exchange (SURVEY §8(e) "pairwise half-shard exchange ... chunked through a
+// bounce buffer"): chunk i is packed on the handle's stream, moved by `comm(b, cnt)` on the transfer
+// stream (NCCL grouped send/recv, or device copies between virtual shards), and unpacked on the
+// handle's stream; with two buffers per direction pack(i+1) and unpack(i-1) run while chunk i is in
+// flight. Events order buffer reuse: comm(i) waits pack(i) and unpack(i-2); unpack(i) waits comm(i).
+template <class Comm>
+int exchange_pipelined(sv_state_s* h, XSide* sides, int nsides, int L, int64_t half, int64_t chunk, Comm comm) {
+  ShardState& S = *h->shard;
+  int rc = ensure_xstream(h);
+  if (rc) return rc;
+  const int64_t nch = (half + chunk - 1) / chunk;
+  cudaError_t e = cudaSuccess;
+  for (int64_t i = 0; i <= nch && e == cudaSuccess; ++i) {
+    if (i < nch) {
+      const int b = (int)(i & 1);
+      const int64_t off = i * chunk, cnt = std::min(chunk, half - off);
+      // pack(i) reuses sendb[b] after comm(i-2): ordered, unpack(i-2) (earlier on this stream) waited for it
+      for (int sd = 0; sd < nsides && e == cudaSuccess; ++sd)
+        e = launch_pack_half(sides[sd].shard, sides[sd].sendb[b], L, sides[sd].hsend, off, cnt, true, h->stream);
+      if (e == cudaSuccess) e = cudaEventRecord(S.ev_pack[b], h->stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(S.xstream, S.ev_pack[b], 0);
+      if (e == cudaSuccess && i >= 2) e = cudaStreamWaitEvent(S.xstream, S.ev_unpack[b], 0);  // recvb[b] free
+      if (e == cudaSuccess) {
+        const int crc = comm(b, cnt);
+        if (crc) return crc;
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(S.ev_comm[b], S.xstream);
+      h->stats.kernel_launches += nsides;
+    }
+    if (i >= 1 && e == cudaSuccess) {
+      const int64_t j = i - 1;
+      const int b = (int)(j & 1);
+      const int64_t off = j * chunk, cnt = std::min(chunk, half - off);
+      e = cudaStreamWaitEvent(h->stream, S.ev_comm[b], 0);
+      for (int sd = 0; sd < nsides && e == cudaSuccess; ++sd)
+        e = launch_pack_half(sides[sd].shard, sides[sd].recvb[b], L, sides[sd].hsend, off, cnt, false, h->stream);
+      if (e == cudaSuccess) e = cudaEventRecord(S.ev_unpack[b], h->stream);
+      h->stats.kernel_launches += nsides;
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(h, e, "pipelined exchange");
+  return SV_OK;
+}
+
 // Swap physical positions G (global) and L (local) of the vectors `vecs` (per held shard).
 int swap_qubits(sv_state_s* h, const std::vector<std::vector<double*>>& vecs, int G, int L) {
   ShardState& S = *h->shard;
   const int nl = h->n_local;
   const int j = G - nl;
   h->stats.exchanges += 1;
-  // SV_VIRTUAL_BOUNCE=<chunk amplitudes>: virtual shards exchange through the NCCL path's
-  // pack / bounce-buffer / unpack sequence (device copies instead of ncclSend/ncclRecv), chunked,
-  // so the tests exercise that code on one GPU.
+  XTimer timer(h);
+  const int64_t half = int64_t(1) << (nl - 1);
+  // SV_VIRTUAL_BOUNCE=<chunk amplitudes>: virtual shards exchange through the NCCL transport's
+  // pipelined pack / bounce-buffer / unpack sequence, with device copies on the transfer stream in
+  // place of ncclSend / ncclRecv, so the tests exercise that code (and its event ordering) on one GPU.
   const char* bounce_env = std::getenv("SV_VIRTUAL_BOUNCE");
   const int64_t bounce_chunk = bounce_env ? std::max<int64_t>(1, std::atoll(bounce_env)) : 0;
   if (S.virt && bounce_chunk > 0) {
-    const int64_t half = int64_t(1) << (nl - 1);
     const int64_t chunk = std::min(half, bounce_chunk);
-    if (!S.sendb.ensure((size_t)chunk * 16) || !S.recvb.ensure((size_t)chunk * 16)) return fail(SV_E_OOM, "bounce buffers");
+    for (int b = 0; b < 2; ++b)
+      if (!S.sendb[b].ensure((size_t)chunk * 16) || !S.recvb[b].ensure((size_t)chunk * 16) ||
+          !S.psend[b].ensure((size_t)chunk * 16) || !S.precv[b].ensure((size_t)chunk * 16))
+        return fail(SV_E_OOM, "bounce buffers");
     for (const auto& v : vecs) {
       for (size_t a = 0; a < S.ranks.size(); ++a) {
         const int r = S.ranks[a];
         if ((r >> j) & 1) continue;
         const size_t p = (size_t)(r | (1 << j));
-        for (int64_t off = 0; off < half; off += chunk) {
-          const int64_t cnt = std::min(chunk, half - off);
-          // r packs its half with bit L = 1, p its half with bit L = 0; each unpacks the other's
-          cudaError_t e = launch_pack_half(v[a], static_cast<double*>(S.sendb.p), L, 1, off, cnt, true, h->stream);
-          if (e == cudaSuccess) e = launch_pack_half(v[p], static_cast<double*>(S.recvb.p), L, 0, off, cnt, true, h->stream);
-          if (e == cudaSuccess) e = launch_pack_half(v[a], static_cast<double*>(S.recvb.p), L, 1, off, cnt, false, h->stream);
-          if (e == cudaSuccess) e = launch_pack_half(v[p], static_cast<double*>(S.sendb.p), L, 0, off, cnt, false, h->stream);
-          if (e != cudaSuccess) return cuda_fail(h, e, "bounce exchange");
-          h->stats.kernel_launches += 4;
+        // r sends its half with bit L = 1, the partner p its half with bit L = 0
+        XSide sides[2] = {{v[a], 1, {}, {}}, {v[p], 0, {}, {}}};
+        for (int b = 0; b < 2; ++b) {
+          sides[0].sendb[b] = static_cast<double*>(S.sendb[b].p);
+          sides[0].recvb[b] = static_cast<double*>(S.recvb[b].p);
+          sides[1].sendb[b] = static_cast<double*>(S.psend[b].p);
+          sides[1].recvb[b] = static_cast<double*>(S.precv[b].p);
         }
+        int rc = exchange_pipelined(h, sides, 2, L, half, chunk, [&](int b, int64_t cnt) {
+          cudaError_t e = cudaMemcpyAsync(sides[1].recvb[b], sides[0].sendb[b], (size_t)cnt * 16, cudaMemcpyDeviceToDevice,
+                                          S.xstream);
+          if (e == cudaSuccess)
+            e = cudaMemcpyAsync(sides[0].recvb[b], sides[1].sendb[b], (size_t)cnt * 16, cudaMemcpyDeviceToDevice, S.xstream);
+          return e == cudaSuccess ? (int)SV_OK : cuda_fail(h, e, "bounce copy");
+        });
+        if (rc) return rc;
       }
     }
     h->stats.algorithmic_bytes += 32.0 * (double)(1ull << nl) * (double)S.ranks.size() * vecs.size() / 2.0;
+    h->stats.exchange_bytes += 16.0 * (double)half * (double)S.ranks.size() * vecs.size();
     return SV_OK;
   }
   if (S.virt) {
@@ -280,33 +377,33 @@ int swap_qubits(sv_state_s* h, const std::vector<std::vector<double*>>& vecs, in
       }
     }
     h->stats.algorithmic_bytes += 32.0 * (double)(1ull << nl) * (double)S.ranks.size() * vecs.size() / 2.0;
+    h->stats.exchange_bytes += 16.0 * (double)half * (double)S.ranks.size() * vecs.size();
     return SV_OK;
   }
   // NCCL: one held shard
   const int r = S.ranks[0];
   const int peer = r ^ (1 << j);
   const int h_send = ((r >> j) & 1) ? 0 : 1;  // send the half whose bit L differs from our bit j
-  const int64_t half = int64_t(1) << (nl - 1);
   const int64_t chunk = std::min(half, kChunkAmps);
-  if (!S.sendb.ensure((size_t)chunk * 16) || !S.recvb.ensure((size_t)chunk * 16)) return fail(SV_E_OOM, "bounce buffers");
+  for (int b = 0; b < 2; ++b)
+    if (!S.sendb[b].ensure((size_t)chunk * 16) || !S.recvb[b].ensure((size_t)chunk * 16))
+      return fail(SV_E_OOM, "bounce buffers");
   for (const auto& v : vecs) {
-    double* shard = v[0];
-    for (int64_t off = 0; off < half; off += chunk) {
-      const int64_t cnt = std::min(chunk, half - off);
-      cudaError_t e = launch_pack_half(shard, static_cast<double*>(S.sendb.p), L, h_send, off, cnt, true, h->stream);
-      if (e != cudaSuccess) return cuda_fail(h, e, "pack");
+    XSide side{v[0], h_send, {static_cast<double*>(S.sendb[0].p), static_cast<double*>(S.sendb[1].p)},
+               {static_cast<double*>(S.recvb[0].p), static_cast<double*>(S.recvb[1].p)}};
+    int rc = exchange_pipelined(h, &side, 1, L, half, chunk, [&](int b, int64_t cnt) {
       ncclResult_t nr = ncclGroupStart();
-      if (nr == ncclSuccess) nr = ncclSend(S.sendb.p, (size_t)cnt * 2, ncclDouble, peer, S.comm, h->stream);
-      if (nr == ncclSuccess) nr = ncclRecv(S.recvb.p, (size_t)cnt * 2, ncclDouble, peer, S.comm, h->stream);
+      if (nr == ncclSuccess) nr = ncclSend(side.sendb[b], (size_t)cnt * 2, ncclDouble, peer, S.comm, S.xstream);
+      if (nr == ncclSuccess) nr = ncclRecv(side.recvb[b], (size_t)cnt * 2, ncclDouble, peer, S.comm, S.xstream);
       ncclResult_t ne = ncclGroupEnd();
       if (nr != ncclSuccess) return nccl_fail(h, nr, "exchange");
       if (ne != ncclSuccess) return nccl_fail(h, ne, "exchange");
-      e = launch_pack_half(shard, static_cast<double*>(S.recvb.p), L, h_send, off, cnt, false, h->stream);
-      if (e != cudaSuccess) return cuda_fail(h, e, "unpack");
-      h->stats.kernel_launches += 2;
-    }
+      return (int)SV_OK;
+    });
+    if (rc) return rc;
   }
   h->stats.algorithmic_bytes += 32.0 * (double)half * vecs.size();
+  h->stats.exchange_bytes += 16.0 * (double)half * vecs.size();
   return SV_OK;
 }
 
@@ -402,8 +499,17 @@ void destroy_sharding(sv_state_s* h) {
   for (auto& b : S.bufs) b.release();
   for (auto& b : S.wpsi) b.release();
   for (auto& b : S.wlam) b.release();
-  S.sendb.release();
-  S.recvb.release();
+  for (int b = 0; b < 2; ++b) {
+    S.sendb[b].release();
+    S.recvb[b].release();
+    S.psend[b].release();
+    S.precv[b].release();
+    if (S.ev_pack[b]) cudaEventDestroy(S.ev_pack[b]);
+    if (S.ev_comm[b]) cudaEventDestroy(S.ev_comm[b]);
+    if (S.ev_unpack[b]) cudaEventDestroy(S.ev_unpack[b]);
+  }
+  if (S.xstream) cudaStreamDestroy(S.xstream);
+  S.eacc.release();
   S.scalar.release();
   if (S.comm) ncclCommDestroy(S.comm);
   delete h->shard;
@@ -502,26 +608,81 @@ int shard_apply(sv_state_s* h, const std::vector<BoundGate>& bg) {
   return SV_OK;
 }
 
-// Swaps global positions of the x-masks in `groups` to local ones (state perm updated), one group
-// at a time, then evaluates the group on every held shard. Returns the per-handle partial sum
-// (not yet all-reduced). lam (optional, per shard) receives H psi.
+// The listed logical groups in one shard's physical layout: x / z masks permuted to physical local
+// positions, the rank-bit part of every Z factor folded into the coefficient (rsig: the rank bits the
+// sign is read from — this shard's, or the partner's for a cross-shard group).
+static PauliGroups shard_groups(const PauliGroups& G, const std::vector<int>& sel, const std::vector<int>& perm, int nl,
+                                uint64_t rsig) {
+  PauliGroups out;
+  const uint64_t lmask = (1ull << nl) - 1;
+  for (int gi : sel) {
+    out.xs.push_back(permute_mask(G.xs[(size_t)gi], perm) & lmask);
+    out.begin.push_back((int)out.z.size());
+    for (int t = G.begin[(size_t)gi]; t < G.end[(size_t)gi]; ++t) {
+      const uint64_t zp = permute_mask(G.z[(size_t)t], perm);
+      const double sgn = (__builtin_popcountll((zp >> nl) & rsig) & 1) ? -1.0 : 1.0;
+      out.z.push_back(zp & lmask);
+      out.c.push_back(sgn * G.c[2 * (size_t)t]);
+      out.c.push_back(sgn * G.c[2 * (size_t)t + 1]);
+    }
+    out.end.push_back((int)out.z.size());
+  }
+  return out;
+}
+
+// Sharded <H> (and lambda = H psi): groups whose x-mask is local in the current layout are evaluated
+// together by the tiled multi-group passes on every held shard; a group with global x bits first
+// swaps them with local qubits (the state's layout perm is updated; `swaps` records them); a group
+// whose x-mask is wider than a shard streams the partner shard r ^ x_g in chunks (NCCL: 1 GiB
+// chunks through a bounce buffer; virtual shards: read in place) — no whole-shard copy, so a
+// 34-qubit state fits on 2 GPUs. Partials stay on the device until one read-back at the end.
+// Returns the per-handle E (not yet all-reduced). lam (optional, per shard) receives H psi and E is
+// then Re<psi|lam>.
 static int sharded_groups(sv_state_s* h, const PauliGroups& G, std::vector<int>& perm,
                           const std::vector<std::vector<double*>>& swap_vecs, const std::vector<double*>& psi,
                           const std::vector<double*>& lam, double* out_e, std::vector<std::pair<int, int>>* swaps) {
   ShardState& S = *h->shard;
   const int nl = h->n_local;
   const uint64_t lmask = (1ull << nl) - 1;
-  const int grid = pauli_grid(nl);
-  double E = 0.0;
-  if (!h->d_partials.ensure((size_t)grid * 8 + 8) || !h->d_out.ensure(64)) return fail(SV_E_OOM, "partials");
-  std::vector<bool> lam_started(psi.size(), false);
-  if (!lam.empty())
-    for (size_t a = 0; a < lam.size(); ++a) {
-      cudaError_t e = cudaMemsetAsync(lam[a], 0, size_t(16) << nl, h->stream);
-      if (e != cudaSuccess) return cuda_fail(h, e, "zero lambda");
+  const bool grad = !lam.empty();
+  const int grid_t = pauli_tile_grid(nl, pauli_k(nl)), grid_x = pauli_grid(nl);
+  const int grid_max = std::max(grid_t, grid_x);
+  const size_t max_units = (G.xs.size() + 2) * S.ranks.size() * 2 + 8;
+  if (!h->d_partials.ensure((G.xs.size() + 2) * (size_t)grid_max * 8 + 64) || !S.eacc.ensure(max_units * 8))
+    return fail(SV_E_OOM, "partials");
+  double* dp = static_cast<double*>(h->d_partials.p);
+  double* eacc = static_cast<double*>(S.eacc.p);
+  size_t units = 0;
+  cudaError_t e = cudaSuccess;
+  if (grad)
+    for (size_t a = 0; a < lam.size() && e == cudaSuccess; ++a) e = cudaMemsetAsync(lam[a], 0, size_t(16) << nl, h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "zero lambda");
+  auto eval_local = [&](const std::vector<int>& sel) -> int {
+    for (size_t a = 0; a < S.ranks.size(); ++a) {
+      const PauliGroups Gs = shard_groups(G, sel, perm, nl, (uint64_t)S.ranks[a]);
+      int ns = 0;
+      int rc = run_groups(h, Gs, psi[a], grad ? lam[a] : nullptr, dp, grid_t, &ns, nullptr, true);
+      if (rc) return rc;
+      if (!grad && ns > 0) {
+        if (units + (size_t)ns > max_units) return fail(SV_E_ARG, "internal: expectation units");
+        cudaError_t er = launch_reduce_slots(dp, ns, grid_t, eacc + units, h->stream);
+        if (er != cudaSuccess) return cuda_fail(h, er, "reduce");
+        units += (size_t)ns;
+        h->stats.kernel_launches += 1;
+      }
     }
-  for (size_t gi = 0; gi < G.xs.size(); ++gi) {
-    uint64_t xp = permute_mask(G.xs[gi], perm);
+    return SV_OK;
+  };
+  // 1. every group that is local in the current layout: one tiled evaluation per shard
+  std::vector<int> now, later;
+  for (size_t gi = 0; gi < G.xs.size(); ++gi) ((permute_mask(G.xs[gi], perm) >> nl) ? later : now).push_back((int)gi);
+  if (!now.empty()) {
+    int rc = eval_local(now);
+    if (rc) return rc;
+  }
+  // 2. groups with global x bits: swap them local where possible, else stream the partner shard
+  for (int gi : later) {
+    uint64_t xp = permute_mask(G.xs[(size_t)gi], perm);
     while (xp >> nl) {
       const int Gpos = 63 - __builtin_clzll(xp);
       int L = -1;
@@ -532,63 +693,82 @@ static int sharded_groups(sv_state_s* h, const PauliGroups& G, std::vector<int>&
       if (rc) return rc;
       do_swap_perm(perm, Gpos, L);
       if (swaps) swaps->push_back({Gpos, L});
-      xp = permute_mask(G.xs[gi], perm);
+      xp = permute_mask(G.xs[(size_t)gi], perm);
     }
     const uint64_t xg = xp >> nl;
+    if (xg == 0) {
+      int rc = eval_local({gi});
+      if (rc) return rc;
+      continue;
+    }
+    const uint64_t xl = xp & lmask;
+    const int64_t NL = int64_t(1) << nl, chunk = std::min<int64_t>(NL, kChunkAmps);
     for (size_t a = 0; a < S.ranks.size(); ++a) {
       const uint64_t r = (uint64_t)S.ranks[a];
-      std::vector<uint64_t> z;
-      std::vector<double> c;
-      const uint64_t rsig = xg ? (r ^ xg) : r;  // cross-shard: signs of the partner's rank bits
-      for (int t = G.begin[gi]; t < G.end[gi]; ++t) {
-        const uint64_t zp = permute_mask(G.z[t], perm);
-        const double sgn = (__builtin_popcountll((zp >> nl) & rsig) & 1) ? -1.0 : 1.0;
-        z.push_back(zp & lmask);
-        c.push_back(sgn * G.c[2 * t]);
-        c.push_back(sgn * G.c[2 * t + 1]);
+      const PauliGroups Gs = shard_groups(G, {gi}, perm, nl, r ^ xg);  // signs of the partner's rank bits
+      const int nt = (int)Gs.z.size();
+      const size_t zb = ((size_t)nt * 8 + 15) & ~size_t(15);
+      if (!h->d_terms.ensure(zb + (size_t)nt * 16 + 16)) return fail(SV_E_OOM, "terms");
+      if (h->terms_upload_done) {
+        e = cudaEventSynchronize(h->terms_upload_done);  // the term buffer is free again
+        if (e != cudaSuccess) return cuda_fail(h, e, "terms");
       }
-      const size_t zb = (z.size() * 8 + 15) & ~size_t(15);
-      if (!h->d_terms.ensure(zb + c.size() * 8 + 16)) return fail(SV_E_OOM, "terms");
-      h->h_stage.assign(zb + c.size() * 8, 0);
-      std::memcpy(h->h_stage.data(), z.data(), z.size() * 8);
-      std::memcpy(h->h_stage.data() + zb, c.data(), c.size() * 8);
-      cudaError_t e = cudaMemcpyAsync(h->d_terms.p, h->h_stage.data(), h->h_stage.size(), cudaMemcpyHostToDevice, h->stream);
+      h->h_stage.assign(zb + (size_t)nt * 16, 0);
+      std::memcpy(h->h_stage.data(), Gs.z.data(), (size_t)nt * 8);
+      std::memcpy(h->h_stage.data() + zb, Gs.c.data(), (size_t)nt * 16);
+      e = cudaMemcpyAsync(h->d_terms.p, h->h_stage.data(), h->h_stage.size(), cudaMemcpyHostToDevice, h->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // pageable staging
       if (e != cudaSuccess) return cuda_fail(h, e, "terms");
-      double* dp = static_cast<double*>(h->d_partials.p);
       const uint64_t* dz = static_cast<const uint64_t*>(h->d_terms.p);
       const double* dc = reinterpret_cast<const double*>(static_cast<const char*>(h->d_terms.p) + zb);
-      if (xg == 0) {
-        e = launch_pauli_group(psi[a], lam.empty() ? nullptr : lam[a], true, nl, xp, dz, dc, (int)z.size(), dp, grid,
-                               h->stream);
-      } else {
-        // partner shard r ^ xg: another virtual shard, or a full copy fetched over NCCL
+      if (!S.virt && (!S.recvb[0].ensure((size_t)chunk * 16))) return fail(SV_E_OOM, "partner chunk buffer");
+      const int peer = (int)(r ^ xg);
+      XTimer timer(h);
+      for (int64_t off = 0; off < NL; off += chunk) {
         const double* partner = nullptr;
         if (S.virt) {
-          partner = psi[(size_t)(r ^ xg)];
+          partner = psi[(size_t)peer] + 2 * off;
         } else {
-          const int peer = (int)(r ^ xg);
-          if (!S.recvb.ensure(size_t(16) << nl)) return fail(SV_E_OOM, "partner shard buffer");
+          // both ranks of the pair stream the same chunk index to each other (no pack: contiguous)
           ncclResult_t nr = ncclGroupStart();
-          if (nr == ncclSuccess) nr = ncclSend(psi[a], (size_t(2) << nl), ncclDouble, peer, S.comm, h->stream);
-          if (nr == ncclSuccess) nr = ncclRecv(S.recvb.p, (size_t(2) << nl), ncclDouble, peer, S.comm, h->stream);
+          if (nr == ncclSuccess) nr = ncclSend(psi[a] + 2 * off, (size_t)chunk * 2, ncclDouble, peer, S.comm, h->stream);
+          if (nr == ncclSuccess) nr = ncclRecv(S.recvb[0].p, (size_t)chunk * 2, ncclDouble, peer, S.comm, h->stream);
           ncclResult_t ne = ncclGroupEnd();
-          if (nr != ncclSuccess) return nccl_fail(h, nr, "partner exchange");
-          if (ne != ncclSuccess) return nccl_fail(h, ne, "partner exchange");
-          partner = static_cast<const double*>(S.recvb.p);
+          if (nr != ncclSuccess) return nccl_fail(h, nr, "partner stream");
+          if (ne != ncclSuccess) return nccl_fail(h, ne, "partner stream");
+          partner = static_cast<const double*>(S.recvb[0].p);
+          h->stats.exchange_bytes += 16.0 * (double)chunk;
         }
-        e = launch_pauli_cross(psi[a], partner, lam.empty() ? nullptr : lam[a], nl, xp & lmask, dz, dc, (int)z.size(), dp,
-                               grid, h->stream);
+        e = launch_pauli_cross(psi[a], partner, grad ? lam[a] : nullptr, off, chunk, xl, dz, dc, nt, dp, grid_x,
+                               off == 0, h->stream);
+        if (e != cudaSuccess) return cuda_fail(h, e, "cross-shard Pauli chunk");
+        h->stats.kernel_launches += 1;
       }
-      if (e == cudaSuccess) e = launch_reduce_slots(dp, 1, grid, static_cast<double*>(h->d_out.p), h->stream);
-      double v = 0;
-      if (e == cudaSuccess) e = cudaMemcpyAsync(&v, h->d_out.p, 8, cudaMemcpyDeviceToHost, h->stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-      if (e != cudaSuccess) return cuda_fail(h, e, "sharded expectation");
-      h->stats.kernel_launches += 2;
       h->stats.expectation_passes += 1;
-      E += v;
+      if (!grad) {
+        e = launch_reduce_slots(dp, 1, grid_x, eacc + units, h->stream);
+        if (e != cudaSuccess) return cuda_fail(h, e, "reduce");
+        ++units;
+        h->stats.kernel_launches += 1;
+      }
     }
   }
+  // 3. lambda mode: E = Re<psi|lambda> per shard (lambda holds every group's H psi)
+  if (grad)
+    for (size_t a = 0; a < S.ranks.size(); ++a) {
+      e = launch_redot(psi[a], lam[a], int64_t(1) << nl, dp, grid_x, h->stream);
+      if (e == cudaSuccess) e = launch_reduce_slots(dp, 1, grid_x, eacc + units, h->stream);
+      if (e != cudaSuccess) return cuda_fail(h, e, "Re<psi|lambda>");
+      ++units;
+      h->stats.kernel_launches += 2;
+    }
+  // one read-back; fixed-order sum
+  std::vector<double> ev(units);
+  if (units) e = cudaMemcpyAsync(ev.data(), eacc, units * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "sharded expectation");
+  double E = 0.0;
+  for (double v : ev) E += v;
   *out_e = E;
   return SV_OK;
 }

@@ -76,6 +76,7 @@ struct sv_state_s {
   int c64_split = 3;  // SV_OPT_C64_SPLIT
   sv_stats stats{};
   sv::ShardState* shard = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> xev;  // exchange timing (start, end) on the stream
 };
 
 namespace sv {
@@ -98,8 +99,10 @@ struct PauliGroups {
   std::vector<uint64_t> z;
   std::vector<double> c;              // complex coefficients c_t * i^{popc(x&z)} (re, im)
 };
+// psi32: complex64 state, E only, tiled groups only. lam_accumulate: every pass adds H_pass psi to
+// lam (no pass reports E; the caller computes Re<psi|lam> afterwards).
 int run_groups(sv_state_s* h, const PauliGroups& G, const double* psi, double* lam, double* d_partials, int grid,
-               int* nslots, const float* psi32 = nullptr);  // psi32: complex64 state, E only, tiled groups only
+               int* nslots, const float* psi32 = nullptr, bool lam_accumulate = false);
 bool pauli_groups_all_tiled(const sv_state_s* h, const PauliGroups& G);
 int pauli_k(int n_local);
 

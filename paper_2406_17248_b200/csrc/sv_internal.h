@@ -317,11 +317,15 @@ cudaError_t launch_pauli_tile(const double* psi, double* lam, int mode, int n_lo
                               const uint64_t* d_z, const double* d_c, double* d_partials, int grid, cudaStream_t s);
 cudaError_t launch_pauli_tile_c64(const float* psi, int n_local, const PauliPassDesc& pp, const uint64_t* d_z,
                                   const double* d_c, double* d_partials, int grid, cudaStream_t s);
-cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int n_local, uint64_t xl,
-                               const uint64_t* d_z, const double* d_c, int nterms, double* d_partials, int grid,
-                               cudaStream_t s);
+// One streamed chunk (partner amplitudes [off, off + cnt), cnt a power of two, off a multiple of
+// cnt) of a cross-shard Pauli group; partials accumulate over chunks (first: overwrite).
+cudaError_t launch_pauli_cross(const double* psi, const double* partner, double* lam, int64_t off, int64_t cnt,
+                               uint64_t xl, const uint64_t* d_z, const double* d_c, int nterms, double* d_partials,
+                               int grid, bool first, cudaStream_t s);
 cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out,
                                 cudaStream_t s);
+// Re<x|y> per-CTA partials (grid of them)
+cudaError_t launch_redot(const double* x, const double* y, int64_t n, double* d_partials, int grid, cudaStream_t s);
 
 // Batch mode (kernels_batch.cu): one CTA per parameter row, whole state in shared memory.
 struct BatchOp {
