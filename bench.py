@@ -14,10 +14,14 @@ C-ABI with host buffers, clocks during the timed region.
 --impl reference: the CPU oracle (oracle/, test infrastructure) timed on the host cores on a
 bounded sample of the same workload (the tier's reference arm).
 
-Multi-GPU (torchrun, N>1): the state is sharded over the N GPUs by its top log2(N) qubits (NCCL
-exchanges over NVLink, all-reduced expectation). Weak scaling: n = 30 + log2(N) qubits (2^30
-amplitudes per GPU), value in 30q-equivalent gates/s (gates x 2^(n-30) / s). `--virtual-shards P`
-runs the same sharded executor with P shards on one GPU. See DESIGN.md §7.
+Multi-GPU (N>1): BASELINE.json configs[4] "C5", a 34-qubit random circuit (depth 40, seed 3440)
++ 50-term JW <H>, sharded over the N GPUs by its top log2(N) qubits (pipelined NCCL half-shard
+exchanges over NVLink, chunked cross-shard Pauli streams, one all-reduce). The total problem is
+fixed (strong scaling); value = 30q-equivalent gates/s (gates x 2^(n-30) / s, equal to gates/s at
+30 qubits) so the per-GPU rate compares with N=1's C4. `python bench.py --gpus N` without a torchrun
+environment re-launches itself under torch.distributed.run with N ranks and fails loudly when the
+box has fewer than N GPUs. `--virtual-shards P` runs the sharded executor with P shards on one GPU
+(weak scaling, 30 + log2 P qubits). See DESIGN.md §7.
 """
 from __future__ import annotations
 
@@ -36,13 +40,23 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP64_PEAK_TFLOPS = 36.9  # measured FP64 tensor (DMMA) peak = DMMA+DFMA mixed peak on this pool's B200
+FP64_PEAK_PATH = os.path.join(ROOT, "profiles", "fp64_peak.json")  # tools/measure_fp64_peak.py (committed)
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md; 900 GB/s nominal)
 TF32_SPLIT_PEAK_TFLOPS = 277.3 / 3  # measured mma.sync TF32 peak / 3 products (complex64 dense stages)
 # dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
 # --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
 TRAFFIC_PER_LAUNCH = {"C4": (17.181665 + 17.543235) * 1e9}  # profiles/r01_ncu_pass30_full.txt (k_pass_dense)
 TRAFFIC_PER_LAUNCH_C64 = (8.614921 + 8.540025) * 1e9  # profiles/r01_ncu_c64_pass30_full.txt (k_pass_c64)
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+
+
+def _fp64_peak():
+    """The measured FP64 peak (DMMA / DFMA / mixed, best) with its clock record."""
+    with open(FP64_PEAK_PATH) as f:
+        d = json.load(f)
+    return float(d["peak_tflops"]), (f"measured {d['when']} on this pool's B200 at {d['sm_mhz_median_under_load']:.0f} MHz "
+                                     f"({d['source']}: DMMA {d['dmma_tflops']}, DFMA {d['dfma_tflops']}, mixed "
+                                     f"{d['mixed_tflops']} TF); profiles/fp64_peak.json")
 
 
 def _peaks():
@@ -147,9 +161,12 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.mean(times))
     value = G / (ms / 1e3)
-    sample = f"first {G} gates of {args.config} at n={w.n} per step"
-    metric = C4_METRIC if args.config == "C4" else f"gates/sec ({args.config} circuit evolution, oracle sample)"
-    line = {"metric": metric, "value": value, "unit": "gates/s", "impl": "reference",
+    sample = f"first {G} gates of {args.config} at n={w.n} per step (no <H>)"
+    # a sampled workload, not the full C4 step: its own metric string (the units agree, so the ratio
+    # of the two arms is gates/s over gates/s, but it is not a same-config comparison)
+    metric = f"gates/sec (oracle sample of the {args.config} circuit evolution; first {G} gates per step, no <H>)"
+    line = {"metric": metric, "value": value, "unit": "gates/s", "impl": "reference", "same_config": False,
+            "sample": sample,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic", "config": {"workload": args.config, "n_qubits": w.n, "gates": len(w.gates),
@@ -159,10 +176,51 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-# the headline metric string (BASELINE.json); both arms print the same one
+# the headline metric string (BASELINE.json)
 C4_METRIC = "gates/sec (30q random circuit C4 evolution + 50-term <H>), SV GB/s, grad evals/sec"
 
 GRAD_CONFIGS = ("C1", "C2", "C3", "C3dc", "C4g")
+
+
+def cpu_grad_sample(config: str, threads: int, budget_s: float = 8.0):
+    """The oracle's adjoint gradient (or_adjoint_grad, as it stands) timed on the host cores with
+    `threads` OpenMP threads, in a subprocess (the thread count is fixed per process), on a bounded
+    sample: the full task when it fits the budget, else the first G gates of the circuit with the
+    first T Hamiltonian terms (G doubled until one evaluation takes about budget_s / 4; T = all terms
+    up to 20 qubits, else the single lightest term — the oracle applies every Pauli string qubit by
+    qubit, which alone is minutes per term at 30 qubits). Returns a cpu_baseline dict (value = evaluations per second of
+    the sample, which is named)."""
+    code = f"""
+import json, sys, time
+sys.path.insert(0, {ROOT!r})
+import oracle, workloads as W
+w = W.config({config!r})
+if w.n > 20:  # one lightest term (fewest non-identity qubits: fewest oracle passes)
+    w.ham = sorted(w.ham, key=lambda t: len(t[1]))[:1]
+T = len(w.ham)
+G = len(w.gates) if w.n <= 16 else (8 if w.n <= 24 else 2)
+while True:
+    t0 = time.perf_counter(); oracle.adjoint_grad(w.n, w.gates[:G], w.params, w.ham[:T]); dt = time.perf_counter() - t0
+    if G >= len(w.gates) or dt > {budget_s} / 4: break
+    G = min(len(w.gates), 2 * G)
+reps = max(1, int({budget_s} / max(dt, 1e-6) / 2))
+t0 = time.perf_counter()
+for _ in range(reps): oracle.adjoint_grad(w.n, w.gates[:G], w.params, w.ham[:T])
+dt = (time.perf_counter() - t0) / reps
+print(json.dumps({{"G": G, "total": len(w.gates), "T": T, "terms": len(W.config({config!r}).ham), "n": w.n, "s": dt}}))
+"""
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+        full = d["G"] == d["total"] and d["T"] == d["terms"]
+        return {"value": 1.0 / d["s"], "unit": "grad evals/s" + ("" if full else " (sample)"), "cores": threads,
+                "kind": "oracle", "sample": (f"oracle.adjoint_grad on the full {config} task" if full else
+                                             f"oracle.adjoint_grad on the first {d['G']} of {d['total']} gates and "
+                                             f"{d['T']} of {d['terms']} terms of {config} (n={d['n']}), "
+                                             f"{d['s']:.2f} s per evaluation")}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "grad evals/s", "cores": threads, "kind": "oracle", "sample": f"failed: {e}"}
 
 
 def run_grad_config(args, P, torch):
@@ -218,10 +276,15 @@ def run_grad_config(args, P, torch):
                                             "rows_per_step": evals,
                                             "param_updates": "parameters changed every step (optimiser loop)"},
             "fixed_params_value": evals / dt_fixed,
+            "launches_per_eval": int(st["kernel_launches"]) / max(1, args.steps),
             "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
             "e2e": {"value": evals / dt, "unit": "grad evals/s (host call incl.)",
                     "h2d_bytes_per_step": int(ga.nbytes + pa.nbytes + (rows.nbytes if rows is not None else w.params.nbytes)),
                     "d2h_bytes_per_step": int(8 * evals * (1 + len(w.params)))}}
+    if not args.no_cpu_baseline:
+        nproc = os.cpu_count() or 1
+        line["cpu_baseline"] = cpu_grad_sample(args.config, nproc)
+        line["cpu_baseline_1thread"] = cpu_grad_sample(args.config, 1)
     print(json.dumps(line), flush=True)
     sv.close()
 
@@ -285,6 +348,25 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        # one process per GPU: re-launch under torch.distributed.run with --gpus ranks
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py --gpus {args.gpus}: this box exposes {have} GPU(s); refusing to report a "
+                  f"{have}-GPU number as {args.gpus}", file=sys.stderr, flush=True)
+            sys.exit(2)
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world_env is not None and int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}")
 
     import torch
     import paper_2406_17248_b200 as P
@@ -305,14 +387,18 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     shards = world if world > 1 else max(1, args.virtual_shards)
-    if shards > 1:
-        # weak scaling (BASELINE configs[4] shape): C4's generator at
-        # n = 30 + log2(P) qubits, 2^30 amplitudes (16 GiB) per GPU, + 50-term JW H
+    if world > 1 or args.config == "C5":
+        # BASELINE configs[4]: 34 qubits, 256 GiB total (128 / 64 / 32 GiB per GPU at N = 2 / 4 / 8)
+        w = W.config("C5")
+        n = w.n
+        workload = f"C5: {n}q random circuit depth 40 (Haar 1q + CZ bricks, seed 3440) + 50-term JW H, sharded over {shards} GPUs"
+    elif shards > 1:
+        # virtual shards on one GPU (weak scaling): C4's generator at n = 30 + log2(P) qubits
         g = shards.bit_length() - 1
         n = 30 + g
         w = W.random_circuit(n, 40, seed=3440)
         w.ham = W.jw_hamiltonian(n, 50, 3440)
-        workload = f"C5w: {n}q random circuit depth 40 (Haar 1q + CZ bricks) + 50-term JW H, sharded over {shards}"
+        workload = f"C5w: {n}q random circuit depth 40 (Haar 1q + CZ bricks) + 50-term JW H, {shards} virtual shards on 1 GPU"
     else:
         w = W.config(args.config)
         n = w.n
@@ -373,10 +459,14 @@ def main():
     amps_total = float(1 << n)
     # 30q-equivalent gates/s: gates x (state size / 2^30) per second (= plain gates/s at N = 1)
     value = n_gates * (amps_total / float(1 << 30)) / (ms_step / 1e3)
-    passes = st["gate_passes"] // args.steps // (1 if world > 1 else shards)
     hbm_peak, peak_src = _peaks()
-    amps = amps_total / shards  # per GPU shard
-    pass_ms = circ_ms / max(passes, 1)
+    fp64_peak, fp64_src = _fp64_peak()
+    amps = amps_total / shards  # per shard
+    passes_total = st["gate_passes"] / args.steps  # every shard this handle holds
+    passes = passes_total / (1 if world > 1 else shards)  # per shard
+    x_ms = st["exchange_ms"] / args.steps  # exchange device time inside the timed steps
+    x_bytes = st["exchange_bytes"] / args.steps
+    pass_ms = (circ_ms - (x_ms if shards > 1 else 0.0)) / max(passes_total, 1)  # one shard's pass on this GPU
     pass_bytes = (16.0 if args.precision == "c64" else 32.0) * amps
     achieved = pass_bytes / (pass_ms / 1e3) / 1e9
     plan_bytes = st["algorithmic_bytes"] / args.steps / (1 if world > 1 else shards)
@@ -389,7 +479,10 @@ def main():
         c64 = args.precision == "c64"
         # complex64: the dense stages run TF32 MMAs with a 3-term split, so the peak for the
         # algorithmic (complex matrix-vector) flops is the measured TF32 mma.sync rate / 3
-        peak = TF32_SPLIT_PEAK_TFLOPS if c64 else FP64_PEAK_TFLOPS
+        peak = TF32_SPLIT_PEAK_TFLOPS if c64 else fp64_peak
+        # t_roof = sum over passes of max(bytes / BW, FP64 flops / rate)
+        bw = hbm_peak * 1e9
+        t_roof = sum(max(pass_bytes / bw, 2.0 * p["fma_per_amp"] * amps / (peak * 1e12)) for p in plan)
         roof = {
             "bound": "tensor",
             "kernel": ("k_pass_c64 (complex64 tiles; dense stages on TF32 tensor cores, 3-term split; register stages)"
@@ -397,19 +490,24 @@ def main():
                        "k_pass_dense / k_pass_reg<3,false> (fused forward tile passes: FP64 DMMA dense stages + register stages)"),
             "achieved": fp64_flops / passes / (pass_ms / 1e3) / 1e12, "peak": peak,
             "peak_source": ("measured legacy mma.sync TF32 277 TF (tools/microbench/mma_legacy.cu, "
-                            "profiles/r01_mma_legacy_microbench.jsonl) / 3 for the 3-term split" if c64 else
-                            "measured on this pool's B200 (tools/microbench/fp64_mix.cu: DMMA alone and "
-                            "DMMA+DFMA mixed 36.9 TF, DFMA alone 34.1 TF; profiles/r01_fp64_*.jsonl)"),
+                            "profiles/r01_mma_legacy_microbench.jsonl) / 3 for the 3-term split" if c64 else fp64_src),
             "unit": "TFLOP/s", "frac": fp64_flops / passes / (pass_ms / 1e3) / 1e12 / peak,
             "traffic": TRAFFIC_PER_LAUNCH.get(args.config) if args.precision == "c128" else TRAFFIC_PER_LAUNCH_C64,
             "algorithmic_flops_per_launch": fp64_flops / passes, "avg_launch_ms": pass_ms,
+            "t_roof_ms": 1e3 * t_roof, "t_roof_frac": 1e3 * t_roof / circ_ms,
             "hbm": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src,
                     "unit": "GB/s", "frac": achieved / hbm_peak, "algorithmic_bytes_per_launch": pass_bytes}}
     else:
-        roof = {"bound": "hbm", "kernel": "k_pass_reg<3,false> on each shard", "achieved": achieved,
-                "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": None, "algorithmic_bytes_per_launch": pass_bytes, "avg_launch_ms": pass_ms,
-                "exchanges_per_step": st["exchanges"] / args.steps / (1 if world > 1 else 1)}
+        roof = {"bound": "hbm", "kernel": "k_pass_dense / k_pass_reg<3,false> (forward passes on each shard)",
+                "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "algorithmic_bytes_per_launch": pass_bytes,
+                "avg_launch_ms": pass_ms, "passes_per_shard": passes,
+                "exchange": {"swaps_per_step": st["exchanges"] / args.steps, "bytes_per_step": x_bytes,
+                             "ms_per_step": x_ms, "achieved_gbs": (x_bytes / (x_ms / 1e3) / 1e9) if x_ms > 0 else None,
+                             "peak_gbs": NVLINK_PEER_GBS if world > 1 else None,
+                             "peak_source": ("measured peer copy per direction (B200_PROFILING.md; 900 nominal)"
+                                             if world > 1 else "virtual shards: device copies on one GPU (no NVLink)"),
+                             "frac": ((x_bytes / (x_ms / 1e3) / 1e9) / NVLINK_PEER_GBS) if (world > 1 and x_ms > 0) else None}}
     clocks = clk.summary()
 
     # e2e: the same step through the public C ABI with host inputs (gate / term arrays marshalled
@@ -431,7 +529,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = ga.nbytes + pa.nbytes + w.params.nbytes
-    e2e = {"value": n_gates * (amps_total / float(1 << 30)) / e2e_s, "unit": "gates/s (30q-equivalent)",
+    e2e = {"value": n_gates * (amps_total / float(1 << 30)) / e2e_s,
+           "unit": "gates/s" if n == 30 else "gates/s (30q-equivalent)",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8}
 
     grad = None
@@ -463,14 +562,15 @@ def main():
     if rank == 0:
         line = {
             "metric": C4_METRIC,
-            "value": value, "unit": "gates/s" if shards == 1 else "gates/s (30q-equivalent: gates x 2^(n-30))",
+            "value": value, "unit": "gates/s" if n == 30 else "gates/s (30q-equivalent: gates x 2^(n-30))",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if (world > 1 or args.config == "C5") else "weak", "vs_baseline": None,
             "dtype": "c64 (f32 dense stages, f64 register ops)" if args.precision == "c64" else "c128 (f64)",
             "data": "synthetic",
             "config": {"workload": workload, "n_qubits": n, "gates": n_gates, "ham_terms": len(w.ham),
                        "state_bytes": int((8 if args.precision == "c64" else 16) * amps_total), "shards": shards,
-                       "l2": "inputs (16 GiB per GPU) larger than L2; no flush",
+                       "l2": f"inputs ({int((8 if args.precision == 'c64' else 16) * amps) >> 30} GiB per shard) larger than L2; no flush",
                        "parallelism": (f"state sharded over {world} GPUs (NCCL)" if world > 1 else
                                        f"{shards} virtual shards on 1 GPU" if shards > 1 else "1 GPU")},
             "circuit_ms": circ_ms, "passes_per_circuit": passes, "E": E,

@@ -117,6 +117,9 @@ typedef struct {
                                     cross-shard Pauli streams (each direction counted once)      */
   double exchange_ms;            /* sharded: device time of those exchanges (CUDA events around each
                                     exchange on the handle's stream; summed at sv_get_stats)      */
+  int64_t gate_applications;     /* instrumented cost counter: gate-vector
+                                    applications the executed plans performed — a forward plan of N
+                                    gates adds N, an adjoint plan 2N (psi and lambda)             */
 } sv_stats;
 
 /* Option keys for sv_set_option (A/B evidence; defaults are the tuned values). */

@@ -64,6 +64,10 @@ def lib():
         L.or_splitmix64.restype = u64
         L.or_sample.argtypes = [P, ctypes.c_int, i64, u64, P]
         L.or_sample.restype = None
+        L.or_get_gate_applications.argtypes = []
+        L.or_get_gate_applications.restype = i64
+        L.or_reset_gate_applications.argtypes = []
+        L.or_reset_gate_applications.restype = None
         L.or_state_zero.argtypes = [P, ctypes.c_int]
         L.or_state_zero.restype = None
         _lib = L
@@ -204,6 +208,15 @@ def shift_grad(n: int, gates, params, ham, psi0: Optional[np.ndarray] = None) ->
     if rc != 0:
         raise ValueError("non-differentiable gate carries a parameter")
     return g[:P]
+
+
+def gate_applications() -> int:
+    """The oracle's instrumented gate-application counter (or_apply_gate calls since the last reset)."""
+    return int(lib().or_get_gate_applications())
+
+
+def reset_gate_applications() -> None:
+    lib().or_reset_gate_applications()
 
 
 def splitmix64(x: int) -> int:

@@ -208,9 +208,16 @@ static void or_conj_transpose(int d, const cplx* m, cplx* out) {
 }
 
 /* Applies gate g (or its inverse when dagger != 0), with `extra` added to its angle. */
+/* Instrumented gate-application counter (SPEC S:478, S:695 cost contract): every application of a
+ * circuit gate (or its inverse) to a state vector through or_apply_gate increments it. */
+static int64_t or_gate_applications = 0;
+int64_t or_get_gate_applications(void) { return or_gate_applications; }
+void or_reset_gate_applications(void) { or_gate_applications = 0; }
+
 static void or_apply_gate(cplx* psi, int n, const or_circuit* c, int64_t g, const double* params,
                           double extra, int dagger) {
   cplx m[16], md[16];
+  ++or_gate_applications;
   int d = or_gate_matrix_c(c->kinds[g], or_angle(c, g, params) + extra, c->mats + 32 * g, m);
   if (dagger) { or_conj_transpose(d, m, md); memcpy(m, md, sizeof(cplx) * d * d); }
   or_apply_matrix_c(psi, n, d == 4 ? 2 : 1, c->targets + 2 * g, c->cmasks[g], m);

@@ -282,6 +282,7 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
       da_done += (size_t)n_da;
     }
     const double amps = (double)(1ull << h->n_local);
+    if (i == 0) h->stats.gate_applications += plan.n_src_gates * (lam ? 2 : 1);
     if (lam) {
       h->stats.adjoint_passes += 1;
       h->stats.algorithmic_bytes += 64.0 * amps;

@@ -1021,6 +1021,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
   // ---- 2. emit passes (forward order, or reversed with daggered ops for the adjoint sweep) ----
   plan->passes.clear();
   plan->reverse = reverse;
+  plan->n_src_gates = (int64_t)gates.size();
   plan->grid_cache = 0;
   plan->grid_cache_n = -1;  // the plan_grid memo belongs to the plan being replaced
   plan->pass_grid.clear();

@@ -196,6 +196,7 @@ struct Plan {
   int max_da_per_pass = 0;  // R accumulator slots (2^m_outer per adjoint dense stage) of the largest pass
   int da_slots_total = 0;
   bool reverse = false;  // adjoint plan: passes run on (psi, lambda) with the DUAL kernel
+  int64_t n_src_gates = 0;  // bound gates the plan applies (cost counter: x1 forward, x2 adjoint)
   mutable int grid_cache = 0, grid_cache_n = -1;  // plan_grid memo (occupancy query once per plan)
   mutable std::vector<int> pass_grid;             // per-pass CTAs (register passes: occupancy of that pass)
 };

@@ -366,3 +366,30 @@ def test_concurrent_handles_two_threads(P):
         t.join()
     assert len(errs[0]) == 4 and len(errs[1]) == 4
     assert max(errs[0] + errs[1]) <= 1e-9, errs
+
+
+def test_adjoint_cost_contract(P):
+    """S:478 / S:695 cost contract on the GPU path: one evaluation of sv_expectation_with_grad
+    performs N (forward plan) + 2N (adjoint plan over psi and lambda) = 3N gate applications
+    (instrumented counter sv_stats.gate_applications), and the same numbers of HBM passes,
+    whatever the number of distinct parameters P the circuit's rotations share."""
+    import dataclasses
+    base = W.random_complex(14, 6, seed=3, n_params=12)
+    ham = W.random_hamiltonian(14, 6, seed=3)
+    N = len(base.gates)
+    seen = set()
+    for nparam in (1, 4, 12):
+        gates = []
+        for g in base.gates:
+            gates.append(dataclasses.replace(g, param=g.param % nparam) if g.param >= 0 else g)
+        params = base.params[:nparam]
+        sv = P.StateVector(14)
+        P.sv_reset_stats(sv.h)
+        E, g = sv.expectation_with_grad(gates, params, ham)
+        st = sv.stats()
+        sv.close()
+        E0, g0 = oracle.adjoint_grad(14, gates, params, ham)
+        assert abs(E - E0) < 1e-9 and np.max(np.abs(g - g0)) < 1e-9
+        assert st["gate_applications"] == 3 * N, (nparam, st["gate_applications"], N)
+        seen.add((st["gate_passes"], st["adjoint_passes"]))
+    assert len(seen) == 1, seen  # pass counts do not grow with P

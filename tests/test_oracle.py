@@ -431,3 +431,19 @@ def test_sample_frequencies_match_probabilities():
     # deterministic under the seed, different under another seed
     assert np.array_equal(idx, oracle.sample_indices(psi, shots, seed=11))
     assert not np.array_equal(idx, oracle.sample_indices(psi, shots, seed=12))
+
+
+def test_oracle_adjoint_cost_contract():
+    """S:478 / S:695: the adjoint gradient performs one forward pass and one backward sweep with two
+    un-applications per gate — 3N gate applications, independent of the parameter count P (the
+    instrumented counter of or_apply_gate); parameter-shift needs O(N P)."""
+    for P in (1, 4, 12):
+        w = W.random_complex(6, 6, seed=P, n_params=P)
+        ham = W.random_hamiltonian(6, 5, seed=P)
+        N = len(w.gates)
+        oracle.reset_gate_applications()
+        oracle.adjoint_grad(6, w.gates, w.params, ham)
+        assert oracle.gate_applications() == 3 * N, (P, oracle.gate_applications(), N)
+        oracle.reset_gate_applications()
+        oracle.shift_grad(6, w.gates, w.params, ham)
+        assert oracle.gate_applications() > 3 * N  # the shift rule re-evaluates per occurrence
