@@ -62,7 +62,9 @@ __device__ __forceinline__ double2 cneg(double2 a) { return make_double2(-a.x, -
 struct RegArgs {
   int32_t k, low, nops, nstages, n_outer, nmats, ngrad, grid;
   int32_t n_da, pstride;  // pstride: slot-row stride of partials (>= grid)
-  int32_t c64_terms, pad_;  // complex64 dense stages: 3 = hi/lo split products (default), 1 = hi only
+  int32_t c64_terms;  // complex64 dense stages: 3 = hi/lo split products (default), 1 = hi only
+  int32_t acc_thread; // adjoint: 1 = overlap partials per thread ([grad op][thread] in shared memory, summed
+                      // once at the end), 0 = warp-shuffle reduced per op ([grad op][warp])
   double* r_partials;  // adjoint dense stages: [da][warp][16 * 32][grid]
   int8_t tq[kMaxTileQubits + 3];
   int8_t oq[64];
@@ -127,6 +129,60 @@ __device__ __forceinline__ void reg_m1(double2 (&v)[1 << NR], const double2* m, 
     v[j] = cfma(m00, a, cmul(m01, b));
     v[j1] = cfma(m10, a, cmul(m11, b));
   }
+}
+
+// Real-structured rotations on register bit RB (no register controls): RX [[c, -is], [-is, c]],
+// RY [[c, -s], [s, c]]; 4 FP64 instructions per amplitude.
+template <int NR, int RB>
+__device__ __forceinline__ void reg_rx(double2 (&v)[1 << NR], const double2* m) {
+  const double c = m[0].x, s = -m[1].y;
+#pragma unroll
+  for (int j = 0; j < (1 << NR); ++j) {
+    if (j & (1 << RB)) continue;
+    const int j1 = j | (1 << RB);
+    const double2 a = v[j], b = v[j1];
+    v[j] = make_double2(fma(c, a.x, s * b.y), fma(c, a.y, -s * b.x));
+    v[j1] = make_double2(fma(c, b.x, s * a.y), fma(c, b.y, -s * a.x));
+  }
+}
+template <int NR, int RB>
+__device__ __forceinline__ void reg_ry(double2 (&v)[1 << NR], const double2* m) {
+  const double c = m[0].x, s = -m[1].x;
+#pragma unroll
+  for (int j = 0; j < (1 << NR); ++j) {
+    if (j & (1 << RB)) continue;
+    const int j1 = j | (1 << RB);
+    const double2 a = v[j], b = v[j1];
+    v[j] = make_double2(fma(c, a.x, -s * b.x), fma(c, a.y, -s * b.y));
+    v[j1] = make_double2(fma(s, a.x, c * b.x), fma(s, a.y, c * b.y));
+  }
+}
+// Overlaps of the rotation generators before un-applying (no register controls):
+// RX: G = -(i/2) X -> Re<w|G|v> = (1/2) sum_pairs [Im(conj(w0) v1) + Im(conj(w1) v0)];
+// RY: G = -(i/2) Y = [[0, -1/2], [1/2, 0]] -> (1/2) sum_pairs [Re(conj(w1) v0) - Re(conj(w0) v1)].
+template <int NR, int RB>
+__device__ __forceinline__ double reg_ov_rx(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR]) {
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < (1 << NR); ++j) {
+    if (j & (1 << RB)) continue;
+    const int j1 = j | (1 << RB);
+    a0 = fma(w[j].x, v[j1].y, fma(-w[j].y, v[j1].x, a0));
+    a1 = fma(w[j1].x, v[j].y, fma(-w[j1].y, v[j].x, a1));
+  }
+  return 0.5 * (a0 + a1);
+}
+template <int NR, int RB>
+__device__ __forceinline__ double reg_ov_ry(const double2 (&v)[1 << NR], const double2 (&w)[1 << NR]) {
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < (1 << NR); ++j) {
+    if (j & (1 << RB)) continue;
+    const int j1 = j | (1 << RB);
+    a0 = fma(w[j1].x, v[j].x, fma(w[j1].y, v[j].y, a0));
+    a1 = fma(w[j].x, v[j1].x, fma(w[j].y, v[j1].y, a1));
+  }
+  return 0.5 * (a0 - a1);
 }
 
 template <int NR, int RB, bool CTRL>
@@ -314,6 +370,18 @@ __device__ __forceinline__ void reg_apply_c(double2 (&v)[1 << NR], const Op& o, 
 #undef C1
       break;
     }
+    case OP_RX: {
+#define C1(R) reg_rx<NR, R>(v, m)
+      SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      break;
+    }
+    case OP_RY: {
+#define C1(R) reg_ry<NR, R>(v, m)
+      SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      break;
+    }
     case OP_M2: {
 #define C2(A, B) reg_m2<NR, A, B, CTRL>(v, m, cj)
       SV_DISP2(NR, o.ra(), o.rb(), C2)
@@ -481,6 +549,32 @@ __device__ __forceinline__ double dual_op_c(double2 (&v)[1 << NR], double2 (&w)[
       reg_m1<NR, R, CTRL>(v, m, cj);                            \
       reg_m1<NR, R, CTRL>(w, m, cj);                            \
     }                                                           \
+  }
+      SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      break;
+    }
+    case OP_RX: {
+#define C1(R)                                       \
+  {                                                 \
+    if (ok) {                                       \
+      if (gen) part = reg_ov_rx<NR, R>(v, w);       \
+      reg_rx<NR, R>(v, m);                          \
+      reg_rx<NR, R>(w, m);                          \
+    }                                               \
+  }
+      SV_DISP1(NR, o.ra(), C1)
+#undef C1
+      break;
+    }
+    case OP_RY: {
+#define C1(R)                                       \
+  {                                                 \
+    if (ok) {                                       \
+      if (gen) part = reg_ov_ry<NR, R>(v, w);       \
+      reg_ry<NR, R>(v, m);                          \
+      reg_ry<NR, R>(w, m);                          \
+    }                                               \
   }
       SV_DISP1(NR, o.ra(), C1)
 #undef C1
@@ -706,8 +800,9 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   // tile index -> base offset of its outer qubits: four 64-entry deposit tables (tile bits
   // 6c .. 6c+5 -> their outer qubits), replacing a per-tile loop over n_outer bits
   uint64_t* s_ob = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
-  double* s_acc = reinterpret_cast<double*>(s_ob + 4 * 64);  // [ngrad][nwarps]
-  double* s_racc = s_acc + (DUAL ? a.ngrad * nwarps : 0);   // [n_da][nwarps][512]
+  const int nacc = a.acc_thread ? nthr : nwarps;            // overlap accumulators per grad op
+  double* s_acc = reinterpret_cast<double*>(s_ob + 4 * 64);  // [ngrad][nacc]
+  double* s_racc = s_acc + (DUAL ? a.ngrad * nacc : 0);     // [n_da][nwarps][512]
 
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.ops);
@@ -726,7 +821,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
       s_ob[h] = off;
     }
     if (DUAL) {
-      for (int i = tid; i < a.ngrad * nwarps; i += nthr) s_acc[i] = 0.0;
+      for (int i = tid; i < a.ngrad * nacc; i += nthr) s_acc[i] = 0.0;
       for (int i = tid; i < a.n_da * nwarps * 512; i += nthr) s_racc[i] = 0.0;
     }
   }
@@ -843,9 +938,13 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
           double part = o.cj() ? dual_op_c<NR, true>(v, w, o, m, g, tthr, base, ok)
                                : dual_op_c<NR, false>(v, w, o, m, g, tthr, base, ok);
           if (o.gen()) {
+            if (a.acc_thread) {
+              s_acc[o.grad_local() * nthr + tid] += part;  // this thread's running sum over its tiles
+            } else {
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-            if (lane == 0) s_acc[o.grad_local() * nwarps + warp] += part;
+              for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+              if (lane == 0) s_acc[o.grad_local() * nwarps + warp] += part;
+            }
           }
         } else {
           if (!ok) continue;
@@ -884,7 +983,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
       const Op o = load_op(s_ops + i);
       if (!o.gen()) continue;
       double s = 0.0;
-      for (int wi = 0; wi < nwarps; ++wi) s += s_acc[o.grad_local() * nwarps + wi];
+      for (int wi = 0; wi < nacc; ++wi) s += s_acc[o.grad_local() * nacc + wi];  // fixed order
       a.partials[(int64_t)s_ops[i].grad_slot * a.pstride + blockIdx.x] = s;
     }
   }
@@ -1224,12 +1323,13 @@ size_t dense_pass_smem_bytes(int k, int nstages) {
 }
 
 
-size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da) {
+size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da,
+                      bool acc_thread) {
   size_t b = (size_t(16) << k) * (dual ? 2 : 1) * ((dual && (n_da > 0 || SV_DUAL_SINGLE_BUF)) ? 1 : 2);  // tile buffers
   b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
   b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
   b += (size_t)nmats * 8 + 4 * 64 * 8;
-  b += dual ? (size_t)ngrad * (nthr / 32) * 8 : 0;
+  b += dual ? (size_t)ngrad * (acc_thread ? nthr : nthr / 32) * 8 : 0;
   return b;
 }
 
@@ -1264,8 +1364,22 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual) {
   int n_da = 0;
   for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? (1 << plan.stages[si].m_outer) : 0;
   const int nthr = 1 << (pd.k - pd.R);
+  // adjoint passes: per-thread overlap accumulators when they cost no resident CTA
+  bool acc_thread = false;
+  if (dual) {
+    int b_warp = 0, b_thr = 0;
+    const size_t sw = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
+                                     pd.n_grad, nthr, dual, n_da, false);
+    const size_t st = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
+                                     pd.n_grad, nthr, dual, n_da, true);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_warp, k_pass_reg<3, true>, nthr, sw);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_thr, k_pass_reg<3, true>, nthr, st);
+    acc_thread = b_thr >= b_warp && b_thr > 0 && pd.n_grad > 0;
+    if (plan.pass_acc.size() != plan.passes.size()) plan.pass_acc.assign(plan.passes.size(), 0);
+    plan.pass_acc[i] = acc_thread ? 1 : 0;
+  }
   const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da);
+                                     pd.n_grad, nthr, dual, n_da, acc_thread);
   int blocks = 0;
   if (pass_all_dense(plan, pd)) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense, nthr,
@@ -1312,7 +1426,8 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   a.n_da = L.n_da;
   a.pstride = L.pstride > 0 ? L.pstride : L.grid;
   a.r_partials = L.r_partials;
-  const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual, a.n_da);
+  a.acc_thread = dual ? L.acc_thread : 0;
+  const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual, a.n_da, a.acc_thread != 0);
   {
     cudaError_t e = set_reg_attrs();
     if (e != cudaSuccess) return e;

@@ -1136,6 +1136,23 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
       const uint32_t pa = o.pa >= 0 ? (uint32_t)o.pa : 31u, pb = o.pb >= 0 ? (uint32_t)o.pb : 31u;
       const uint32_t gen = o.grad_slot >= 0 ? (o.gen_dim == 4 ? 2u : 1u) : 0u;
       uint32_t dfl = 0;
+      uint32_t type = (uint32_t)o.type;
+      if (o.type == OP_M1 && o.cj == 0 && o.ra >= 0) {
+        // real-structured rotations (RX / RY and their daggers) run as OP_RX / OP_RY: exact for any
+        // matrix of that form; a generator must be the rotation's own (-i/2 X or -i/2 Y)
+        const double* m = plan->mats.data() + pd.mat_begin + o.mat_off;  // m00 m01 m10 m11 (re, im)
+        const bool rx = m[1] == 0.0 && m[2] == 0.0 && m[7] == 0.0 && m[6] == m[0] && m[4] == 0.0 && m[5] == m[3];
+        const bool ry = m[1] == 0.0 && m[3] == 0.0 && m[5] == 0.0 && m[7] == 0.0 && m[6] == m[0] && m[4] == -m[2];
+        bool gen_ok = true;
+        if (o.grad_slot >= 0) {
+          const double* gm = plan->mats.data() + pd.mat_begin + o.gen_off;
+          const double gx[8] = {0, 0, 0, -0.5, 0, -0.5, 0, 0}, gy[8] = {0, 0, -0.5, 0, 0.5, 0, 0, 0};
+          const double* want = rx ? gx : gy;
+          gen_ok = o.gen_dim == 2 && !o.gen_diag;
+          for (int e = 0; e < 8 && gen_ok; ++e) gen_ok = gm[e] == want[e];
+        }
+        if ((rx || ry) && gen_ok) type = rx ? OP_RX : OP_RY;
+      }
       if (o.type == OP_D1) {
         const double* m = plan->mats.data() + pd.mat_begin + o.mat_off;
         if (m[0] == 1.0 && m[1] == 0.0) {
@@ -1143,7 +1160,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
           if (m[2] == -1.0 && m[3] == 0.0) dfl |= 2u;
         }
       }
-      r.code = (uint32_t)o.type | (ra << 4) | (rb << 8) | ((uint32_t)o.cj << 12) | (pa << 16) | (pb << 21) |
+      r.code = type | (ra << 4) | (rb << 8) | ((uint32_t)o.cj << 12) | (pa << 16) | (pb << 21) |
                (gen << 26) | ((o.gen_diag ? 1u : 0u) << 28) | (dfl << 29);
       r.mat_off = (uint16_t)(o.mat_off / 2);
       r.gen_off = (uint16_t)(o.gen_off / 2);

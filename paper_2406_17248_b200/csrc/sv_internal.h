@@ -62,6 +62,11 @@ enum OpType : int32_t {
   OP_M2 = 3,   // 4x4 on tile positions pa (index bit 0), pb (bit 1) mat: 32 doubles
   OP_D2 = 4,   // diagonal 4 entries on physical qubits qa (bit0), qb (bit1)  mat: 8 doubles
   OP_SWAP = 5, // SWAP of tile positions pa, pb                    mat: none
+  // register-kernel op codes only (RegOp): rotations with real structure, no register controls
+  // (mat: the 2x2 as for OP_M1; the kernel reads c = m00.re and s from m01): 4 FP64 per amplitude
+  // instead of 8 for a general complex 2x2
+  OP_RX = 6,   // [[c, -i s], [-i s, c]]
+  OP_RY = 7,   // [[c, -s], [s, c]]
 };
 
 struct DevOp {
@@ -199,6 +204,7 @@ struct Plan {
   int64_t n_src_gates = 0;  // bound gates the plan applies (cost counter: x1 forward, x2 adjoint)
   mutable int grid_cache = 0, grid_cache_n = -1;  // plan_grid memo (occupancy query once per plan)
   mutable std::vector<int> pass_grid;             // per-pass CTAs (register passes: occupancy of that pass)
+  mutable std::vector<uint8_t> pass_acc;          // adjoint passes: 1 = per-thread overlap accumulators
 };
 constexpr int kMaxDAPerPass = 4;  // adjoint dense stages per pass (16 KiB of R accumulators each at 2^10 tiles; measured best, profiles/r01_da_per_pass_sweep.txt)
 
@@ -256,6 +262,7 @@ struct PassLaunch {
   int pstride = 0;         // stride of d_partials' slot rows (>= grid; 0: grid)
   bool all_dense = false;  // forward register pass of dense stages only (k_pass_dense)
   int c64_terms = 3;       // complex64 dense stages: TF32 split products (3) or one product (1)
+  int acc_thread = 0;      // adjoint: overlaps accumulate per thread in shared memory (no per-op shuffles)
   int n_local;
   uint64_t rank_bits;      // (sharded) global index bits of this shard, for controls/diagonals on
                            // global qubits folded by the planner (0 single-GPU)
