@@ -98,6 +98,7 @@ struct Op {
   __device__ __forceinline__ int32_t grad_local() const { return (int32_t)(int16_t)(w2 >> 16); }
   __device__ __forceinline__ uint32_t qa() const { return w3 & 0xffu; }
   __device__ __forceinline__ uint32_t qb() const { return (w3 >> 8) & 0xffu; }
+  __device__ __forceinline__ uint32_t run_len() const { return w3 >> 16; }
 };
 
 __device__ __forceinline__ Op load_op(const RegOp* p) {
@@ -639,6 +640,192 @@ __device__ __forceinline__ double dual_op_c(double2 (&v)[1 << NR], double2 (&w)[
   return part;
 }
 
+// ---------------------------------------------------------------- diagonal runs (DUAL)
+//
+// A run of consecutive diagonal ops (Z-like / two-qubit diagonal, no register controls) in an
+// adjoint stage. For diagonal U, conj(U^+ lam)_e (U^+ psi)_e = conj(lam_e) psi_e, so every op of the
+// run sees the same p_e = conj(lam_e) psi_e, and its overlap Re<lam|Pi_C G|psi> (G = i diag(gq),
+// purely imaginary for RZ / RZZ / PS) is -sum_e gq(e) Im(p_e) over control-satisfied e. The run's
+// un-application is one phase per amplitude: the product of the ops' entries, accumulated per thread
+// in factor tables over the 3 register bits (U: ops on thread / outer bits only; A[r][b]: one
+// register target r; B[pair][b_r + 2 b_s]: two register targets) and applied once to psi and lambda.
+// psi and lambda are parked in their tile slots meanwhile (their registers carry the tables).
+struct DiagTables {
+  double2 U;
+  double2 A[3][2];
+  double2 B[3][4];  // pairs (0,1), (0,2), (1,2)
+};
+
+__device__ __forceinline__ void tab_one(double2& t) { t = make_double2(1.0, 0.0); }
+
+// Sum over j of Im(p_j) with bit R of j equal to b (R compile-time)
+template <int R>
+__device__ __forceinline__ void half_sums(const double (&P)[8], double& s0, double& s1) {
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if ((j >> R) & 1) b += P[j];
+    else a += P[j];
+  }
+  s0 = a;
+  s1 = b;
+}
+// Quarter sums by (bit RA, bit RB) -> index bit_RA + 2 bit_RB
+template <int RA, int RB>
+__device__ __forceinline__ void quarter_sums(const double (&P)[8], double (&s)[4]) {
+  s[0] = s[1] = s[2] = s[3] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s[((j >> RA) & 1) | (((j >> RB) & 1) << 1)] += P[j];
+}
+
+// one op of a run: entries d[] (un-apply), generator imaginary parts gq[] (zero without gen)
+template <int RA, int RB>  // register positions; -1: uniform (value ta / tb); RB = -2: one target
+__device__ __forceinline__ double diag_run_op(DiagTables& T, const double (&P)[8], double Ptot, const double2* m,
+                                              const double2* g, bool gen, uint32_t ta, uint32_t tb) {
+  constexpr bool TWO = RB != -2;
+  double2 d[4];
+  double gq[4];
+#pragma unroll
+  for (int q = 0; q < (TWO ? 4 : 2); ++q) {
+    d[q] = lds(m + q);
+    gq[q] = gen ? lds(g + q).y : 0.0;
+  }
+  if constexpr (!TWO) {  // one target
+    if constexpr (RA < 0) {
+      T.U = cmul(T.U, d[ta]);
+      return -gq[ta] * Ptot;
+    } else {
+      T.A[RA][0] = cmul(T.A[RA][0], d[0]);
+      T.A[RA][1] = cmul(T.A[RA][1], d[1]);
+      if (!gen) return 0.0;
+      double s0, s1;
+      half_sums<RA>(P, s0, s1);
+      return -(gq[0] * s0 + gq[1] * s1);
+    }
+  } else if constexpr (RA < 0 && RB < 0) {  // two targets, both uniform
+    T.U = cmul(T.U, d[ta | (tb << 1)]);
+    return -gq[ta | (tb << 1)] * Ptot;
+  } else if constexpr (RA < 0 || RB < 0) {  // one register target R, the other uniform (value u)
+    constexpr int R = RA < 0 ? RB : RA;
+    const uint32_t u = RA < 0 ? ta : tb;
+    // entries with bit_R = 0 / 1 (index bit 0 <-> target a, bit 1 <-> target b)
+    const int j0 = RA < 0 ? (int)u : (int)(u << 1), j1 = RA < 0 ? (int)u | 2 : (int)(u << 1) | 1;
+    T.A[R][0] = cmul(T.A[R][0], d[j0]);
+    T.A[R][1] = cmul(T.A[R][1], d[j1]);
+    if (!gen) return 0.0;
+    double s0, s1;
+    half_sums<R>(P, s0, s1);
+    return -(gq[j0] * s0 + gq[j1] * s1);
+  } else {  // two register targets: table index b_LO + 2 b_HI, entry index b_RA + 2 b_RB
+    constexpr int LO = RA < RB ? RA : RB, HI = RA < RB ? RB : RA;
+    constexpr int PAIR = (LO == 0 && HI == 1) ? 0 : ((LO == 0) ? 1 : 2);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int blo = q & 1, bhi = q >> 1;
+      const int e = RA < RB ? (blo | (bhi << 1)) : (bhi | (blo << 1));
+      T.B[PAIR][q] = cmul(T.B[PAIR][q], d[e]);
+    }
+    if (!gen) return 0.0;
+    double s[4];
+    quarter_sums<RA, RB>(P, s);
+    return -(gq[0] * s[0] + gq[1] * s[1] + gq[2] * s[2] + gq[3] * s[3]);
+  }
+}
+
+// The run [ops, ops + len) of a DUAL stage on this thread's amplitudes v (psi), w (lambda); slots
+// A ^ SR[...] hold them in the tile. Overlaps accumulate like single ops (per thread or per warp).
+__device__ __forceinline__ void dual_diag_run(double2 (&v)[8], double2 (&w)[8], const RegOp* ops, int len,
+                                              const double2* mats2, uint32_t tthr, uint64_t base, double2* tp,
+                                              double2* tl, uint32_t A, const uint32_t (&SR)[3], double* s_acc,
+                                              int nthr, int tid, int nwarps, int warp, int lane, bool acc_thread) {
+  double P[8];
+  double Ptot = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    P[j] = fma(w[j].x, v[j].y, -w[j].y * v[j].x);  // Im(conj(lambda) psi)
+    Ptot += P[j];
+  }
+  uint32_t ad[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    ad[j] = A ^ ((j & 1) ? SR[0] : 0u) ^ ((j & 2) ? SR[1] : 0u) ^ ((j & 4) ? SR[2] : 0u);
+    tp[ad[j]] = v[j];  // parked: their registers carry the tables during the run
+    tl[ad[j]] = w[j];
+  }
+  DiagTables T;
+  tab_one(T.U);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) { tab_one(T.A[r][0]); tab_one(T.A[r][1]); }
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tab_one(T.B[p][q]);
+  for (int k = 0; k < len; ++k) {
+    const Op o = load_op(ops + k);
+    const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
+    const bool gen = o.gen() != 0u;
+    double part = 0.0;
+    if (ok) {
+      const uint32_t ta = o.pa() != 31u ? (tthr >> o.pa()) & 1u : (uint32_t)((base >> o.qa()) & 1ull);
+      const uint32_t tb = o.pb() != 31u ? (tthr >> o.pb()) & 1u : (uint32_t)((base >> o.qb()) & 1ull);
+      const double2* m = mats2 + o.mat_off();
+      const double2* g = mats2 + o.gen_off();
+      if (o.type() == OP_D1) {
+        switch (o.ra()) {
+          case 0: part = diag_run_op<0, -2>(T, P, Ptot, m, g, gen, ta, tb); break;
+          case 1: part = diag_run_op<1, -2>(T, P, Ptot, m, g, gen, ta, tb); break;
+          case 2: part = diag_run_op<2, -2>(T, P, Ptot, m, g, gen, ta, tb); break;
+          default: part = diag_run_op<-1, -2>(T, P, Ptot, m, g, gen, ta, tb); break;
+        }
+      } else {
+        const uint32_t ra = o.ra() > 2u ? 3u : o.ra(), rb = o.rb() > 2u ? 3u : o.rb();
+#define CR(X, Y) part = diag_run_op<X, Y>(T, P, Ptot, m, g, gen, ta, tb)
+        switch (ra * 4 + rb) {
+          case 1: CR(0, 1); break;
+          case 2: CR(0, 2); break;
+          case 3: CR(0, -1); break;
+          case 4: CR(1, 0); break;
+          case 6: CR(1, 2); break;
+          case 7: CR(1, -1); break;
+          case 8: CR(2, 0); break;
+          case 9: CR(2, 1); break;
+          case 11: CR(2, -1); break;
+          case 12: CR(-1, 0); break;
+          case 13: CR(-1, 1); break;
+          case 14: CR(-1, 2); break;
+          default: CR(-1, -1); break;
+        }
+#undef CR
+      }
+    }
+    if (gen) {
+      if (acc_thread) {
+        s_acc[o.grad_local() * nthr + tid] += part;
+      } else {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+        if (lane == 0) s_acc[o.grad_local() * nwarps + warp] += part;
+      }
+    }
+  }
+  // phase of amplitude j = U A0[b0] A1[b1] A2[b2] B01[b0 + 2 b1] B02[b0 + 2 b2] B12[b1 + 2 b2], built bit by bit
+  double2 q1[2], q2[4];
+#pragma unroll
+  for (int b0 = 0; b0 < 2; ++b0) q1[b0] = cmul(T.U, T.A[0][b0]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int b0 = i & 1, b1 = i >> 1;
+    q2[i] = cmul(cmul(q1[b0], T.A[1][b1]), T.B[0][b0 | (b1 << 1)]);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int b0 = j & 1, b1 = (j >> 1) & 1, b2 = j >> 2;
+    const double2 ph = cmul(cmul(cmul(q2[j & 3], T.A[2][b2]), T.B[1][b0 | (b2 << 1)]), T.B[2][b1 | (b2 << 1)]);
+    v[j] = cmul(ph, tp[ad[j]]);
+    w[j] = cmul(ph, tl[ad[j]]);
+  }
+}
+
 // ---------------------------------------------------------------- dense FP64-MMA stage
 //
 // The stage's ops were folded on the host into a 16x16 complex matrix U per variant; with
@@ -931,6 +1118,15 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
       }
       for (int i = S.op_begin; i < S.op_end; ++i) {
         const Op o = load_op(s_ops + i);
+        if constexpr (DUAL) {
+          const uint32_t rl = o.run_len();
+          if (rl) {  // a run of diagonal ops, evaluated together
+            dual_diag_run(v, w, s_ops + i, (int)rl, mats2, tthr, base, tp, tl, A, SR, s_acc, nthr, tid, nwarps, warp,
+                          lane, a.acc_thread != 0);
+            i += (int)rl - 1;
+            continue;
+          }
+        }
         const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
         const double2* m = mats2 + o.mat_off();
         if constexpr (DUAL) {

@@ -323,6 +323,9 @@ int da_min_cost_for(int n_local, int opt) {
   return n_local >= 24 ? 96 : 250;
 }
 const int g_da_enable = env_int("SV_DA", 1);
+// shortest run of diagonal ops the DUAL kernel evaluates as one (its fixed cost: conj(lambda) psi,
+// parking psi / lambda, the phase tables' product and one application)
+const int g_diag_run_min = env_int("SV_DIAG_RUN_MIN", 4);
 const int g_da_max_per_pass = env_int("SV_DA_MAX_PER_PASS", kMaxDAPerPass);
 
 const int g_da_max_tile = env_int("SV_DA_MAX_TILE", 2);
@@ -850,6 +853,45 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
 
 // Plans the register stages of pass `pd` (ops already emitted in pass order) and rewrites the
 // pass' op range in stage order.
+// Adjoint stages: diagonal ops the DUAL kernel can evaluate as one run (no register controls,
+// purely imaginary diagonal generator) are moved back to join the previous run of the stage when
+// they commute with every op in between (disjoint non-diagonal supports, the planner's rule; the
+// overlap <lam|D|psi> is unchanged by moving D past a commuting unitary N: <N^+ lam|D|N^+ psi> =
+// <lam|N D N^+|psi> = <lam|D|psi>). Longer runs: one conj(lam) psi, one phase application each.
+bool diag_run_eligible(const DevOp& o, const PassDesc& pd, const Plan* plan) {
+  if ((o.type != OP_D1 && o.type != OP_D2) || o.cj != 0) return false;
+  if (o.grad_slot < 0) return true;
+  if (!o.gen_diag) return false;
+  const double* gm = plan->mats.data() + pd.mat_begin + o.gen_off;
+  for (int e = 0; e < o.gen_dim; ++e)
+    if (gm[2 * e] != 0.0) return false;
+  return true;
+}
+
+void group_diag_runs(StagePlan* sp, const PassDesc& pd, const Plan* plan) {
+  std::vector<DevOp> out;
+  out.reserve(sp->ops.size());
+  std::vector<char> elig;
+  for (const DevOp& o : sp->ops) {
+    const bool e = diag_run_eligible(o, pd, plan);
+    size_t pos = out.size();
+    if (e) {
+      uint64_t N, A;
+      phys_masks(o, pd, &N, &A);
+      long j = (long)out.size() - 1;
+      for (; j >= 0 && !elig[(size_t)j]; --j) {
+        uint64_t Nj, Aj;
+        phys_masks(out[(size_t)j], pd, &Nj, &Aj);
+        if ((N & Aj) || (Nj & A)) break;  // does not commute: stay after it
+      }
+      if (j >= 0 && elig[(size_t)j]) pos = (size_t)j + 1;
+    }
+    out.insert(out.begin() + (long)pos, o);
+    elig.insert(elig.begin() + (long)pos, e ? 1 : 0);
+  }
+  sp->ops.swap(out);
+}
+
 void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_local, int da_cost,
                       std::vector<DenseJob>* jobs) {
   const int k = pd->k;
@@ -908,6 +950,7 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
       int rp[4];
       for (int r = 0; r < 4; ++r) rp[r] = sp.sd.regpos[r];
       bind_stage_ops(&sp, rp, pd->R, (int)si, plan, *pd);
+      if (!forward) group_diag_runs(&sp, *pd, plan);
     } else {
       for (DevOp& o : sp.ops) o.stage = (int16_t)si;
     }
@@ -1171,6 +1214,30 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
       r.couter = o.couter;
       r.grad_slot = o.grad_slot;
       plan->rops[i] = r;
+    }
+    // adjoint passes: runs of >= 2 consecutive diagonal ops of a sequential stage without register
+    // controls (their generators purely imaginary diagonals: RZ, RZZ, PS) are evaluated together by
+    // the DUAL kernel (conj(lambda) psi is invariant under diagonal un-applies, so every overlap of
+    // the run uses it; the run's phases are multiplied into per-thread factor tables and applied
+    // once). The first op of a run carries the run length.
+    if (!plan->reverse) continue;
+    for (int si = pd.stage_begin; si < pd.stage_end; ++si) {
+      const StageDesc& S = plan->stages[si];
+      if (S.dense) continue;
+      auto eligible = [&](int i) { return diag_run_eligible(plan->ops[i], pd, plan); };
+      const int b = pd.op_begin + S.op_begin, e = pd.op_begin + S.op_end;
+      for (int i = b; i < e;) {
+        int j = i;
+        while (j < e && eligible(j)) ++j;
+        if (j - i >= g_diag_run_min) {
+          plan->rops[i].pad = (uint16_t)std::min(j - i, 65535);
+          static const bool dbg = std::getenv("SV_PLAN_DEBUG") != nullptr;
+          if (dbg) std::fprintf(stderr, "diag run: pass %d stage %d ops %d\n", (int)(&pd - plan->passes.data()), si, j - i);
+          i = std::min(j, i + 65535);
+        } else {
+          i = j + 1;
+        }
+      }
     }
   }
 }

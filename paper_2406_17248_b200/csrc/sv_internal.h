@@ -138,7 +138,7 @@ struct RegOp {
   uint16_t cthr;       // control bits on thread positions (tile-position space)
   int16_t grad_local;  // index among the pass' grad ops, -1 none
   uint8_t qa, qb;      // physical qubits (outer target bits of diagonal ops)
-  uint16_t pad;
+  uint16_t pad;        // adjoint passes: length of the diagonal run this op starts (0: none)
   uint64_t couter;     // control bits outside the tile (local physical index space)
   int32_t grad_slot;   // global adjoint slot (-1 none)
   uint32_t pad2;
