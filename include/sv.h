@@ -120,6 +120,9 @@ typedef struct {
   int64_t gate_applications;     /* instrumented cost counter: gate-vector
                                     applications the executed plans performed — a forward plan of N
                                     gates adds N, an adjoint plan 2N (psi and lambda)             */
+  int64_t plan_builds;           /* host plans built from scratch                                  */
+  int64_t plan_refreshes;        /* host plans reused by structure with new matrix values (new
+                                    angles of the same circuit: passes and stages kept)          */
 } sv_stats;
 
 /* Option keys for sv_set_option (A/B evidence; defaults are the tuned values). */

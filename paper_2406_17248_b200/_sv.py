@@ -46,7 +46,8 @@ class sv_stats(ctypes.Structure):  # include/sv.h
                 ("adjoint_passes", ctypes.c_int64), ("expectation_passes", ctypes.c_int64),
                 ("exchanges", ctypes.c_int64), ("algorithmic_bytes", ctypes.c_double),
                 ("gates_applied", ctypes.c_int64), ("exchange_bytes", ctypes.c_double),
-                ("exchange_ms", ctypes.c_double), ("gate_applications", ctypes.c_int64)]
+                ("exchange_ms", ctypes.c_double), ("gate_applications", ctypes.c_int64),
+                ("plan_builds", ctypes.c_int64), ("plan_refreshes", ctypes.c_int64)]
 
 
 class sv_pass_info(ctypes.Structure):

@@ -177,6 +177,25 @@ static CachedPlan* plan_slot(sv_state_s* h) {
 
 static int upload_plan(sv_state_s* h, CachedPlan* c, uint64_t key, const CachedPlan** out);
 
+// The structure of a circuit: everything planning decisions depend on except matrix values (the
+// angles of an optimiser step, user matrices): class, kind, qubits, controls, parameter slot,
+// chain-rule coefficient, generator size.
+static std::vector<int64_t> struct_ident(const std::vector<BoundGate>& gates, const PlanMeta& meta) {
+  std::vector<int64_t> v;
+  v.reserve(gates.size() * 7 + 10);
+  for (const BoundGate& g : gates) {
+    int64_t cb;
+    std::memcpy(&cb, &g.coeff, 8);
+    v.push_back(((int64_t)g.cls << 32) | (uint32_t)g.kind);
+    v.push_back(((int64_t)g.t0 << 32) | (uint32_t)g.t1);
+    v.push_back((int64_t)g.controls);
+    v.push_back(((int64_t)g.param << 32) | (uint32_t)g.gen_dim);
+    v.push_back(cb);
+  }
+  for (int m : meta.v) v.push_back(m);
+  return v;
+}
+
 int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, const CachedPlan** out) {
   const PlanMeta meta = plan_meta(h, gates, reverse);
   const uint64_t key = plan_key(gates, meta);
@@ -186,15 +205,32 @@ int get_plan(sv_state_s* h, const std::vector<BoundGate>& gates, bool reverse, c
       *out = c;
       return SV_OK;
     }
-  CachedPlan* c = plan_slot(h);
-  c->key = 0;
-  {
+  auto set_ident = [&](CachedPlan* c) {
     const size_t gb = gates.size() * sizeof(BoundGate);
     c->ident.resize(gb + sizeof(meta));
     std::memcpy(c->ident.data(), gates.data(), gb);
     std::memcpy(c->ident.data() + gb, &meta, sizeof(meta));
-  }
+  };
+  // same structure, new values (an optimiser step): refresh that plan's matrices in place
+  std::vector<int64_t> sid = struct_ident(gates, meta);
+  const uint64_t skey = hash_bytes(sid.data(), sid.size() * 8, 0x5bd1e995ull);
+  static const bool no_refresh = std::getenv("SV_PLAN_REFRESH") && std::atoi(std::getenv("SV_PLAN_REFRESH")) == 0;
+  if (!no_refresh)
+    for (CachedPlan* c : h->plan_cache)
+      if (c->key != 0 && c->skey == skey && c->sident == sid) {
+        c->key = 0;
+        set_ident(c);
+        refresh_plan(gates, &c->plan);
+        h->stats.plan_refreshes += 1;
+        return upload_plan(h, c, key, out);
+      }
+  CachedPlan* c = plan_slot(h);
+  c->key = 0;
+  set_ident(c);
+  c->skey = skey;
+  c->sident.swap(sid);
   build_plan(gates, h->n_local, h->opts, reverse, &c->plan);
+  h->stats.plan_builds += 1;
   return upload_plan(h, c, key, out);
 }
 

@@ -26,6 +26,9 @@
 #include "sv_internal.h"
 
 namespace sv {
+
+void emit_rops(Plan* plan);  // below (compact register-kernel op codes)
+
 namespace {
 
 inline int popc(uint64_t x) { return __builtin_popcountll(x); }
@@ -562,6 +565,12 @@ struct DenseJob {
   int m_tile = 0, m_outer = 0;
   int da = -1;  // adjoint dense stage: index in plan->da whose B matrices this job also fills
 };
+
+}  // namespace
+struct PlanJobs {
+  std::vector<DenseJob> jobs;
+};
+namespace {
 
 // B_{j,v} = V^dagger (Pi_C G_j) V for variant v of an adjoint dense stage (V: product of the
 // stage's ops before its j-th parametrised op, register space).
@@ -1141,6 +1150,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
         }
         pd.n_grad++;
       }
+      op.src = gi;
       plan->ops.push_back(op);
     }
     pd.op_end = (int)plan->ops.size();
@@ -1167,7 +1177,41 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
   lap("emitted");
   fill_dense_variants(plan, jobs);
   lap("dense variants");
-  // compact register-kernel ops
+  emit_rops(plan);
+  plan->jobs = std::make_shared<PlanJobs>();
+  plan->jobs->jobs = std::move(jobs);
+}
+
+// (matrix entries of one op, in the emission layout of build_plan)
+static void write_op_mats(double* dst, const BoundGate& g) {
+  auto put = [&](int& k, Cx c) { dst[k++] = c.re; dst[k++] = c.im; };
+  int k = 0;
+  switch (g.cls) {
+    case GC_GEN1: for (int e = 0; e < 4; ++e) put(k, g.m[e]); break;
+    case GC_XLIKE: put(k, g.m[0]); put(k, g.m[1]); break;
+    case GC_ZLIKE: put(k, g.m[0]); put(k, g.m[1]); break;
+    case GC_GEN2: for (int e = 0; e < 16; ++e) put(k, g.m[e]); break;
+    case GC_DIAG2: for (int e = 0; e < 4; ++e) put(k, g.m[e]); break;
+    default: break;
+  }
+}
+
+void refresh_plan(const std::vector<BoundGate>& gates, Plan* plan) {
+  for (const PassDesc& pd : plan->passes)
+    for (int i = pd.op_begin; i < pd.op_end; ++i) {
+      const DevOp& o = plan->ops[i];
+      const BoundGate g = plan->reverse ? dagger(gates[(size_t)o.src]) : gates[(size_t)o.src];
+      write_op_mats(plan->mats.data() + pd.mat_begin + o.mat_off, g);
+    }
+  if (plan->jobs) {
+    // the jobs hold copies of their ops; their matrices are read from plan->mats
+    fill_dense_variants(plan, plan->jobs->jobs);
+  }
+  emit_rops(plan);
+}
+
+// compact register-kernel ops (value-dependent codes: fast diagonal flags, RX / RY, diagonal runs)
+void emit_rops(Plan* plan) {
   plan->rops.assign(plan->ops.size(), RegOp{});
   for (const PassDesc& pd : plan->passes) {
     if (pd.R == 0) continue;

@@ -39,6 +39,8 @@ struct CachedPlan {
   uint64_t key = 0;
   std::vector<unsigned char> ident;  // the bound gates' bytes + planning meta: a hash hit is verified
                                      // by comparing these (no silent reuse on a 64-bit collision)
+  uint64_t skey = 0;                 // structural key (gates without their matrix values)
+  std::vector<int64_t> sident;       // structural identity, verified on a structural hit
   uint64_t stamp = 0;
   Plan plan;
   DevBuf buf;

@@ -83,6 +83,7 @@ struct DevOp {
   int16_t gen_diag;    // 1: generator diagonal (entries gen_off[0..gen_dim)), evaluated per element
   int16_t stage;       // register-kernel: stage index within the pass
   int16_t grad_local;  // index among the pass' grad ops (-1 none)
+  int32_t src;         // index of the bound gate the op applies (plan refresh with new angles)
   uint64_t ctile;      // control bits in tile-position space
   uint64_t cthr;       // register-kernel: control bits on the thread-bit positions of the op's stage
   uint64_t couter;     // control bits in local physical index space, outside the tile
@@ -179,6 +180,7 @@ struct NoInitAlloc : std::allocator<T> {
   void construct(U* p, A&&... a) { ::new (static_cast<void*>(p)) U(std::forward<A>(a)...); }
 };
 
+struct PlanJobs;  // plan.cpp: the deferred dense-stage fills, kept for refresh_plan
 struct Plan {
   std::vector<PassDesc> passes;
   std::vector<DevOp> ops;
@@ -205,6 +207,7 @@ struct Plan {
   mutable int grid_cache = 0, grid_cache_n = -1;  // plan_grid memo (occupancy query once per plan)
   mutable std::vector<int> pass_grid;             // per-pass CTAs (register passes: occupancy of that pass)
   mutable std::vector<uint8_t> pass_acc;          // adjoint passes: 1 = per-thread overlap accumulators
+  std::shared_ptr<PlanJobs> jobs;                 // dense-variant / adjoint-B fills (re-run on refresh)
 };
 constexpr int kMaxDAPerPass = 4;  // adjoint dense stages per pass (16 KiB of R accumulators each at 2^10 tiles; measured best, profiles/r01_da_per_pass_sweep.txt)
 
@@ -243,6 +246,12 @@ int choose_tile_qubits(int n_local, const PlanOptions& o, bool dual);
 void host_parallel_for(int n, const std::function<void(int)>& f);
 void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOptions& o, bool reverse_for_adjoint,
                 Plan* plan);
+// Structural reuse: `plan` was built by build_plan for gates of the same structure (kinds, qubits,
+// controls, parameter slots) — only matrix VALUES differ (new angles, new user matrices). Rewrites
+// every op's matrix from `gates`, re-fills the dense-stage variants and adjoint B matrices, and
+// re-derives the value-dependent op codes (fast diagonal flags, RX / RY forms, diagonal runs).
+// The pass / stage / layout decisions are kept (they stay correct for any values).
+void refresh_plan(const std::vector<BoundGate>& gates, Plan* plan);
 // FP64 FMAs per amplitude of pass i of a plan (dense stages 64, sequential ops by class).
 int pass_fma_per_amp(const Plan& plan, size_t i);
 

@@ -393,3 +393,32 @@ def test_adjoint_cost_contract(P):
         assert st["gate_applications"] == 3 * N, (nparam, st["gate_applications"], N)
         seen.add((st["gate_passes"], st["adjoint_passes"]))
     assert len(seen) == 1, seen  # pass counts do not grow with P
+
+
+def test_structural_plan_refresh(P):
+    """An optimiser loop re-evaluates one circuit structure with new angles: the library reuses the
+    cached plan's passes and stages and rewrites only its matrices (sv_stats.plan_refreshes). Every
+    evaluation must equal the oracle's — including angles that flip value-dependent fast paths
+    (RZ(0) = identity diagonal, RX(0)), dense stages (C4-shaped 1q matrices) and adjoint plans."""
+    w = W.qaoa(16, 3, seed_graph=3, seed_angles=4, dc=True)
+    sv = P.StateVector(16)
+    P.sv_reset_stats(sv.h)
+    for r, p in enumerate([w.params, w.params * 0.5 + 0.1, np.zeros_like(w.params), w.params[::-1].copy()]):
+        E, g = sv.expectation_with_grad(w.gates, p, w.ham)
+        E0, g0 = oracle.adjoint_grad(16, w.gates, p, w.ham)
+        assert abs(E - E0) < 1e-9 and np.max(np.abs(g - g0)) < 1e-9, r
+    st = sv.stats()
+    assert st["plan_refreshes"] >= 6 and st["plan_builds"] == 2, st  # forward + adjoint built once
+    sv.close()
+    # forward: the same C4-shaped structure with new Haar matrices (dense-stage variants re-filled)
+    a = W.random_circuit(18, 6, seed=1)
+    b = W.random_circuit(18, 6, seed=2)
+    sv = P.StateVector(18)
+    sv.apply_circuit(a.gates)
+    sv.reset()
+    sv.apply_circuit(b.gates)
+    got = sv.get_state()
+    st = sv.stats()
+    sv.close()
+    assert st["plan_refreshes"] >= 1
+    assert np.max(np.abs(got - oracle.apply_circuit(18, b.gates))) <= 1e-10
