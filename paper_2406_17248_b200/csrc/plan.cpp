@@ -1202,6 +1202,14 @@ void refresh_plan(const std::vector<BoundGate>& gates, Plan* plan) {
       const DevOp& o = plan->ops[i];
       const BoundGate g = plan->reverse ? dagger(gates[(size_t)o.src]) : gates[(size_t)o.src];
       write_op_mats(plan->mats.data() + pd.mat_begin + o.mat_off, g);
+      if (o.grad_slot >= 0) {  // generators can carry values too (sharded shards fold rank-bit signs)
+        double* gm = plan->mats.data() + pd.mat_begin + o.gen_off;
+        int k = 0;
+        if (o.gen_diag)
+          for (int j = 0; j < g.gen_dim; ++j) { gm[k++] = g.gen[j * g.gen_dim + j].re; gm[k++] = g.gen[j * g.gen_dim + j].im; }
+        else
+          for (int e = 0; e < g.gen_dim * g.gen_dim; ++e) { gm[k++] = g.gen[e].re; gm[k++] = g.gen[e].im; }
+      }
     }
   if (plan->jobs) {
     // the jobs hold copies of their ops; their matrices are read from plan->mats
