@@ -258,6 +258,7 @@ def run_grad_config(args, P, torch):
             out = step(args.warmup + i)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / args.steps
+    st = P.sv_get_stats(sv.h)  # the timed (moving-parameter) steps only
     # the same evaluation with unchanged parameters (plans reused from the handle's cache)
     step(0, moving=False)
     torch.cuda.synchronize()
@@ -266,7 +267,6 @@ def run_grad_config(args, P, torch):
         step(0, moving=False)
     torch.cuda.synchronize()
     dt_fixed = (time.perf_counter() - t0) / args.steps
-    st = P.sv_get_stats(sv.h)
     evals = rows.shape[0] if rows is not None else 1
     line = {"metric": "expectation + adjoint-gradient evaluations per second", "value": evals / dt,
             "unit": "grad evals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt,

@@ -1,4 +1,4 @@
-# usage: bash tools/exp_grad.sh TAG  -> appends C2/C3/C4g grad evals/s lines to gpurun_out/exp_grad.txt
+# usage: bash tools/experiments/exp_grad.sh TAG  -> appends C2/C3/C4g grad evals/s lines to gpurun_out/exp_grad.txt
 set -u
 mkdir -p gpurun_out
 for cfg in C2 C3 C4g; do
