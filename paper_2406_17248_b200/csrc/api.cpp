@@ -1074,6 +1074,7 @@ sv_status sv_apply_gate(sv_handle h, const sv_gate* g, const double* params, int
 }
 
 sv_status sv_apply_circuit(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params, int32_t n_params) {
+  NvtxRange nvtx("sv_apply_circuit");
   int rc = check_handle(h);
   if (rc) return rc;
   DeviceGuard dev_guard(h->device);
@@ -1086,6 +1087,7 @@ sv_status sv_apply_circuit(sv_handle h, const sv_gate* gates, int64_t n_gates, c
 }
 
 sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, double* out_value) {
+  NvtxRange nvtx("sv_expectation");
   int rc = check_handle(h);
   if (rc) return rc;
   DeviceGuard dev_guard(h->device);
@@ -1156,6 +1158,7 @@ sv_status sv_expectation(sv_handle h, const sv_pauli* terms, int64_t n_terms, do
 sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_gates, const double* params,
                                    int32_t n_params, const sv_pauli* terms, int64_t n_terms, double* out_value,
                                    double* out_grad) {
+  NvtxRange nvtx("sv_expectation_with_grad");
   int rc = check_handle(h);
   if (rc) return rc;
   DeviceGuard dev_guard(h->device);
@@ -1189,7 +1192,10 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
   rc = get_plan(h, bg, false, &fwdp);
   if (rc) return rc;
   lap("fwd plan");
-  rc = run_plan(h, *fwdp, psi, nullptr, nullptr, 0, nullptr, nullptr);
+  {
+    NvtxRange r("forward");
+    rc = run_plan(h, *fwdp, psi, nullptr, nullptr, 0, nullptr, nullptr);
+  }
   if (rc) return rc;
   lap("fwd launched");
   h->stats.gates_applied += (int64_t)bg.size();
@@ -1203,7 +1209,10 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
     const size_t ng = G.xs.size();
     if (!h->d_partials.ensure(ng * pgrid * 8 + 8) || !h->d_out.ensure(ng * 8 + 8)) return fail(SV_E_OOM, "partials");
     int nslots = 0;
-    rc = run_groups(h, G, psi, lam, static_cast<double*>(h->d_partials.p), pgrid, &nslots);
+    {
+      NvtxRange r("lambda = H psi");
+      rc = run_groups(h, G, psi, lam, static_cast<double*>(h->d_partials.p), pgrid, &nslots);
+    }
     if (rc) return rc;
     e = launch_reduce_slots(static_cast<double*>(h->d_partials.p), nslots, pgrid, static_cast<double*>(h->d_out.p),
                             h->stream);
@@ -1221,7 +1230,10 @@ sv_status sv_expectation_with_grad(sv_handle h, const sv_gate* gates, int64_t n_
     rc = get_plan(h, bg, true, &revp);
     if (rc) return rc;
     lap("rev plan");
-    rc = run_reverse(h, *revp, psi, lam, &d);
+    {
+      NvtxRange r("adjoint sweep");
+      rc = run_reverse(h, *revp, psi, lam, &d);
+    }
     if (rc) return rc;
     lap("reverse done");
     e = cudaStreamSynchronize(h->stream);

@@ -324,6 +324,7 @@ int swap_qubits(sv_state_s* h, const std::vector<std::vector<double*>>& vecs, in
   const int nl = h->n_local;
   const int j = G - nl;
   h->stats.exchanges += 1;
+  NvtxRange nvtx("qubit swap exchange");
   XTimer timer(h);
   const int64_t half = int64_t(1) << (nl - 1);
   // SV_VIRTUAL_BOUNCE=<chunk amplitudes>: virtual shards exchange through the NCCL transport's

@@ -6,10 +6,19 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler attaches
+
 #include "sv.h"
 #include "sv_internal.h"
 
 namespace sv {
+
+// NVTX range around a phase of an entry point (forward plan, lambda, adjoint sweep, exchanges):
+// visible in nsys / ncu range filters, free otherwise.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct DevBuf {
   void* p = nullptr;
