@@ -33,6 +33,12 @@
 #ifndef SV_DUAL_CTAS
 #define SV_DUAL_CTAS 3  // adjoint-pass (2^10-tile, 128-thread) CTAs per SM (register cap 65536 / (128 * 3))
 #endif
+#ifndef SV_FWD_CTRL_SPLIT
+#define SV_FWD_CTRL_SPLIT 0  // 1: forward register passes get separate code for ops with / without register controls
+#endif
+#ifndef SV_DUAL_CTRL_SPLIT
+#define SV_DUAL_CTRL_SPLIT 0  // 1: separate DUAL op code for ops with / without register controls
+#endif
 #ifndef SV_DUAL_SINGLE_BUF
 #define SV_DUAL_SINGLE_BUF 0  // 1: every adjoint pass single-buffers its tile (more CTAs per SM)
 #endif
@@ -424,8 +430,12 @@ __device__ __forceinline__ void reg_apply_c(double2 (&v)[1 << NR], const Op& o, 
 template <int NR>
 __device__ __forceinline__ void reg_apply(double2 (&v)[1 << NR], const Op& o, const double2* m, uint32_t tthr,
                                           uint64_t base) {
+#if SV_FWD_CTRL_SPLIT
   if (o.cj()) reg_apply_c<NR, true>(v, o, m, tthr, base);
   else reg_apply_c<NR, false>(v, o, m, tthr, base);
+#else
+  reg_apply_c<NR, true>(v, o, m, tthr, base);  // one instantiation (cj = 0 never skips)
+#endif
 }
 
 template <int NR, bool CTRL>
@@ -1131,8 +1141,14 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
         const double2* m = mats2 + o.mat_off();
         if constexpr (DUAL) {
           const double2* g = mats2 + o.gen_off();
+#if SV_DUAL_CTRL_SPLIT
           double part = o.cj() ? dual_op_c<NR, true>(v, w, o, m, g, tthr, base, ok)
                                : dual_op_c<NR, false>(v, w, o, m, g, tthr, base, ok);
+#else
+          // one instantiation (register controls tested per amplitude; cj = 0 never skips): half the
+          // DUAL code size (instruction-cache misses) and one switch join for v / w
+          double part = dual_op_c<NR, true>(v, w, o, m, g, tthr, base, ok);
+#endif
           if (o.gen()) {
             if (a.acc_thread) {
               s_acc[o.grad_local() * nthr + tid] += part;  // this thread's running sum over its tiles
