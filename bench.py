@@ -69,8 +69,12 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML from a thread (first sample
+    at entry, then every 20 ms, and one more at exit, so even a millisecond region has a reading);
+    `nvidia-smi -lms` as the fallback when pynvml is missing."""
 
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -78,18 +82,69 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.rows = []
+        self.out = ""
+
+    def _bus_id(self):
+        """PCI bus id of CUDA device `index` (NVML enumerates every GPU of the host, whatever
+        CUDA_VISIBLE_DEVICES selects)."""
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            return f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        except Exception:
+            return None
+
+    def _nvml_sample(self):
+        import pynvml
+        sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.rows.append((float(sm), float(mx), r))
 
     def __enter__(self):
+        import threading
+        self.rows = []
+        self.nvml = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            bus = self._bus_id()
+            self.h = (pynvml.nvmlDeviceGetHandleByPciBusId(bus) if bus else
+                      pynvml.nvmlDeviceGetHandleByIndex(self.index))
+            self._nvml_sample()  # the first reading, taken as the region starts
+            self.nvml = True
+            self.stop = threading.Event()
+
+            def loop():
+                while not self.stop.wait(0.02):
+                    try:
+                        self._nvml_sample()
+                    except Exception:
+                        return
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = False
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                ["nvidia-smi", "-i", self._bus_id() or str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits",
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        if self.nvml:
+            try:
+                self._nvml_sample()  # and one as it ends (before the caller's next work)
+            except Exception:
+                pass
+            self.stop.set()
+            self.thread.join(timeout=1)
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -98,8 +153,13 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.rows:
+            reasons = sorted({name for (_, _, r) in self.rows for name, bit in self.REASONS if r & bit})
+            return {"sm_mhz": float(np.median([r[0] for r in self.rows])),
+                    "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons, "samples": len(self.rows),
+                    "source": "nvml"}
         rows = []
-        for line in (getattr(self, "out", "") or "").splitlines():
+        for line in (self.out or "").splitlines():
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -112,7 +172,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[j] for r in rows for j in range(4) if r[2 + j].lower().startswith("active")})
         return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": "nvidia-smi"}
 
 
 def _ham_terms(ham):
@@ -252,12 +312,18 @@ def run_grad_config(args, P, torch):
         step(i)
     torch.cuda.synchronize()
     P.sv_reset_stats(sv.h)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         t0 = time.perf_counter()
+        e0.record(stream)
         for i in range(args.steps):
             out = step(args.warmup + i)
+        e1.record(stream)
         torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) / args.steps
+        dt_wall = (time.perf_counter() - t0) / args.steps
+    # value: device time on the handle's stream (CUDA events); e2e: host wall clock around the same
+    # public calls (each one uploads its parameters and reads E and the gradient back, synchronously)
+    dt = e0.elapsed_time(e1) / 1e3 / args.steps
     st = P.sv_get_stats(sv.h)  # the timed (moving-parameter) steps only
     # the same evaluation with unchanged parameters (plans reused from the handle's cache)
     step(0, moving=False)
@@ -278,7 +344,7 @@ def run_grad_config(args, P, torch):
             "fixed_params_value": evals / dt_fixed,
             "launches_per_eval": int(st["kernel_launches"]) / max(1, args.steps),
             "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
-            "e2e": {"value": evals / dt, "unit": "grad evals/s (host call incl.)",
+            "e2e": {"value": evals / dt_wall, "unit": "grad evals/s",
                     "h2d_bytes_per_step": int(ga.nbytes + pa.nbytes + (rows.nbytes if rows is not None else w.params.nbytes)),
                     "d2h_bytes_per_step": int(8 * evals * (1 + len(w.params)))}}
     if not args.no_cpu_baseline:
@@ -312,11 +378,13 @@ def run_density_config(args, P, torch):
     P.sv_reset_stats(dm.h)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
+        t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
             E = step()
         e1.record(stream)
         torch.cuda.synchronize()
+        ms_wall = 1e3 * (time.perf_counter() - t0) / args.steps
     ms = e0.elapsed_time(e1) / args.steps
     st = P.sv_get_stats(dm.h)
     line = {"metric": "density-matrix gates/sec (rho <- U rho U^dagger) + tr(rho H)", "value": len(w.gates) / (ms / 1e3),
@@ -326,7 +394,7 @@ def run_density_config(args, P, torch):
                                                       "C4 generator depth 40, 50-term JW H", "n_qubits": n,
                                             "gates": len(w.gates)},
             "E": E, "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
-            "e2e": {"value": len(w.gates) / (ms / 1e3), "unit": "gates/s", "h2d_bytes_per_step": int(ga.nbytes + pa.nbytes),
+            "e2e": {"value": len(w.gates) / (ms_wall / 1e3), "unit": "gates/s", "h2d_bytes_per_step": int(ga.nbytes + pa.nbytes),
                     "d2h_bytes_per_step": 8}}
     print(json.dumps(line), flush=True)
     dm.close()
@@ -474,15 +542,19 @@ def main():
     roof = None
     if shards == 1:
         plan = P.sv_plan_info(n, ga, w.params)
-        fma_per_amp = sum(p["fma_per_amp"] for p in plan)
-        fp64_flops = 2.0 * fma_per_amp * amps  # algorithmic FP64 work of the executed plan
+        # FP64 work of the executed plan: 2 flops per FMA (dense stages: 48 per amplitude, three
+        # real products per complex entry) + the Gauss sums (3 DADDs per amplitude and dense stage)
         c64 = args.precision == "c64"
+        # (complex64: the TF32 dense stages run the four-product form, 64 FMAs per amplitude)
+        pass_flops = [(2.0 * (p["fma_per_amp"] + 16 * p["n_dense"]) if c64 else
+                       2.0 * p["fma_per_amp"] + p["add_per_amp"]) * amps for p in plan]
+        fp64_flops = sum(pass_flops)
         # complex64: the dense stages run TF32 MMAs with a 3-term split, so the peak for the
         # algorithmic (complex matrix-vector) flops is the measured TF32 mma.sync rate / 3
         peak = TF32_SPLIT_PEAK_TFLOPS if c64 else fp64_peak
         # t_roof = sum over passes of max(bytes / BW, FP64 flops / rate)
         bw = hbm_peak * 1e9
-        t_roof = sum(max(pass_bytes / bw, 2.0 * p["fma_per_amp"] * amps / (peak * 1e12)) for p in plan)
+        t_roof = sum(max(pass_bytes / bw, f / (peak * 1e12)) for f in pass_flops)
         roof = {
             "bound": "tensor",
             "kernel": ("k_pass_c64 (complex64 tiles; dense stages on TF32 tensor cores, 3-term split; register stages)"

@@ -26,8 +26,8 @@ typedef struct {
   int32_t n_dense;      /* stages executed as dense FP64-MMA stages                              */
   int32_t mat_doubles;  /* matrix data of the pass (doubles)                                     */
   int32_t fma_per_amp;  /* FP64 fused multiply-adds per amplitude the pass executes (dense stages   */
-                        /* 64 each; sequential ops by class) — the roofline's algorithmic work     */
-  int32_t pad;
+                        /* 48 each: three real products per complex entry; sequential ops by class) */
+  int32_t add_per_amp;  /* FP64 additions per amplitude besides them (dense stages: 3)             */
 } sv_pass_info;
 
 /* Plans `gates` for an n-qubit single-GPU state exactly as sv_apply_circuit (adjoint = 0) or the

@@ -54,7 +54,7 @@ class sv_pass_info(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("low", ctypes.c_int32), ("R", ctypes.c_int32), ("n_ops", ctypes.c_int32),
                 ("n_stages", ctypes.c_int32), ("n_grad", ctypes.c_int32), ("tile_mask", ctypes.c_uint64),
                 ("nondiag_mask", ctypes.c_uint64), ("n_dense", ctypes.c_int32), ("mat_doubles", ctypes.c_int32),
-                ("fma_per_amp", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("fma_per_amp", ctypes.c_int32), ("add_per_amp", ctypes.c_int32)]
 
 
 class sv_shard_step(ctypes.Structure):

@@ -1384,7 +1384,7 @@ extern "C" sv_status sv_plan_info(int32_t n_qubits, const sv_gate* gates, int64_
     for (int si = pd.stage_begin; si < pd.stage_end; ++si) r.n_dense += plan.stages[si].dense ? 1 : 0;
     r.mat_doubles = (int32_t)(((i + 1 < plan.passes.size()) ? plan.passes[i + 1].mat_begin : (int)plan.mats.size()) - pd.mat_begin);
     r.fma_per_amp = pass_fma_per_amp(plan, i);
-    r.pad = 0;
+    r.add_per_amp = pass_add_per_amp(plan, i);
     r.nondiag_mask = 0;
     for (int j = pd.op_begin; j < pd.op_end; ++j) {
       const DevOp& op = plan.ops[j];

@@ -27,8 +27,27 @@
 #include "cx.cuh"
 #include "sv_internal.h"
 
+#ifndef SV_DENSE_CTAS
+#define SV_DENSE_CTAS 2  // k_pass_dense CTAs per SM (128 registers: the Gauss form's live set)
+#endif
+#ifndef SV_DENSE_NBUF
+#define SV_DENSE_NBUF 2  // k_pass_dense tile ring depth (3: no gain measured)
+#endif
+#ifndef SV_DENSE_XOR_ADDR
+#define SV_DENSE_XOR_ADDR 1
+#endif
+#ifndef SV_DENSE_VT
+#define SV_DENSE_VT 1
+#endif
+#ifndef SV_DA_R_3M
+#define SV_DA_R_3M 1  // adjoint dense stages: R = sum psi lambda^H with three real products
+#endif
 #ifndef SV_FWD_CTAS
-#define SV_FWD_CTAS 3   // forward-pass CTAs per SM (register budget 65536 / (256 * CTAs))
+#define SV_FWD_CTAS 2   // forward register passes: CTAs per SM (register budget 65536 / (256 * CTAs));
+                        // 2 (128 registers) fits the dense stages' Gauss live set (3: 80, spills)
+#endif
+#ifndef SV_C64_CTAS
+#define SV_C64_CTAS 3   // complex64 forward passes
 #endif
 #ifndef SV_DUAL_CTAS
 #define SV_DUAL_CTAS 3  // adjoint-pass (2^10-tile, 128-thread) CTAs per SM (register cap 65536 / (128 * 3))
@@ -117,6 +136,15 @@ __device__ __forceinline__ Op load_op(const RegOp* p) {
   o.w3 = a.w;
   o.couter = (uint64_t)b.x | ((uint64_t)b.y << 32);
   return o;
+}
+
+// 16-byte aligned pointer into the dynamic shared block, derived from smem_raw by a byte offset
+// (not through an integer round trip, which would hide the shared address space from the compiler
+// and turn every access through it into a generic LD / ST)
+template <typename T>
+__device__ __forceinline__ T* smem_align16(unsigned char* smem_raw, const void* after) {
+  const size_t off = (size_t)(reinterpret_cast<const unsigned char*>(after) - smem_raw);
+  return reinterpret_cast<T*>(smem_raw + ((off + 15) & ~size_t(15)));
 }
 
 // ---------------------------------------------------------------- register-resident op kernels
@@ -838,12 +866,18 @@ __device__ __forceinline__ void dual_diag_run(double2 (&v)[8], double2 (&w)[8], 
 
 // ---------------------------------------------------------------- dense FP64-MMA stage
 //
-// The stage's ops were folded on the host into a 16x16 complex matrix U per variant; with
-// X = [Re; Im] of the tile's 2^(k-4) vectors of 16 amplitudes, Y = [[Ur, -Ui], [Ui, Ur]] X is a
-// real 32 x 32 x 2^(k-4) GEMM, run as mma.sync m8n8k4 f64 (DMMA): per warp 4 N-tiles of 8 vectors,
-// 4 M-tiles x 8 K-tiles. Fragment layouts (PTX m8n8k4 .f64): A[r = lane/4][c = lane%4],
-// B[k = lane%4][n = lane/4], D[r = lane/4][c = 2 (lane%4) + {0,1}].
-constexpr uint32_t kDenseRow = 16;  // complex entries per stored variant-matrix row (plan.cpp kDenseStride)
+// The stage's ops were folded on the host into a 16x16 complex matrix U per variant, applied to the
+// tile's 2^(k-4) vectors of 16 amplitudes X as mma.sync m8n8k4 f64 (DMMA) fragments with three
+// real products instead of four (Gauss): with T = Ur (Xr + Xi),
+//   Re Y = T + Cb Xi,  Cb = -(Ur + Ui),      Im Y = T + Cc Xr,  Cc = Ui - Ur,
+// so 48 DMMAs per warp and stage instead of 64, one DADD per input element (Xr + Xi) and two per
+// A entry (Cb, Cc: computed here; stored by the host after U, the extra A loads cost more than the
+// DADDs), and T seeds both chains as the C operand of their first MMA (no output additions).
+// Per warp 2 N-tiles of 8 vectors, 2 M-halves x 4 K-steps; both N-tiles advance together (4 T
+// chains, then 8 Re / Im chains in flight). Fragment layouts (PTX m8n8k4 .f64):
+// A[r = lane/4][c = lane%4], B[k = lane%4][n = lane/4], D[r = lane/4][c = 2 (lane%4) + {0,1}].
+constexpr uint32_t kDenseRow = 16;  // double2 per stored variant-matrix row (plan.cpp kDenseStride)
+constexpr uint32_t kDenseVar = 16u * kDenseRow;  // double2 per variant matrix
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -851,84 +885,129 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// D = A B + C with C and D distinct registers (T seeds the Re and Im chains)
+__device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
 
-// A operand of a dense stage: this warp's variant matrix (global, L2-resident), 8 entries per lane.
-__device__ __forceinline__ void dense_load_a(const StageDesc& S, const double2* __restrict__ gmats2, uint64_t base,
-                                             int warp, int lane, double2 (&ue)[2][4]) {
-  uint32_t var = S.warp_var[warp];
-  for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
-  const double2* U = gmats2 + S.dense_off + var * (16u * kDenseRow);
+// A operand of a dense stage for this lane: 8 entries (rows 8 mh + lane/4, columns 4 kh + lane%4)
+// of the warp's variant matrix U (global, L2-resident)
+struct DenseA {
+  double2 u[2][4];
+};
+
+__device__ __forceinline__ void dense_load_u(const double2* __restrict__ U, int lane, DenseA& A) {
 #pragma unroll
   for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
-    for (int kh = 0; kh < 4; ++kh) ue[mh][kh] = __ldg(U + (8 * mh + (lane >> 2)) * kDenseRow + 4 * kh + (lane & 3));
+    for (int kh = 0; kh < 4; ++kh) {
+      A.u[mh][kh] = __ldg(U + (8 * mh + (lane >> 2)) * kDenseRow + 4 * kh + (lane & 3));
+    }
 }
 
-// warp-owned vectors: 2 N-tiles (n0) x 8 MMA columns (c0 c1 c2); all address parts are
-// host-precomputed swizzled offsets (the swizzle is XOR-linear)
-__device__ __forceinline__ double2 tile_ld(const double2& v) { return v; }
-__device__ __forceinline__ double2 tile_ld(const float2& v) { return make_double2((double)v.x, (double)v.y); }
-__device__ __forceinline__ void tile_st(double2& d, double2 v) { d = v; }
-__device__ __forceinline__ void tile_st(float2& d, double2 v) { d = make_float2((float)v.x, (float)v.y); }
+__device__ __forceinline__ void dense_load_a(const StageDesc& S, const double2* __restrict__ gmats2, uint64_t base,
+                                             int warp, int lane, DenseA& A) {
+  uint32_t var = S.warp_var[warp];
+  for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
+  dense_load_u(gmats2 + S.dense_off + var * kDenseVar, lane, A);
+}
 
-// T: double2 (complex128 tile) or float2 (complex64 tile, NEXT-3: widened to FP64 for the MMAs)
-template <typename T>
-__device__ __forceinline__ void dense_apply_a(T* tp, const StageDesc& S, const double2 (&ue)[2][4], int warp,
-                                              int lane) {
+// 32-bit shared-window accesses: the swizzled offsets are XOR-linear in (nt, kq) and (nt, mh, v),
+// so the 8 load and 8 store offsets are XORs of three basis values each (one LOP3 + one LEA per
+// access)
+__device__ __forceinline__ double2 lds_v2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double x) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(x) : "memory");
+}
+
+__device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, const DenseA& A, int warp, int lane) {
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(tp);
   const uint32_t wsw = S.warp_swz[warp];
-  const uint32_t baseB = wsw ^ S.lane_b[lane];
-  double b[2][8];
+  const uint32_t bB = wsw ^ (uint32_t)S.lane_b[lane], bD = wsw ^ (uint32_t)S.lane_d[lane];
+  const uint32_t Lk0 = S.swz_reg[1], Lk1 = S.swz_reg[2], Ln = S.swz_reg[4];
+  const uint32_t Sv = S.swz_reg[8 + 1], Sm = S.swz_reg[8 + 2], Sn = S.swz_reg[8 + 4];
+  double xr[2][4], xi[2][4];
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int kq = 0; kq < 4; ++kq) {
-      const double2 x = tile_ld(tp[baseB ^ S.swz_reg[nt * 4 + kq]]);
-      b[nt][kq] = x.x;
-      b[nt][kq + 4] = x.y;
+#if SV_DENSE_XOR_ADDR
+      const uint32_t o = bB ^ (nt ? Ln : 0u) ^ ((kq & 1) ? Lk0 : 0u) ^ ((kq & 2) ? Lk1 : 0u);
+      const double2 x = lds_v2(sb + (o << 4));
+#else
+      const double2 x = tp[bB ^ S.swz_reg[nt * 4 + kq]];
+#endif
+      xr[nt][kq] = x.x;
+      xi[nt][kq] = x.y;
     }
-  // ---- D = A B, A = [[Ur, -Ui], [Ui, Ur]] ----
-  double d[4][2][2];
+  double t[2][2][2];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int kh = 0; kh < 4; ++kh)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
+    for (int nt = 0; nt < 2; ++nt) {
+      const double sx = xr[nt][kh] + xi[nt][kh];
 #pragma unroll
-  for (int mh = 0; mh < 2; ++mh) {
+      for (int mh = 0; mh < 2; ++mh) {
+        if (kh == 0) t[nt][mh][0] = t[nt][mh][1] = 0.0;
+        dmma(t[nt][mh][0], t[nt][mh][1], A.u[mh][kh].x, sx);
+      }
+    }
+  double cb[2][4], cc[2][4];
+#pragma unroll
+  for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
     for (int kh = 0; kh < 4; ++kh) {
-      // one complex entry feeds the four (re/im out) x (re/im in) fragments
-      const double2 e = ue[mh][kh];
-      // consecutive MMAs go to four different accumulators (hides the MMA latency)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        dmma(d[mh][nt][0], d[mh][nt][1], e.x, b[nt][kh]);           // Re out += Ur Re in
-        dmma(d[mh + 2][nt][0], d[mh + 2][nt][1], e.y, b[nt][kh]);   // Im out += Ui Re in
-      }
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        dmma(d[mh][nt][0], d[mh][nt][1], -e.y, b[nt][kh + 4]);      // Re out -= Ui Im in
-        dmma(d[mh + 2][nt][0], d[mh + 2][nt][1], e.x, b[nt][kh + 4]); // Im out += Ur Im in
-      }
+      cb[mh][kh] = -(A.u[mh][kh].x + A.u[mh][kh].y);
+      cc[mh][kh] = A.u[mh][kh].y - A.u[mh][kh].x;
     }
-  }
-  // ---- stores: amps j = 8 mh + lane/4 of columns 2 (lane%4) + v ----
-  const uint32_t baseD = wsw ^ S.lane_d[lane];
+  double re[2][2][2], im[2][2][2];
+#pragma unroll
+  for (int kh = 0; kh < 4; ++kh)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int mh = 0; mh < 2; ++mh) {
+        if (kh == 0) {
+          dmma_c(re[nt][mh][0], re[nt][mh][1], cb[mh][0], xi[nt][0], t[nt][mh][0], t[nt][mh][1]);
+          dmma_c(im[nt][mh][0], im[nt][mh][1], cc[mh][0], xr[nt][0], t[nt][mh][0], t[nt][mh][1]);
+        } else {
+          dmma(re[nt][mh][0], re[nt][mh][1], cb[mh][kh], xi[nt][kh]);
+          dmma(im[nt][mh][0], im[nt][mh][1], cc[mh][kh], xr[nt][kh]);
+        }
+      }
+  // stores: amps 8 mh + lane/4 of columns 2 (lane%4) + v, as two 8-byte halves (ptxas fuses them)
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
-      for (int v = 0; v < 2; ++v)
-        tile_st(tp[baseD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]], make_double2(d[mh][nt][v], d[mh + 2][nt][v]));
+      for (int v = 0; v < 2; ++v) {
+#if SV_DENSE_XOR_ADDR
+        const uint32_t a = sb + ((bD ^ (nt ? Sn : 0u) ^ (mh ? Sm : 0u) ^ (v ? Sv : 0u)) << 4);
+        sts_f64(a, re[nt][mh][v]);
+        sts_f64(a + 8, im[nt][mh][v]);
+#else
+        tp[bD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]] = make_double2(re[nt][mh][v], im[nt][mh][v]);
+#endif
+      }
 }
-
 
 __device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, const double2* __restrict__ gmats2,
                                             uint64_t base, int warp, int lane) {
-  double2 ue[2][4];
-  dense_load_a(S, gmats2, base, warp, lane, ue);
-  dense_apply_a(tp, S, ue, warp, lane);
+  DenseA A;
+  dense_load_a(S, gmats2, base, warp, lane, A);
+  dense_apply(tp, S, A, warp, lane);
 }
+
+// complex64 tiles (NEXT-3): widened to FP64 in registers
+__device__ __forceinline__ double2 tile_ld(const float2& v) { return make_double2((double)v.x, (double)v.y); }
+__device__ __forceinline__ void tile_st(float2& d, double2 v) { d = make_float2((float)v.x, (float)v.y); }
 
 // Adjoint dense stage (DUAL): accumulate R = sum_v psi_v lambda_v^H over the warp's 16 vectors at
 // the stage start (FP64 MMAs with K = vectors) into the warp's private shared-memory accumulator,
@@ -949,6 +1028,38 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
       la[mt][kt] = tl[ad];
     }
   double rre[2][2][2], rim[2][2][2];
+#if SV_DA_R_3M
+  // Re R = Pr Lr^T + Pi Li^T, Im R = Pi Lr^T - Pr Li^T with three products (Gauss):
+  // T = (Pr + Pi) Lr^T, Re R = T - Pi (Lr - Li)^T, Im R = T - Pr (Lr + Li)^T
+  double t[2][2][2];
+#pragma unroll
+  for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const double sp = ps[mt][kt].x + ps[mt][kt].y;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        if (kt == 0) t[mt][nt][0] = t[mt][nt][1] = 0.0;
+        dmma(t[mt][nt][0], t[mt][nt][1], sp, la[nt][kt].x);
+      }
+    }
+#pragma unroll
+  for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const double lm = la[nt][kt].x - la[nt][kt].y, lp = la[nt][kt].x + la[nt][kt].y;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (kt == 0) {
+          dmma_c(rre[mt][nt][0], rre[mt][nt][1], -ps[mt][kt].y, lm, t[mt][nt][0], t[mt][nt][1]);
+          dmma_c(rim[mt][nt][0], rim[mt][nt][1], -ps[mt][kt].x, lp, t[mt][nt][0], t[mt][nt][1]);
+        } else {
+          dmma(rre[mt][nt][0], rre[mt][nt][1], -ps[mt][kt].y, lm);
+          dmma(rim[mt][nt][0], rim[mt][nt][1], -ps[mt][kt].x, lp);
+        }
+      }
+    }
+#else
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -965,6 +1076,7 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
         dmma(rre[mt][nt][0], rre[mt][nt][1], ps[mt][kt].y, la[nt][kt].y);
         dmma(rim[mt][nt][0], rim[mt][nt][1], -ps[mt][kt].x, la[nt][kt].y);
       }
+#endif
   // accumulate into the warp's slot: element e = ((mt * 2 + nt) * 2 + comp) * 2 + v, lane-contiguous
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -993,7 +1105,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   double2* tp = smem_tiles;  // (setup-phase alias; the tile loop rebinds per buffer)
   RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + ((DUAL && (a.n_da > 0 || SV_DUAL_SINGLE_BUF)) ? 1 : 2) * NB);
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
-  double* s_mats = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
+  double* s_mats = smem_align16<double>(smem_raw, s_st + a.nstages);
   // tile index -> base offset of its outer qubits: four 64-entry deposit tables (tile bits
   // 6c .. 6c+5 -> their outer qubits), replacing a per-tile loop over n_outer bits
   uint64_t* s_ob = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
@@ -1097,7 +1209,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
           const StageDesc& Sn = s_st[st + S.next_dense];
           uint32_t var = Sn.warp_var[warp];
           for (int b = 0; b < Sn.m_outer; ++b) var |= (uint32_t)((base >> Sn.var_outer[b]) & 1ull) << (Sn.m_tile + b);
-          const double2* U = reinterpret_cast<const double2*>(a.mats) + Sn.dense_off + var * (16u * kDenseRow);
+          const double2* U = reinterpret_cast<const double2*>(a.mats) + Sn.dense_off + var * kDenseVar;
           const double2* q = U + (lane >> 2) * kDenseRow + (lane & 3) * 4;  // one 64-byte line per lane covers 4 entries
           asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q));
           asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q + 8 * kDenseRow));
@@ -1208,13 +1320,17 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
 // leaves room to load the next stage's A operand (its variant matrix, from L2) into registers
 // before the barrier that ends the current stage, and the first stage's before the tile wait:
 // the L2 latency overlaps barrier / load waits instead of stalling the first MMA of every stage.
-__global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __restrict__ psi, RegArgs a) {
+__global__ void __launch_bounds__(256, SV_DENSE_CTAS) k_pass_dense(double2* __restrict__ psi, RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
   const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double2* smem_tiles = reinterpret_cast<double2*>(smem_raw);
-  StageDesc* s_st = reinterpret_cast<StageDesc*>(smem_tiles + 2 * N);
-  uint64_t* s_ob = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
+  StageDesc* s_st = reinterpret_cast<StageDesc*>(smem_tiles + SV_DENSE_NBUF * N);
+  uint64_t* s_ob = smem_align16<uint64_t>(smem_raw, s_st + a.nstages);
+  // per stage, the variant-matrix offset contributed by the tile index: four 64-entry deposit
+  // tables (tile bits 6c .. 6c+5 -> their outer qubits -> variant bits), so a stage's A operand
+  // address costs four shared loads instead of a loop over its outer variant qubits
+  uint32_t* s_vt = reinterpret_cast<uint32_t*>(s_ob + 4 * 64);
   {
     const uint64_t* ss = reinterpret_cast<const uint64_t*>(a.stages);
     uint64_t* sd = reinterpret_cast<uint64_t*>(s_st);
@@ -1226,6 +1342,19 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
         if (((h >> b) & 1) && j < a.n_outer) off |= 1ull << a.oq[j];
       }
       s_ob[h] = off;
+    }
+    for (int e = tid; e < a.nstages * 256; e += nthr) {
+      const StageDesc& S = *reinterpret_cast<const StageDesc*>(reinterpret_cast<const uint64_t*>(a.stages) +
+                                                               (e >> 8) * (int)(sizeof(StageDesc) / 8));
+      const int h = e & 255;
+      uint32_t var = 0;
+      for (int b = 0; b < 6; ++b) {
+        const int jt = (h >> 6) * 6 + b;
+        if (!((h >> b) & 1) || jt >= a.n_outer) continue;
+        for (int t = 0; t < S.m_outer; ++t)
+          if (S.var_outer[t] == a.oq[jt]) var |= 1u << (S.m_tile + t);
+      }
+      s_vt[e] = ((h >> 6) == 0 ? S.dense_off : 0u) + var * kDenseVar;  // summed over the 4 tables
     }
   }
   __syncthreads();
@@ -1242,35 +1371,56 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
       if ((tile >> j) & 1) base |= 1ull << a.oq[j];
     return base;
   };
+  // a ring of SV_DENSE_NBUF tile buffers: tile i + NBUF - 1 streams in while tile i computes (every
+  // iteration commits one cp.async group, empty past the end, so the wait count is constant)
   auto issue_load = [&](int64_t tile, int buf) {
-    const uint64_t bt = tile_base(tile) | dep_t;
-    double2* dp = smem_tiles + (size_t)buf * N;
+    if (tile < a.ntiles) {
+      const uint64_t bt = tile_base(tile) | dep_t;
+      double2* dp = smem_tiles + (size_t)buf * N;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) cp_async16(dp + (swz_t ^ a.zsub[i]), psi + (bt | a.hsub[i]));
+      for (int i = 0; i < 8; ++i) cp_async16(dp + (swz_t ^ a.zsub[i]), psi + (bt | a.hsub[i]));
+    }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  if ((int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
-  double2 ue[2][4];
-  int it = 0;
-  if ((int64_t)blockIdx.x < a.ntiles) dense_load_a(s_st[0], gm2, tile_base(blockIdx.x), warp, lane, ue);
+#pragma unroll
+  for (int j = 0; j < SV_DENSE_NBUF - 1; ++j) issue_load(blockIdx.x + (int64_t)j * gridDim.x, j);
+  DenseA ue;
+  int it = 0, cur = 0;
+  // A operand of stage st for a tile: warp part + tile part (tables; outer bits past 24 by loop)
+  auto load_a = [&](int st, int64_t tile, uint64_t base) {
+    const StageDesc& S = s_st[st];
+    const uint32_t* vt = s_vt + st * 256;
+    uint32_t off = vt[tile & 63] + vt[64 + ((tile >> 6) & 63)] + vt[128 + ((tile >> 12) & 63)] +
+                   vt[192 + ((tile >> 18) & 63)];  // disjoint variant bits: sums are ORs
+    if (a.n_outer > 24) {
+      uint32_t var = 0;
+      for (int b = 0; b < S.m_outer; ++b)
+        for (int jt = 24; jt < a.n_outer; ++jt)
+          if (a.oq[jt] == S.var_outer[b] && ((tile >> jt) & 1)) var |= 1u << (S.m_tile + b);
+      off += var * kDenseVar;
+    }
+    dense_load_u(gm2 + off + (uint32_t)S.warp_var[warp] * kDenseVar, lane, ue);
+  };
+  if ((int64_t)blockIdx.x < a.ntiles) load_a(0, blockIdx.x, tile_base(blockIdx.x));
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-    const int cur = it & 1;
     const uint64_t base = tile_base(tile);
     const int64_t next = tile + gridDim.x;
-    if (next < a.ntiles) {
-      issue_load(next, cur ^ 1);
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    }
+    // the buffer tile - gridDim.x used (its stores are this thread's own slots, issued above)
+    issue_load(tile + (int64_t)(SV_DENSE_NBUF - 1) * gridDim.x, cur == 0 ? SV_DENSE_NBUF - 1 : cur - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SV_DENSE_NBUF - 1) : "memory");
     __syncthreads();
     double2* tp = smem_tiles + (size_t)cur * N;
     for (int st = 0; st < a.nstages; ++st) {
-      dense_apply_a(tp, s_st[st], ue, warp, lane);
+      dense_apply(tp, s_st[st], ue, warp, lane);
       // the next A operand: this tile's next stage, or the next tile's first stage (its L2
       // latency then overlaps the barrier, the store and the next tile's wait)
+#if SV_DENSE_VT
+      if (st + 1 < a.nstages) load_a(st + 1, tile, base);
+      else if (next < a.ntiles) load_a(0, next, 0);
+#else
       if (st + 1 < a.nstages) dense_load_a(s_st[st + 1], gm2, base, warp, lane, ue);
       else if (next < a.ntiles) dense_load_a(s_st[0], gm2, tile_base(next), warp, lane, ue);
+#endif
       __syncthreads();
     }
     {
@@ -1280,7 +1430,9 @@ __global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_dense(double2* __rest
     }
     // no barrier: every thread reloads (cp.async) exactly the slots it just stored from, and the
     // last stage ended with one
+    cur = cur + 1 == SV_DENSE_NBUF ? 0 : cur + 1;
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------- complex64 forward passes (NEXT-3)
@@ -1325,7 +1477,7 @@ __device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S,
   const int g = lane >> 2, t = lane & 3;
   uint32_t var = S.warp_var[warp];
   for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
-  const double2* U = gm2 + S.dense_off + var * (16u * kDenseRow);
+  const double2* U = gm2 + S.dense_off + var * kDenseVar;
   // A entries U[o][i], o in {g, g+8} (a), i = 8 kh + t (+4) (c): complex -> split re / im
   uint32_t ur_h[2][2][2], ur_l[2][2][2], ui_h[2][2][2], ui_l[2][2][2];  // [kh][a][c]
 #pragma unroll
@@ -1405,14 +1557,14 @@ __device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S,
   }
 }
 
-__global__ void __launch_bounds__(256, SV_FWD_CTAS) k_pass_c64(float2* __restrict__ psi, RegArgs a) {
+__global__ void __launch_bounds__(256, SV_C64_CTAS) k_pass_c64(float2* __restrict__ psi, RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
   const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   float2* smem_tiles = reinterpret_cast<float2*>(smem_raw);  // two tiles
   RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + 2 * N);
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
-  double* s_mats = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_st + a.nstages) + 15) & ~uintptr_t(15));
+  double* s_mats = smem_align16<double>(smem_raw, s_st + a.nstages);
   uint64_t* s_ob = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.ops);
@@ -1531,7 +1683,8 @@ __global__ void k_narrow(const double2* __restrict__ a, float2* __restrict__ b, 
 }
 
 size_t dense_pass_smem_bytes(int k, int nstages) {
-  return (size_t(16) << k) * 2 + (size_t)nstages * sizeof(StageDesc) + 16 + 4 * 64 * 8;
+  return (size_t(16) << k) * SV_DENSE_NBUF + (size_t)nstages * sizeof(StageDesc) + 16 + 4 * 64 * 8 +
+         (size_t)nstages * 256 * 4;
 }
 
 

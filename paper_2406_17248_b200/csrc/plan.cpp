@@ -1294,13 +1294,28 @@ void emit_rops(Plan* plan) {
   }
 }
 
+// FP64 additions per amplitude outside the FMAs: the Gauss form's sums (one per input element and
+// two per A entry amortised over the warp's 16 vectors: 24 DADDs per 256 amplitudes = 3 per amp)
+int pass_add_per_amp(const Plan& plan, size_t i) {
+  const PassDesc& pd = plan.passes[i];
+  int f = 0;
+  if (pd.R > 0)
+    for (int si = pd.stage_begin; si < pd.stage_end; ++si) {
+      const StageDesc& S = plan.stages[si];
+      if (S.dense) f += S.dense == 2 ? 3 * 3 : 3;
+    }
+  return f;
+}
+
 int pass_fma_per_amp(const Plan& plan, size_t i) {
   const PassDesc& pd = plan.passes[i];
   int f = 0;
   if (pd.R > 0) {
     for (int si = pd.stage_begin; si < pd.stage_end; ++si) {
       const StageDesc& S = plan.stages[si];
-      if (S.dense) { f += 64; continue; }
+      // Gauss form (kernels_reg.cu dense_apply): 48 DMMA FMAs per amplitude; adjoint dense
+      // stages apply it to psi and lambda and accumulate R (48 more)
+      if (S.dense) { f += S.dense == 2 ? 3 * 48 : 48; continue; }
       for (int j = pd.op_begin + S.op_begin; j < pd.op_begin + S.op_end; ++j)
         f += seq_cost(plan.ops[j], plan.mats.data() + pd.mat_begin + plan.ops[j].mat_off);
     }

@@ -254,6 +254,7 @@ void build_plan(const std::vector<BoundGate>& gates, int n_local, const PlanOpti
 void refresh_plan(const std::vector<BoundGate>& gates, Plan* plan);
 // FP64 FMAs per amplitude of pass i of a plan (dense stages 64, sequential ops by class).
 int pass_fma_per_amp(const Plan& plan, size_t i);
+int pass_add_per_amp(const Plan& plan, size_t i);  // FP64 additions per amplitude (Gauss sums)
 
 // ---------------------------------------------------------------------------------------------
 // Kernel launchers (kernels.cu).
