@@ -42,6 +42,12 @@
 #ifndef SV_DA_R_3M
 #define SV_DA_R_3M 1  // adjoint dense stages: R = sum psi lambda^H with three real products
 #endif
+#ifndef SV_DA_SHARED_A
+#define SV_DA_SHARED_A 1  // adjoint dense stages: one A load and coefficient set for psi and lambda
+#endif
+#ifndef SV_DMMA_VOLATILE
+#define SV_DMMA_VOLATILE 1
+#endif
 #ifndef SV_FWD_CTAS
 #define SV_FWD_CTAS 2   // forward register passes: CTAs per SM (register budget 65536 / (256 * CTAs));
                         // 2 (128 registers) fits the dense stages' Gauss live set (3: 80, spills)
@@ -123,7 +129,8 @@ struct Op {
   __device__ __forceinline__ int32_t grad_local() const { return (int32_t)(int16_t)(w2 >> 16); }
   __device__ __forceinline__ uint32_t qa() const { return w3 & 0xffu; }
   __device__ __forceinline__ uint32_t qb() const { return (w3 >> 8) & 0xffu; }
-  __device__ __forceinline__ uint32_t run_len() const { return w3 >> 16; }
+  __device__ __forceinline__ uint32_t run_len() const { return (w3 >> 16) & kRopRunMask; }
+  __device__ __forceinline__ bool has_ctrl() const { return (w3 >> 31) != 0u; }  // kRopHasCtrl
 };
 
 __device__ __forceinline__ Op load_op(const RegOp* p) {
@@ -800,7 +807,7 @@ __device__ __forceinline__ void dual_diag_run(double2 (&v)[8], double2 (&w)[8], 
     for (int q = 0; q < 4; ++q) tab_one(T.B[p][q]);
   for (int k = 0; k < len; ++k) {
     const Op o = load_op(ops + k);
-    const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
+    const bool ok = !o.has_ctrl() || (((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr()));
     const bool gen = o.gen() != 0u;
     double part = 0.0;
     if (ok) {
@@ -879,15 +886,20 @@ __device__ __forceinline__ void dual_diag_run(double2 (&v)[8], double2 (&w)[8], 
 constexpr uint32_t kDenseRow = 16;  // double2 per stored variant-matrix row (plan.cpp kDenseStride)
 constexpr uint32_t kDenseVar = 16u * kDenseRow;  // double2 per variant matrix
 
+#if SV_DMMA_VOLATILE
+#define SV_ASM_MMA asm volatile
+#else
+#define SV_ASM_MMA asm
+#endif
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  SV_ASM_MMA("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
 
 // D = A B + C with C and D distinct registers (T seeds the Re and Im chains)
 __device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double b, double c0, double c1) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+  SV_ASM_MMA("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
                : "=d"(d0), "=d"(d1)
                : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
@@ -926,7 +938,26 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double x) {
   asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(x) : "memory");
 }
 
-__device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, const DenseA& A, int warp, int lane) {
+// Gauss coefficients of the A entries (two DADDs each)
+struct DenseC {
+  double cb[2][4], cc[2][4];
+};
+__device__ __forceinline__ void dense_coef(const DenseA& A, DenseC& C) {
+#pragma unroll
+  for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+    for (int kh = 0; kh < 4; ++kh) {
+      C.cb[mh][kh] = -(A.u[mh][kh].x + A.u[mh][kh].y);
+      C.cc[mh][kh] = A.u[mh][kh].y - A.u[mh][kh].x;
+    }
+}
+
+// PRE: the coefficients come precomputed in *Cp (one set for the psi and lambda tiles of an adjoint
+// dense stage); otherwise they are computed after the T chains are issued (measured faster than
+// before them in the forward kernel)
+template <bool PRE = false>
+__device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, const DenseA& A, int warp, int lane,
+                                            const DenseC* Cp = nullptr) {
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(tp);
   const uint32_t wsw = S.warp_swz[warp];
   const uint32_t bB = wsw ^ (uint32_t)S.lane_b[lane], bD = wsw ^ (uint32_t)S.lane_d[lane];
@@ -958,14 +989,9 @@ __device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, con
         dmma(t[nt][mh][0], t[nt][mh][1], A.u[mh][kh].x, sx);
       }
     }
-  double cb[2][4], cc[2][4];
-#pragma unroll
-  for (int mh = 0; mh < 2; ++mh)
-#pragma unroll
-    for (int kh = 0; kh < 4; ++kh) {
-      cb[mh][kh] = -(A.u[mh][kh].x + A.u[mh][kh].y);
-      cc[mh][kh] = A.u[mh][kh].y - A.u[mh][kh].x;
-    }
+  DenseC Cl;
+  if (!PRE) dense_coef(A, Cl);
+  const DenseC& C = PRE ? *Cp : Cl;
   double re[2][2][2], im[2][2][2];
 #pragma unroll
   for (int kh = 0; kh < 4; ++kh)
@@ -974,11 +1000,11 @@ __device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, con
 #pragma unroll
       for (int mh = 0; mh < 2; ++mh) {
         if (kh == 0) {
-          dmma_c(re[nt][mh][0], re[nt][mh][1], cb[mh][0], xi[nt][0], t[nt][mh][0], t[nt][mh][1]);
-          dmma_c(im[nt][mh][0], im[nt][mh][1], cc[mh][0], xr[nt][0], t[nt][mh][0], t[nt][mh][1]);
+          dmma_c(re[nt][mh][0], re[nt][mh][1], C.cb[mh][0], xi[nt][0], t[nt][mh][0], t[nt][mh][1]);
+          dmma_c(im[nt][mh][0], im[nt][mh][1], C.cc[mh][0], xr[nt][0], t[nt][mh][0], t[nt][mh][1]);
         } else {
-          dmma(re[nt][mh][0], re[nt][mh][1], cb[mh][kh], xi[nt][kh]);
-          dmma(im[nt][mh][0], im[nt][mh][1], cc[mh][kh], xr[nt][kh]);
+          dmma(re[nt][mh][0], re[nt][mh][1], C.cb[mh][kh], xi[nt][kh]);
+          dmma(im[nt][mh][0], im[nt][mh][1], C.cc[mh][kh], xr[nt][kh]);
         }
       }
   // stores: amps 8 mh + lane/4 of columns 2 (lane%4) + v, as two 8-byte halves (ptxas fuses them)
@@ -1015,6 +1041,10 @@ __device__ __forceinline__ void tile_st(float2& d, double2 v) { d = make_float2(
 // ops follow on the host as tr(B_j R).
 __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDesc& S, const double2* __restrict__ gmats2,
                                          uint64_t base, int warp, int lane, double* racc) {
+#if SV_DA_SHARED_A
+  DenseA A;  // one A operand for the psi and lambda applications, loaded before R (L2 latency hidden)
+  dense_load_a(S, gmats2, base, warp, lane, A);
+#endif
   const uint32_t wsw = S.warp_swz[warp];
   const uint32_t br = wsw ^ S.lane_r[lane];
   // fragments: A = Psi[a = 8 mt + lane/4][v = 4 kt + lane%4], B = Lambda[b = 8 nt + lane/4][v]
@@ -1088,8 +1118,15 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
         racc[((((mt * 2 + nt) * 2 + 1) * 2 + v) << 5) + lane] += rim[mt][nt][v];
       }
   __syncwarp();
+#if SV_DA_SHARED_A
+  DenseC C;
+  dense_coef(A, C);
+  dense_apply<true>(tp, S, A, warp, lane, &C);
+  dense_apply<true>(tl, S, A, warp, lane, &C);
+#else
   dense_stage(tp, S, gmats2, base, warp, lane);
   dense_stage(tl, S, gmats2, base, warp, lane);
+#endif
 }
 
 // ---------------------------------------------------------------- the pass kernel
@@ -1238,7 +1275,8 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
         v[j] = tp[ad];
         if constexpr (DUAL) w[j] = tl[ad];
       }
-      for (int i = S.op_begin; i < S.op_end; ++i) {
+      const int op_end = S.op_end;
+      for (int i = S.op_begin; i < op_end; ++i) {
         const Op o = load_op(s_ops + i);
         if constexpr (DUAL) {
           const uint32_t rl = o.run_len();
@@ -1249,7 +1287,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
             continue;
           }
         }
-        const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
+        const bool ok = !o.has_ctrl() || (((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr()));
         const double2* m = mats2 + o.mat_off();
         if constexpr (DUAL) {
           const double2* g = mats2 + o.gen_off();
@@ -1642,7 +1680,8 @@ __global__ void __launch_bounds__(256, SV_C64_CTAS) k_pass_c64(float2* __restric
           if ((j >> r) & 1) ad ^= SR[r];
         v[j] = tile_ld(tp[ad]);
       }
-      for (int i = S.op_begin; i < S.op_end; ++i) {
+      const int op_end = S.op_end;
+      for (int i = S.op_begin; i < op_end; ++i) {
         const Op o = load_op(s_ops + i);
         const bool ok = ((base & o.couter) == o.couter) && ((tthr & o.cthr()) == o.cthr());
         if (!ok) continue;

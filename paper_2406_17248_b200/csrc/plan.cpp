@@ -1265,6 +1265,7 @@ void emit_rops(Plan* plan) {
       r.qb = (uint8_t)(o.qb >= 0 ? o.qb : 0);
       r.couter = o.couter;
       r.grad_slot = o.grad_slot;
+      r.pad = (o.couter != 0 || o.cthr != 0) ? kRopHasCtrl : 0;  // kernels skip the control test otherwise
       plan->rops[i] = r;
     }
     // adjoint passes: runs of >= 2 consecutive diagonal ops of a sequential stage without register
@@ -1282,10 +1283,10 @@ void emit_rops(Plan* plan) {
         int j = i;
         while (j < e && eligible(j)) ++j;
         if (j - i >= g_diag_run_min) {
-          plan->rops[i].pad = (uint16_t)std::min(j - i, 65535);
+          plan->rops[i].pad = (uint16_t)((plan->rops[i].pad & kRopHasCtrl) | std::min(j - i, (int)kRopRunMask));
           static const bool dbg = std::getenv("SV_PLAN_DEBUG") != nullptr;
           if (dbg) std::fprintf(stderr, "diag run: pass %d stage %d ops %d\n", (int)(&pd - plan->passes.data()), si, j - i);
-          i = std::min(j, i + 65535);
+          i = std::min(j, i + (int)kRopRunMask);
         } else {
           i = j + 1;
         }

@@ -139,12 +139,15 @@ struct RegOp {
   uint16_t cthr;       // control bits on thread positions (tile-position space)
   int16_t grad_local;  // index among the pass' grad ops, -1 none
   uint8_t qa, qb;      // physical qubits (outer target bits of diagonal ops)
-  uint16_t pad;        // adjoint passes: length of the diagonal run this op starts (0: none)
+  uint16_t pad;        // bits 0-11: adjoint passes, length of the diagonal run this op starts (0:
+                       // none); bit 15 (kRopHasCtrl): the op has outer or thread-position controls
   uint64_t couter;     // control bits outside the tile (local physical index space)
   int32_t grad_slot;   // global adjoint slot (-1 none)
   uint32_t pad2;
 };
 static_assert(sizeof(RegOp) == 32, "RegOp layout");
+constexpr uint16_t kRopRunMask = 0x0fff;
+constexpr uint16_t kRopHasCtrl = 0x8000;
 
 constexpr int kMaxTileQubits = 13;
 constexpr int kMaxOpsPerPass = 256;

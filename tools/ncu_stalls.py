@@ -1,13 +1,14 @@
 """Summarise an ncu report: key raw metrics, top stall reasons, per-opcode stall/exec shares.
 
-usage: python tools/ncu_stalls.py REPORT.ncu-rep [N_TOP]"""
+usage: python tools/ncu_stalls.py REPORT.ncu-rep [N_TOP] [LAUNCH_INDEX]"""
 import csv
 import subprocess
 import sys
 from collections import Counter
 
 rep = sys.argv[1]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+sel = ["--launch-skip", sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", rep, *sel, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 h, v = rows[0], rows[2]
 d = dict(zip(h, v))
@@ -24,9 +25,13 @@ st = [(float(d[k]), k) for k in h if k.startswith("smsp__average_warps_issue_sta
 print("# top stall reasons (warps per issue)")
 for x in sorted(st, reverse=True)[:8]:
     print(f"{x[1]:85s} {x[0]:.3f}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+src = subprocess.run(["ncu", "-i", rep, *sel, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(src.splitlines()))
+# one block per kernel ("Kernel Name" row, header row, instructions): the selected launch's block
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+blk = 0 if len(starts) <= 2 or not sel else min(int(sys.argv[3]), len(starts) - 2)
+rows = rows[starts[blk]:starts[blk + 1]]
 h = rows[1]
 data = rows[2:]
 iS, iE = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
