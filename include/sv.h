@@ -139,9 +139,11 @@ enum {
                                    0: every eligible stage (incl. one outer variant bit at any
                                    size); 1 << 20: none */
   SV_OPT_C64_SPLIT = 7           /* complex64 dense stages: 3 (default) TF32 products of the hi/lo
-                                   split (~2^-21 relative per product); 1: the single hi x hi TF32
-                                   product (~2^-11) — kept only to show the tests' tolerance
-                                   detects a precision loss */
+                                   split (~2^-21 relative per product); 0: passes of dense stages
+                                   only widen the tile to FP64 and run the Gauss DMMA stages of the
+                                   complex128 kernel (FP32 rounding once per stage; slower than 3
+                                   on B200); 1: the single hi x hi TF32 product (~2^-11) — kept
+                                   only to show the tests' tolerance detects a precision loss */
 };
 
 /* a1: |0...0> on n_qubits (1 <= n <= 40 subject to memory), current CUDA device, new stream. */

@@ -382,6 +382,7 @@ static int run_plan_c64(sv_state_s* h, const CachedPlan& cp) {
     L.n_local = h->n_local;
     L.rank_bits = 0;
     L.c64_terms = h->c64_split;
+    L.all_dense = pass_all_dense(plan, pd);
     cudaError_t e = launch_pass_c64(h->psi32, L, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "complex64 pass launch");
     h->stats.kernel_launches += 1;
@@ -909,7 +910,7 @@ sv_status sv_set_option(sv_handle h, int32_t key, int64_t value) {
       h->opts.da_cost = (int)value;
       return SV_OK;
     case SV_OPT_C64_SPLIT:
-      if (value != 1 && value != 3) return fail(SV_E_ARG, "complex64 split must be 1 or 3");
+      if (value != 0 && value != 1 && value != 3) return fail(SV_E_ARG, "complex64 split must be 0, 1 or 3");
       h->c64_split = (int)value;
       return SV_OK;
     default: return fail(SV_E_ARG, "unknown option");

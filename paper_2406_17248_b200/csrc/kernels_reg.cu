@@ -33,9 +33,6 @@
 #ifndef SV_DENSE_NBUF
 #define SV_DENSE_NBUF 2  // k_pass_dense tile ring depth (3: no gain measured)
 #endif
-#ifndef SV_DENSE_XOR_ADDR
-#define SV_DENSE_XOR_ADDR 1
-#endif
 #ifndef SV_DENSE_VT
 #define SV_DENSE_VT 1
 #endif
@@ -75,6 +72,10 @@ __host__ __device__ __forceinline__ uint32_t swz(uint32_t t) { return t ^ ((t >>
 // complex64 tiles: 8-byte slots, 16 per 128-byte bank row -> 4-bit XOR fold
 __host__ __device__ __forceinline__ uint32_t swz8(uint32_t t) { return t ^ ((t >> 4 ^ t >> 8 ^ t >> 12) & 15u); }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -955,25 +956,51 @@ __device__ __forceinline__ void dense_coef(const DenseA& A, DenseC& C) {
 // PRE: the coefficients come precomputed in *Cp (one set for the psi and lambda tiles of an adjoint
 // dense stage); otherwise they are computed after the T chains are issued (measured faster than
 // before them in the forward kernel)
-template <bool PRE = false>
-__device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, const DenseA& A, int warp, int lane,
-                                            const DenseC* Cp = nullptr) {
-  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(tp);
+// A dense stage's shared-memory offsets for this lane (swizzled slot indices, XOR-linear): B-load
+// base and basis (kq bit 0, kq bit 1, nt), D-store base and basis (v, mh, nt)
+struct DenseOff {
+  uint32_t bB, Lk0, Lk1, Ln, bD, Sv, Sm, Sn;
+};
+__device__ __forceinline__ DenseOff dense_off(const StageDesc& S, int warp, int lane) {
+  DenseOff o;
   const uint32_t wsw = S.warp_swz[warp];
-  const uint32_t bB = wsw ^ (uint32_t)S.lane_b[lane], bD = wsw ^ (uint32_t)S.lane_d[lane];
-  const uint32_t Lk0 = S.swz_reg[1], Lk1 = S.swz_reg[2], Ln = S.swz_reg[4];
-  const uint32_t Sv = S.swz_reg[8 + 1], Sm = S.swz_reg[8 + 2], Sn = S.swz_reg[8 + 4];
+  o.bB = wsw ^ (uint32_t)S.lane_b[lane];
+  o.bD = wsw ^ (uint32_t)S.lane_d[lane];
+  o.Lk0 = S.swz_reg[1];
+  o.Lk1 = S.swz_reg[2];
+  o.Ln = S.swz_reg[4];
+  o.Sv = S.swz_reg[8 + 1];
+  o.Sm = S.swz_reg[8 + 2];
+  o.Sn = S.swz_reg[8 + 4];
+  return o;
+}
+
+// tile element access on a 32-bit shared address: complex128 slots (16 bytes) or complex64 slots
+// (8 bytes, widened to FP64 for the MMAs and rounded back on the store)
+__device__ __forceinline__ double2 tile_lds(const double2*, uint32_t sb, uint32_t o) { return lds_v2(sb + (o << 4)); }
+__device__ __forceinline__ double2 tile_lds(const float2*, uint32_t sb, uint32_t o) {
+  float x, y;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];\n" : "=f"(x), "=f"(y) : "r"(sb + (o << 3)) : "memory");
+  return make_double2((double)x, (double)y);
+}
+__device__ __forceinline__ void tile_sts(double2*, uint32_t sb, uint32_t o, double re, double im) {
+  const uint32_t a = sb + (o << 4);
+  sts_f64(a, re);
+  sts_f64(a + 8, im);  // (ptxas fuses the halves into one 16-byte store)
+}
+__device__ __forceinline__ void tile_sts(float2*, uint32_t sb, uint32_t o, double re, double im) {
+  asm volatile("st.shared.v2.f32 [%0], {%1,%2};\n" ::"r"(sb + (o << 3)), "f"((float)re), "f"((float)im) : "memory");
+}
+
+template <bool PRE = false, typename T>
+__device__ __forceinline__ void dense_apply_o(T* tp, const DenseOff& O, const DenseA& A, const DenseC* Cp = nullptr) {
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(tp);
   double xr[2][4], xi[2][4];
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int kq = 0; kq < 4; ++kq) {
-#if SV_DENSE_XOR_ADDR
-      const uint32_t o = bB ^ (nt ? Ln : 0u) ^ ((kq & 1) ? Lk0 : 0u) ^ ((kq & 2) ? Lk1 : 0u);
-      const double2 x = lds_v2(sb + (o << 4));
-#else
-      const double2 x = tp[bB ^ S.swz_reg[nt * 4 + kq]];
-#endif
+      const double2 x = tile_lds(tp, sb, O.bB ^ (nt ? O.Ln : 0u) ^ ((kq & 1) ? O.Lk0 : 0u) ^ ((kq & 2) ? O.Lk1 : 0u));
       xr[nt][kq] = x.x;
       xi[nt][kq] = x.y;
     }
@@ -1007,21 +1034,20 @@ __device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, con
           dmma(im[nt][mh][0], im[nt][mh][1], C.cc[mh][kh], xr[nt][kh]);
         }
       }
-  // stores: amps 8 mh + lane/4 of columns 2 (lane%4) + v, as two 8-byte halves (ptxas fuses them)
+  // stores: amps 8 mh + lane/4 of columns 2 (lane%4) + v
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
     for (int mh = 0; mh < 2; ++mh)
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-#if SV_DENSE_XOR_ADDR
-        const uint32_t a = sb + ((bD ^ (nt ? Sn : 0u) ^ (mh ? Sm : 0u) ^ (v ? Sv : 0u)) << 4);
-        sts_f64(a, re[nt][mh][v]);
-        sts_f64(a + 8, im[nt][mh][v]);
-#else
-        tp[bD ^ S.swz_reg[8 + nt * 4 + mh * 2 + v]] = make_double2(re[nt][mh][v], im[nt][mh][v]);
-#endif
-      }
+      for (int v = 0; v < 2; ++v)
+        tile_sts(tp, sb, O.bD ^ (nt ? O.Sn : 0u) ^ (mh ? O.Sm : 0u) ^ (v ? O.Sv : 0u), re[nt][mh][v], im[nt][mh][v]);
+}
+
+template <bool PRE = false>
+__device__ __forceinline__ void dense_apply(double2* tp, const StageDesc& S, const DenseA& A, int warp, int lane,
+                                            const DenseC* Cp = nullptr) {
+  dense_apply_o<PRE>(tp, dense_off(S, warp, lane), A, Cp);
 }
 
 __device__ __forceinline__ void dense_stage(double2* tp, const StageDesc& S, const double2* __restrict__ gmats2,
@@ -1358,17 +1384,29 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
 // leaves room to load the next stage's A operand (its variant matrix, from L2) into registers
 // before the barrier that ends the current stage, and the first stage's before the tile wait:
 // the L2 latency overlaps barrier / load waits instead of stalling the first MMA of every stage.
-__global__ void __launch_bounds__(256, SV_DENSE_CTAS) k_pass_dense(double2* __restrict__ psi, RegArgs a) {
+// T = double2: complex128 state; T = float2: complex64 state (NEXT-3), 8-byte slots with the swz8
+// fold, widened to FP64 for the Gauss DMMA stages and rounded back to FP32 once per stage.
+template <typename T>
+__device__ __forceinline__ uint32_t tile_swz(uint32_t t) { return sizeof(T) == 16 ? swz(t) : swz8(t); }
+
+template <typename T>
+__global__ void __launch_bounds__(256, SV_DENSE_CTAS) k_pass_dense(T* __restrict__ psi, RegArgs a) {
+  constexpr bool C64 = sizeof(T) == 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
   const int nthr = blockDim.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double2* smem_tiles = reinterpret_cast<double2*>(smem_raw);
-  StageDesc* s_st = reinterpret_cast<StageDesc*>(smem_tiles + SV_DENSE_NBUF * N);
+  T* smem_tiles = reinterpret_cast<T*>(smem_raw);
+  StageDesc* s_st = smem_align16<StageDesc>(smem_raw, smem_tiles + SV_DENSE_NBUF * N);
   uint64_t* s_ob = smem_align16<uint64_t>(smem_raw, s_st + a.nstages);
   // per stage, the variant-matrix offset contributed by the tile index: four 64-entry deposit
   // tables (tile bits 6c .. 6c+5 -> their outer qubits -> variant bits), so a stage's A operand
   // address costs four shared loads instead of a loop over its outer variant qubits
   uint32_t* s_vt = reinterpret_cast<uint32_t*>(s_ob + 4 * 64);
+  // complex64: the stages' swz8 slot offsets (the StageDesc ones are for 16-byte slots), from the
+  // stage's positions (XOR-linear, as plan.cpp make_dense builds them): per stage 8 warp bases,
+  // 32 B-load and 32 D-store lane parts, 6 basis values
+  uint16_t* s_o8 = reinterpret_cast<uint16_t*>(s_vt + a.nstages * 256);
+  constexpr int kO8 = 8 + 32 + 32 + 8;
   {
     const uint64_t* ss = reinterpret_cast<const uint64_t*>(a.stages);
     uint64_t* sd = reinterpret_cast<uint64_t*>(s_st);
@@ -1394,13 +1432,39 @@ __global__ void __launch_bounds__(256, SV_DENSE_CTAS) k_pass_dense(double2* __re
       }
       s_vt[e] = ((h >> 6) == 0 ? S.dense_off : 0u) + var * kDenseVar;  // summed over the 4 tables
     }
+    if (C64)
+      for (int e = tid; e < a.nstages * kO8; e += nthr) {
+        const StageDesc& S = *reinterpret_cast<const StageDesc*>(reinterpret_cast<const uint64_t*>(a.stages) +
+                                                                 (e / kO8) * (int)(sizeof(StageDesc) / 8));
+        const int q = e % kO8;
+        auto b8 = [&](int pos) { return pos >= 0 ? swz8(1u << pos) : 0u; };
+        const uint32_t p0 = b8(S.regpos[0]), p1 = b8(S.regpos[1]), p2 = b8(S.regpos[2]), p3 = b8(S.regpos[3]);
+        const uint32_t c0 = b8(S.thrpos[0]), c1 = b8(S.thrpos[1]), c2 = b8(S.thrpos[2]), n0 = b8(S.thrpos[3]);
+        uint32_t v = 0;
+        if (q < 8) {
+          for (int bb = 0; bb < 3; ++bb)
+            if ((q >> bb) & 1) v ^= b8(S.thrpos[4 + bb]);
+        } else if (q < 40) {
+          const int l = q - 8;
+          v = (((l >> 2) & 1) ? c0 : 0u) ^ (((l >> 3) & 1) ? c1 : 0u) ^ (((l >> 4) & 1) ? c2 : 0u) ^ ((l & 1) ? p0 : 0u) ^
+              ((l & 2) ? p1 : 0u);
+        } else if (q < 72) {
+          const int l = q - 40;
+          v = (((l >> 2) & 1) ? p0 : 0u) ^ (((l >> 3) & 1) ? p1 : 0u) ^ (((l >> 4) & 1) ? p2 : 0u) ^ ((l & 1) ? c1 : 0u) ^
+              ((l & 2) ? c2 : 0u);
+        } else {
+          const uint32_t basis[8] = {p2, p3, n0, c0, p3, n0, 0u, 0u};  // Lk0 Lk1 Ln | Sv Sm Sn
+          v = basis[q - 72];
+        }
+        s_o8[e] = (uint16_t)v;
+      }
   }
   __syncthreads();
   const int nthr_bits = a.k - 3;
   uint64_t dep_t = 0;
   for (int b = 0; b < nthr_bits; ++b)
     if ((tid >> b) & 1) dep_t |= 1ull << a.tq[b];
-  const uint32_t swz_t = swz((uint32_t)tid);
+  const uint32_t swz_t = tile_swz<T>((uint32_t)tid);
   const double2* gm2 = reinterpret_cast<const double2*>(a.mats);
   auto tile_base = [&](int64_t tile) {
     uint64_t base = s_ob[tile & 63] | s_ob[64 + ((tile >> 6) & 63)] | s_ob[128 + ((tile >> 12) & 63)] |
@@ -1414,9 +1478,12 @@ __global__ void __launch_bounds__(256, SV_DENSE_CTAS) k_pass_dense(double2* __re
   auto issue_load = [&](int64_t tile, int buf) {
     if (tile < a.ntiles) {
       const uint64_t bt = tile_base(tile) | dep_t;
-      double2* dp = smem_tiles + (size_t)buf * N;
+      T* dp = smem_tiles + (size_t)buf * N;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) cp_async16(dp + (swz_t ^ a.zsub[i]), psi + (bt | a.hsub[i]));
+      for (int i = 0; i < 8; ++i) {
+        if (C64) cp_async8(dp + (swz_t ^ a.zsub[i]), psi + (bt | a.hsub[i]));
+        else cp_async16(dp + (swz_t ^ a.zsub[i]), psi + (bt | a.hsub[i]));
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -1447,9 +1514,23 @@ __global__ void __launch_bounds__(256, SV_DENSE_CTAS) k_pass_dense(double2* __re
     issue_load(tile + (int64_t)(SV_DENSE_NBUF - 1) * gridDim.x, cur == 0 ? SV_DENSE_NBUF - 1 : cur - 1);
     asm volatile("cp.async.wait_group %0;\n" ::"n"(SV_DENSE_NBUF - 1) : "memory");
     __syncthreads();
-    double2* tp = smem_tiles + (size_t)cur * N;
+    T* tp = smem_tiles + (size_t)cur * N;
     for (int st = 0; st < a.nstages; ++st) {
-      dense_apply(tp, s_st[st], ue, warp, lane);
+      if (C64) {
+        const uint16_t* o8 = s_o8 + st * kO8;
+        DenseOff O;
+        O.bB = (uint32_t)o8[warp] ^ o8[8 + lane];
+        O.bD = (uint32_t)o8[warp] ^ o8[40 + lane];
+        O.Lk0 = o8[72];
+        O.Lk1 = o8[73];
+        O.Ln = o8[74];
+        O.Sv = o8[75];
+        O.Sm = o8[76];
+        O.Sn = o8[77];
+        dense_apply_o(tp, O, ue);
+      } else {
+        dense_apply_o(tp, dense_off(s_st[st], warp, lane), ue);
+      }
       // the next A operand: this tile's next stage, or the next tile's first stage (its L2
       // latency then overlaps the barrier, the store and the next tile's wait)
 #if SV_DENSE_VT
@@ -1482,10 +1563,6 @@ __global__ void __launch_bounds__(256, SV_DENSE_CTAS) k_pass_dense(double2* __re
 // same op code as the complex128 kernel (one rounding per stage); dense stages run on the TF32
 // tensor cores with a 3-term split (dense_stage_tf32). Measured alternatives: FP32 FFMA on the CUDA
 // cores and widening to the FP64 MMAs were both slower.
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
 
 __constant__ uint32_t kPerm24[24] = {228, 180, 216, 120, 156, 108, 225, 177, 201, 57, 141, 45, 210, 114, 198, 54, 78, 30, 147, 99, 135, 39, 75, 27};  // plan.cpp make_dense order
 
@@ -1510,8 +1587,36 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// The TF32 dense stage's swz8 slot offsets (XOR-linear in the positions): vector n = 8 nt + col (col
+// bits -> the warp's first three vector positions in the host-chosen order StageDesc::c64_perm, nt ->
+// the fourth), register index r (bit i -> regpos[i]). Entry q of the stage's 80: q < 8 warp part,
+// 8 + lane B-load lane part (n col = g, in amp r = t), 40 + lane D-store lane part (out amp o = g,
+// n col = 2 t), 72.. the bases of nt, r bit 2, r bit 3 and n col bit 0.
+constexpr int kC64Off = 80;
+__device__ __forceinline__ uint16_t c64_stage_offset(const StageDesc& S, int q) {
+  auto sp = [&](int pos) { return pos >= 0 ? swz8(1u << pos) : 0u; };
+  const uint32_t pc = kPerm24[S.c64_perm];
+  const int X[4] = {S.thrpos[pc & 3], S.thrpos[(pc >> 2) & 3], S.thrpos[(pc >> 4) & 3], S.thrpos[(pc >> 6) & 3]};
+  uint32_t v = 0;
+  if (q < 8) {
+    for (int b = 0; b < 3; ++b)
+      if ((q >> b) & 1) v ^= sp(S.thrpos[4 + b]);
+  } else if (q < 72) {
+    const int l = (q - 8) & 31, g = l >> 2, t = l & 3;
+    const bool load = q < 40;
+    for (int b = 0; b < 3; ++b)
+      if ((g >> b) & 1) v ^= load ? sp(X[b]) : sp(S.regpos[b]);
+    for (int b = 0; b < 2; ++b)
+      if ((t >> b) & 1) v ^= load ? sp(S.regpos[b]) : sp(X[b + 1]);
+  } else if (q < 76) {
+    const int which = q - 72;
+    v = which == 0 ? sp(X[3]) : which == 1 ? sp(S.regpos[2]) : which == 2 ? sp(S.regpos[3]) : sp(X[0]);
+  }
+  return (uint16_t)v;
+}
+
 __device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S, const double2* __restrict__ gm2,
-                                                 uint64_t base, int warp, int lane, bool split) {
+                                                 uint64_t base, int warp, int lane, bool split, const uint16_t* o8) {
   const int g = lane >> 2, t = lane & 3;
   uint32_t var = S.warp_var[warp];
   for (int b = 0; b < S.m_outer; ++b) var |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << (S.m_tile + b);
@@ -1528,27 +1633,9 @@ __device__ __forceinline__ void dense_stage_tf32(float2* tp, const StageDesc& S,
         split_tf32((float)u.x, ur_h[kh][a][c], ur_l[kh][a][c]);
         split_tf32((float)u.y, ui_h[kh][a][c], ui_l[kh][a][c]);
       }
-  // slot parts (swz is XOR-linear): vector n = 8 nt + col (col bits -> thrpos[0..2], nt -> thrpos[3]),
-  // register index r (bit i -> regpos[i])
-  auto sp = [&](int pos) { return swz8(1u << pos); };
-  // the warp's four vector positions in the host-chosen order (StageDesc::c64_perm)
-  const uint32_t pc = kPerm24[S.c64_perm];
-  const int X[4] = {S.thrpos[pc & 3], S.thrpos[(pc >> 2) & 3], S.thrpos[(pc >> 4) & 3], S.thrpos[(pc >> 6) & 3]};
-  uint32_t wsw = 0;
-  for (int b = 0; b < 3; ++b)
-    if (((warp >> b) & 1) && S.thrpos[4 + b] >= 0) wsw ^= sp(S.thrpos[4 + b]);
-  uint32_t bB = wsw, bD = wsw;
-#pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    if ((g >> b) & 1) bB ^= sp(X[b]);   // B: n col = g
-    if ((g >> b) & 1) bD ^= sp(S.regpos[b]);   // D: out amp o = g (+8)
-  }
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
-    if ((t >> b) & 1) bB ^= sp(S.regpos[b]);      // B: in amp r = t (+4, +8)
-    if ((t >> b) & 1) bD ^= sp(X[b + 1]);  // D: n col = 2 t (+1)
-  }
-  const uint32_t sN = sp(X[3]), sR2 = sp(S.regpos[2]), sR3 = sp(S.regpos[3]), sC0 = sp(X[0]);
+  // slot parts: the stage's table (k_pass_c64 setup, c64_stage_offsets)
+  const uint32_t bB = (uint32_t)o8[warp] ^ o8[8 + lane], bD = (uint32_t)o8[warp] ^ o8[40 + lane];
+  const uint32_t sN = o8[72], sR2 = o8[73], sR3 = o8[74], sC0 = o8[75];
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     // B fragments: in amps r = t + 4 c + 8 kh of vector (8 nt + g): Re for K-steps 0-1, Im for 2-3
@@ -1604,6 +1691,7 @@ __global__ void __launch_bounds__(256, SV_C64_CTAS) k_pass_c64(float2* __restric
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
   double* s_mats = smem_align16<double>(smem_raw, s_st + a.nstages);
   uint64_t* s_ob = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
+  uint16_t* s_o8 = reinterpret_cast<uint16_t*>(s_ob + 4 * 64);  // [nstages][kC64Off] TF32 stage offsets
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.ops);
     uint4* dst = reinterpret_cast<uint4*>(s_ops);
@@ -1619,6 +1707,11 @@ __global__ void __launch_bounds__(256, SV_C64_CTAS) k_pass_c64(float2* __restric
         if (((h >> b) & 1) && j < a.n_outer) off |= 1ull << a.oq[j];
       }
       s_ob[h] = off;
+    }
+    for (int e = tid; e < a.nstages * kC64Off; e += nthr) {
+      const StageDesc& S = *reinterpret_cast<const StageDesc*>(reinterpret_cast<const uint64_t*>(a.stages) +
+                                                               (e / kC64Off) * (int)(sizeof(StageDesc) / 8));
+      s_o8[e] = S.dense ? c64_stage_offset(S, e % kC64Off) : (uint16_t)0;
     }
   }
   __syncthreads();
@@ -1660,7 +1753,7 @@ __global__ void __launch_bounds__(256, SV_C64_CTAS) k_pass_c64(float2* __restric
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
       if (S.dense) {
-        dense_stage_tf32(tp, S, gm2, base, warp, lane, a.c64_terms != 1);
+        dense_stage_tf32(tp, S, gm2, base, warp, lane, a.c64_terms != 1, s_o8 + st * kC64Off);
         __syncthreads();
         continue;
       }
@@ -1709,7 +1802,7 @@ __global__ void __launch_bounds__(256, SV_C64_CTAS) k_pass_c64(float2* __restric
 
 size_t c64_pass_smem_bytes(int k, int nops, int nstages, int nmats) {
   return (size_t(8) << k) * 2 + (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16 +
-         (size_t)nmats * 8 + 4 * 64 * 8;
+         (size_t)nmats * 8 + 4 * 64 * 8 + (size_t)nstages * kC64Off * 2;
 }
 
 __global__ void k_widen(const float2* __restrict__ a, double2* __restrict__ b, int64_t n) {
@@ -1721,9 +1814,9 @@ __global__ void k_narrow(const double2* __restrict__ a, float2* __restrict__ b, 
     tile_st(b[i], a[i]);
 }
 
-size_t dense_pass_smem_bytes(int k, int nstages) {
-  return (size_t(16) << k) * SV_DENSE_NBUF + (size_t)nstages * sizeof(StageDesc) + 16 + 4 * 64 * 8 +
-         (size_t)nstages * 256 * 4;
+size_t dense_pass_smem_bytes(int k, int nstages, bool c64) {
+  return (size_t(c64 ? 8 : 16) << k) * SV_DENSE_NBUF + 16 + (size_t)nstages * sizeof(StageDesc) + 16 + 4 * 64 * 8 +
+         (size_t)nstages * 256 * 4 + (size_t)nstages * (8 + 32 + 32 + 8) * 2;
 }
 
 
@@ -1752,7 +1845,8 @@ static cudaError_t set_reg_attrs() {
   return once_per_device(done, [] {
     cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     return e;
   });
 }
@@ -1786,8 +1880,8 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual) {
                                      pd.n_grad, nthr, dual, n_da, acc_thread);
   int blocks = 0;
   if (pass_all_dense(plan, pd)) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense, nthr,
-                                                                  dense_pass_smem_bytes(pd.k, pd.stage_end - pd.stage_begin));
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense<double2>, nthr,
+                                                                  dense_pass_smem_bytes(pd.k, pd.stage_end - pd.stage_begin, false));
     return (e == cudaSuccess && blocks > 0) ? blocks : 1;
   }
   cudaError_t e = dual ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem)
@@ -1844,7 +1938,7 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   } else {
     if (pd.R != 3) return cudaErrorInvalidValue;
     if (L.all_dense) {
-      k_pass_dense<<<L.grid, nthr, dense_pass_smem_bytes(a.k, a.nstages), s>>>(reinterpret_cast<double2*>(psi), a);
+      k_pass_dense<double2><<<L.grid, nthr, dense_pass_smem_bytes(a.k, a.nstages, false), s>>>(reinterpret_cast<double2*>(psi), a);
     } else {
       k_pass_reg<3, false><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
     }
@@ -1887,6 +1981,20 @@ cudaError_t launch_pass_c64(float* psi, const PassLaunch& L, cudaStream_t s) {
   a.stages = L.d_stages + pd.stage_begin;
   a.c64_terms = L.c64_terms;
   const int nthr = 1 << tb;
+  if (L.all_dense && L.c64_terms == 0) {
+    // FP64 Gauss DMMA stages on the widened tile (SV_OPT_C64_SPLIT = 0)
+    cudaError_t e = set_reg_attrs();
+    if (e != cudaSuccess) return e;
+    const size_t sm = dense_pass_smem_bytes(a.k, a.nstages, true);
+    if (sm > 227 * 1024) return cudaErrorInvalidValue;
+    int blocks = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense<float2>, nthr, sm);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = std::min<int64_t>(a.ntiles, (int64_t)device_sm_count() * std::max(1, blocks));
+    a.grid = (int)grid;
+    k_pass_dense<float2><<<(int)grid, nthr, sm, s>>>(reinterpret_cast<float2*>(psi), a);
+    return cudaGetLastError();
+  }
   const size_t smem = c64_pass_smem_bytes(a.k, a.nops, a.nstages, a.nmats);
   static std::atomic<uint64_t> attr{0};
   {

@@ -84,7 +84,10 @@ struct sv_state_s {
   std::vector<sv::CachedPlan*> plan_cache;  // owned, LRU (small)
   uint64_t plan_clock = 0;
   sv::PlanOptions opts;
-  int c64_split = 3;  // SV_OPT_C64_SPLIT
+#ifndef SV_C64_DEFAULT_SPLIT
+#define SV_C64_DEFAULT_SPLIT 3
+#endif
+  int c64_split = SV_C64_DEFAULT_SPLIT;  // SV_OPT_C64_SPLIT
   sv_stats stats{};
   sv::ShardState* shard = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> xev;  // exchange timing (start, end) on the stream

@@ -159,3 +159,23 @@ def test_c64_tolerance_detects_single_tf32(P):
         sv.close()
     assert errs[3] <= REL, errs
     assert errs[1] > 10 * REL, errs
+
+
+@pytest.mark.parametrize("n", [19, 21])
+def test_c64_fp64_dense_stages(P, n):
+    """SV_OPT_C64_SPLIT = 0: all-dense complex64 passes widen the tile to FP64 and run the Gauss DMMA
+    stages of the complex128 kernel (k_pass_dense<float2>), rounding to FP32 once per stage (no
+    2^-21 TF32 product error): inside REL and below the TF32 split's error on the same circuit (the
+    strict inequality also shows the FP64 path ran: from 19 qubits the planner's tiles hold 2^10+
+    amplitudes and passes of dense stages only appear)."""
+    w = W.random_circuit(n, 8, seed=100 + n)
+    ref = oracle.apply_circuit(n, w.gates)
+    errs = {}
+    for split in (0, 3):
+        sv = P.StateVectorC64(n)
+        sv.set_option(P.SV_OPT_C64_SPLIT, split)
+        sv.apply_circuit(w.gates)
+        errs[split] = rel_err(sv.get_state(), ref)
+        sv.close()
+    assert errs[0] <= REL, errs
+    assert errs[0] < errs[3], errs
