@@ -44,9 +44,9 @@ FP64_PEAK_PATH = os.path.join(ROOT, "profiles", "fp64_peak.json")  # tools/measu
 NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md; 900 GB/s nominal)
 TF32_SPLIT_PEAK_TFLOPS = 277.3 / 3  # measured mma.sync TF32 peak / 3 products (complex64 dense stages)
 # dram__bytes_read.sum + dram__bytes_write.sum per forward-pass launch from the committed ncu
-# --set full capture (profiles/r01_ncu_pass30_full.txt); None until captured.
-TRAFFIC_PER_LAUNCH = {"C4": (17.181665 + 17.543235) * 1e9}  # profiles/r01_ncu_pass30_full.txt (k_pass_dense)
-TRAFFIC_PER_LAUNCH_C64 = (8.614921 + 8.540025) * 1e9  # profiles/r01_ncu_c64_pass30_full.txt (k_pass_c64)
+# --set full capture (profiles/r02_ncu_pass30_full.txt); None until captured.
+TRAFFIC_PER_LAUNCH = {"C4": (17.184045 + 17.121930) * 1e9}  # profiles/r02_ncu_pass30_full.txt (k_pass_dense)
+TRAFFIC_PER_LAUNCH_C64 = (8.608543 + 8.541884) * 1e9  # profiles/r02_ncu_c64_pass30_full.txt (k_pass_c64)
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
 
 
