@@ -963,7 +963,7 @@ static int plan_grid_uncached(const Plan& plan, int n_local) {
     for (size_t i = 0; i < plan.passes.size(); ++i) {
       const PassDesc& p = plan.passes[i];
       const int64_t nt = 1ll << (n_local - p.k);
-      const int ctas = env > 0 ? env : reg_pass_ctas_per_sm(plan, i, dual);
+      const int ctas = env > 0 ? env : reg_pass_ctas_per_sm(plan, i, dual, n_local);
       const int64_t want = (int64_t)num_sms() * ctas;
       plan.pass_grid[i] = (int)(nt < want ? nt : want);
       mx = std::max(mx, plan.pass_grid[i]);

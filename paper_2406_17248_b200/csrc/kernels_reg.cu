@@ -61,8 +61,8 @@
 #ifndef SV_DUAL_CTRL_SPLIT
 #define SV_DUAL_CTRL_SPLIT 0  // 1: separate DUAL op code for ops with / without register controls
 #endif
-#ifndef SV_DUAL_SINGLE_BUF
-#define SV_DUAL_SINGLE_BUF 0  // 1: every adjoint pass single-buffers its tile (more CTAs per SM)
+#ifndef SV_DUAL_SINGLE_BUF_MAX_N
+#define SV_DUAL_SINGLE_BUF_MAX_N 26  // adjoint passes up to this many local qubits may single-buffer
 #endif
 
 namespace sv {
@@ -97,6 +97,8 @@ struct RegArgs {
   int32_t c64_terms;  // complex64 dense stages: 3 = hi/lo split products (default), 1 = hi only
   int32_t acc_thread; // adjoint: 1 = overlap partials per thread ([grad op][thread] in shared memory, summed
                       // once at the end), 0 = warp-shuffle reduced per op ([grad op][warp])
+  int32_t single_buf; // adjoint: one (psi, lambda) tile buffer (more resident CTAs; passes with adjoint
+                      // dense stages always)
   double* r_partials;  // adjoint dense stages: [da][warp][16 * 32][grid]
   int8_t tq[kMaxTileQubits + 3];
   int8_t oq[64];
@@ -1157,7 +1159,10 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
 
 // ---------------------------------------------------------------- the pass kernel
 
-template <int NR, bool DUAL>
+// SB (adjoint, compile-time): one (psi, lambda) tile buffer — its own instantiation, since the
+// single-buffered loop compiles leaner than a runtime choice (C2 / C3 +5-8% at <= 26 local qubits;
+// 30-qubit adjoint passes keep the double buffer, whose hidden tile load is worth more there)
+template <int NR, bool DUAL, bool SB = false>
 __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD_CTAS) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1166,7 +1171,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   const uint32_t NB = DUAL ? 2 * N : N;  // doubles2 per buffer (psi [+ lambda])
   double2* smem_tiles = reinterpret_cast<double2*>(smem_raw);
   double2* tp = smem_tiles;  // (setup-phase alias; the tile loop rebinds per buffer)
-  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + ((DUAL && (a.n_da > 0 || SV_DUAL_SINGLE_BUF)) ? 1 : 2) * NB);
+  RegOp* s_ops = reinterpret_cast<RegOp*>(smem_tiles + ((DUAL && (a.n_da > 0 || SB)) ? 1 : 2) * NB);
   StageDesc* s_st = reinterpret_cast<StageDesc*>(s_ops + a.nops);
   double* s_mats = smem_align16<double>(smem_raw, s_st + a.nstages);
   // tile index -> base offset of its outer qubits: four 64-entry deposit tables (tile bits
@@ -1233,7 +1238,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
   // Adjoint passes with adjoint dense stages keep ONE (psi, lambda) tile buffer: their R
   // accumulators need the shared memory, and a third CTA per SM hides the exposed load better than
   // a second buffer does (the other passes double-buffer).
-  const bool dbuf = !(DUAL && (a.n_da > 0 || SV_DUAL_SINGLE_BUF));
+  const bool dbuf = !(DUAL && (a.n_da > 0 || SB));
   if (dbuf && (int64_t)blockIdx.x < a.ntiles) issue_load(blockIdx.x, 0);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
@@ -1821,8 +1826,8 @@ size_t dense_pass_smem_bytes(int k, int nstages, bool c64) {
 
 
 size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da,
-                      bool acc_thread) {
-  size_t b = (size_t(16) << k) * (dual ? 2 : 1) * ((dual && (n_da > 0 || SV_DUAL_SINGLE_BUF)) ? 1 : 2);  // tile buffers
+                      bool acc_thread, bool single_buf) {
+  size_t b = (size_t(16) << k) * (dual ? 2 : 1) * ((dual && (n_da > 0 || single_buf)) ? 1 : 2);  // tile buffers
   b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
   b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
   b += (size_t)nmats * 8 + 4 * 64 * 8;
@@ -1844,6 +1849,7 @@ static cudaError_t set_reg_attrs() {
   static std::atomic<uint64_t> done{0};
   return once_per_device(done, [] {
     cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1853,7 +1859,7 @@ static cudaError_t set_reg_attrs() {
 
 // Resident CTAs per SM for the register passes of a plan: the largest pass' shared memory decides
 // (one persistent grid serves every pass of the plan, so it must not exceed what is co-resident).
-int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual) {
+int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual, int n_local) {
   if (set_reg_attrs() != cudaSuccess) return 1;
   const PassDesc& pd = plan.passes[i];
   if (pd.R == 0) return 1;
@@ -1867,24 +1873,31 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual) {
   if (dual) {
     int b_warp = 0, b_thr = 0;
     const size_t sw = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, false);
+                                     pd.n_grad, nthr, dual, n_da, false, false);
     const size_t st = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, true);
+                                     pd.n_grad, nthr, dual, n_da, true, false);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_warp, k_pass_reg<3, true>, nthr, sw);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_thr, k_pass_reg<3, true>, nthr, st);
     acc_thread = b_thr >= b_warp && b_thr > 0 && pd.n_grad > 0;
     if (plan.pass_acc.size() != plan.passes.size()) plan.pass_acc.assign(plan.passes.size(), 0);
-    plan.pass_acc[i] = acc_thread ? 1 : 0;
+    plan.pass_acc[i] = acc_thread ? kPassAccThread : 0;
   }
+  // adjoint passes of states up to SV_DUAL_SINGLE_BUF_MAX_N local qubits: one (psi, lambda) tile
+  // buffer (a third resident CTA where shared memory limited it, a smaller footprint otherwise:
+  // C2 / C3 +5-8% measured; only where it adds a CTA: +0-2%; at 30 qubits the exposed tile load
+  // costs more: C4g -1%)
+  const bool single_buf = dual && n_da == 0 && n_local <= SV_DUAL_SINGLE_BUF_MAX_N;
+  if (single_buf) plan.pass_acc[i] |= kPassSingleBuf;
   const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, acc_thread);
+                                     pd.n_grad, nthr, dual, n_da, acc_thread, single_buf);
   int blocks = 0;
   if (pass_all_dense(plan, pd)) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense<double2>, nthr,
                                                                   dense_pass_smem_bytes(pd.k, pd.stage_end - pd.stage_begin, false));
     return (e == cudaSuccess && blocks > 0) ? blocks : 1;
   }
-  cudaError_t e = dual ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem)
+  cudaError_t e = dual ? (single_buf ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true, true>, nthr, smem)
+                                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem))
                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false>, nthr, smem);
   return (e == cudaSuccess && blocks > 0) ? blocks : 1;
 }
@@ -1924,8 +1937,10 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   a.n_da = L.n_da;
   a.pstride = L.pstride > 0 ? L.pstride : L.grid;
   a.r_partials = L.r_partials;
-  a.acc_thread = dual ? L.acc_thread : 0;
-  const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual, a.n_da, a.acc_thread != 0);
+  a.acc_thread = dual ? (L.acc_thread & kPassAccThread) : 0;
+  a.single_buf = dual ? ((L.acc_thread & kPassSingleBuf) ? 1 : 0) : 0;
+  const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual, a.n_da, a.acc_thread != 0,
+                                     a.single_buf != 0);
   {
     cudaError_t e = set_reg_attrs();
     if (e != cudaSuccess) return e;
@@ -1934,7 +1949,10 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   if (dual && nthr > 128) return cudaErrorInvalidValue;  // adjoint passes run 2^10-amplitude tiles
   if (dual) {
     if (pd.R != 3) return cudaErrorInvalidValue;
-    k_pass_reg<3, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
+    if (a.single_buf && a.n_da == 0)
+      k_pass_reg<3, true, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
+    else
+      k_pass_reg<3, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
   } else {
     if (pd.R != 3) return cudaErrorInvalidValue;
     if (L.all_dense) {

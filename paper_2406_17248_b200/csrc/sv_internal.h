@@ -126,6 +126,7 @@ struct StageDesc {
                              // TF32 fragment lanes, chosen on the host for few bank conflicts
 };
 static_assert(sizeof(StageDesc) == 312, "StageDesc layout");
+constexpr uint8_t kPassAccThread = 1, kPassSingleBuf = 2;  // Plan::pass_acc flags
 
 
 // Compact op of the register kernel (32 bytes: two 16-byte shared loads per op).
@@ -209,7 +210,8 @@ struct Plan {
   int64_t n_src_gates = 0;  // bound gates the plan applies (cost counter: x1 forward, x2 adjoint)
   mutable int grid_cache = 0, grid_cache_n = -1;  // plan_grid memo (occupancy query once per plan)
   mutable std::vector<int> pass_grid;             // per-pass CTAs (register passes: occupancy of that pass)
-  mutable std::vector<uint8_t> pass_acc;          // adjoint passes: 1 = per-thread overlap accumulators
+  mutable std::vector<uint8_t> pass_acc;          // adjoint passes: bit 0 (kPassAccThread) per-thread overlap
+                                                  // accumulators, bit 1 (kPassSingleBuf) single-buffered tile
   std::shared_ptr<PlanJobs> jobs;                 // dense-variant / adjoint-B fills (re-run on refresh)
 };
 constexpr int kMaxDAPerPass = 4;  // adjoint dense stages per pass (16 KiB of R accumulators each at 2^10 tiles; measured best, profiles/r01_da_per_pass_sweep.txt)
@@ -290,7 +292,7 @@ cudaError_t launch_widen(const float* a, double* b, int64_t n, cudaStream_t s);
 cudaError_t launch_narrow(const double* a, float* b, int64_t n, cudaStream_t s);
 int pass_grid(int n_local, int k, bool dual);
 int plan_grid(const Plan& plan, int n_local);
-int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual);
+int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual, int n_local);
 bool pass_all_dense(const Plan& plan, const PassDesc& pd);  // k_pass_dense eligible  // resident CTAs/SM of a register pass
 
 cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
