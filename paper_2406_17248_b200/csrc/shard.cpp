@@ -557,14 +557,27 @@ int shard_get_state(sv_state_s* h, double* host) {
       if (e != cudaSuccess) return cuda_fail(h, e, "get_state");
     }
   } else {
+    // chunked all-gather: a (P x chunk) device buffer instead of the whole 2^n state on every GPU
+    // (256 GiB at 34 qubits); rank r's chunk lands at its shard's offset in physical order
+    const uint64_t P = (uint64_t)h->world;
+    const uint64_t CH = std::min<uint64_t>(NL, uint64_t(1) << 24);  // amplitudes per rank and chunk
     DevBuf all;
-    if (!all.ensure(N * 16)) return fail(SV_E_OOM, "gather buffer");
-    ncclResult_t r = ncclAllGather(S.bufs[0].p, all.p, NL * 2, ncclDouble, S.comm, h->stream);
-    if (r != ncclSuccess) { all.release(); return nccl_fail(h, r, "allgather"); }
-    cudaError_t e = cudaMemcpyAsync(phys.data(), all.p, N * 16, cudaMemcpyDeviceToHost, h->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (!all.ensure(P * CH * 16)) return fail(SV_E_OOM, "gather buffer");
+    for (uint64_t c0 = 0; c0 < NL; c0 += CH) {
+      const uint64_t cn = std::min(CH, NL - c0);
+      ncclResult_t r = ncclAllGather(static_cast<const double*>(S.bufs[0].p) + 2 * c0, all.p, cn * 2, ncclDouble,
+                                     S.comm, h->stream);
+      if (r != ncclSuccess) { all.release(); return nccl_fail(h, r, "allgather"); }
+      for (uint64_t rk = 0; rk < P; ++rk) {
+        cudaError_t e = cudaMemcpyAsync(phys.data() + 2 * (NL * rk + c0), static_cast<const double*>(all.p) + 2 * cn * rk,
+                                        cn * 16, cudaMemcpyDeviceToHost, h->stream);
+        if (e != cudaSuccess) { all.release(); return cuda_fail(h, e, "get_state"); }
+      }
+      // the next chunk's all-gather reuses the buffer: wait for the copies out of it
+      cudaError_t e = cudaStreamSynchronize(h->stream);
+      if (e != cudaSuccess) { all.release(); return cuda_fail(h, e, "get_state"); }
+    }
     all.release();
-    if (e != cudaSuccess) return cuda_fail(h, e, "get_state");
   }
   cudaError_t e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "get_state");
