@@ -61,8 +61,12 @@
 #ifndef SV_DUAL_CTRL_SPLIT
 #define SV_DUAL_CTRL_SPLIT 0  // 1: separate DUAL op code for ops with / without register controls
 #endif
+#ifndef SV_DUAL_SB_CTAS
+#define SV_DUAL_SB_CTAS 4  // single-buffered adjoint instantiation: CTAs per SM of its register cap
+                           // (4: 128 registers, a few spills, still +3-7% over 3 at 168)
+#endif
 #ifndef SV_DUAL_SINGLE_BUF_MAX_N
-#define SV_DUAL_SINGLE_BUF_MAX_N 26  // adjoint passes up to this many local qubits may single-buffer
+#define SV_DUAL_SINGLE_BUF_MAX_N 64  // adjoint passes up to this many local qubits single-buffer
 #endif
 
 namespace sv {
@@ -1159,11 +1163,12 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
 
 // ---------------------------------------------------------------- the pass kernel
 
-// SB (adjoint, compile-time): one (psi, lambda) tile buffer — its own instantiation, since the
-// single-buffered loop compiles leaner than a runtime choice (C2 / C3 +5-8% at <= 26 local qubits;
-// 30-qubit adjoint passes keep the double buffer, whose hidden tile load is worth more there)
+// SB (adjoint, compile-time): passes without adjoint dense stages — one (psi, lambda) tile buffer
+// and no adjoint-dense-stage code, so the instantiation fits 128 registers and 4 CTAs per SM
+// (C2 445 -> 476, C3 45.0 -> 46.6, C4g 2.41 -> 2.44 grad evals/s; a runtime single-buffer flag in
+// the general kernel measured slower than this separate instantiation)
 template <int NR, bool DUAL, bool SB = false>
-__global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD_CTAS) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
+__global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? (SB ? SV_DUAL_SB_CTAS : SV_DUAL_CTAS) : SV_FWD_CTAS) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
@@ -1260,7 +1265,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? SV_DUAL_CTAS : SV_FWD
     // ---- stages ----
     for (int st = 0; st < a.nstages; ++st) {
       const StageDesc& S = s_st[st];
-      if constexpr (DUAL) {
+      if constexpr (DUAL && !SB) {  // (single-buffered passes carry no adjoint dense stages)
         if (S.dense == 2) {
           uint32_t ov = 0;  // outer variant of this tile: its own R slot
           for (int b = 0; b < S.m_outer; ++b) ov |= (uint32_t)((base >> S.var_outer[b]) & 1ull) << b;
@@ -1882,10 +1887,7 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual, int n_local) {
     if (plan.pass_acc.size() != plan.passes.size()) plan.pass_acc.assign(plan.passes.size(), 0);
     plan.pass_acc[i] = acc_thread ? kPassAccThread : 0;
   }
-  // adjoint passes of states up to SV_DUAL_SINGLE_BUF_MAX_N local qubits: one (psi, lambda) tile
-  // buffer (a third resident CTA where shared memory limited it, a smaller footprint otherwise:
-  // C2 / C3 +5-8% measured; only where it adds a CTA: +0-2%; at 30 qubits the exposed tile load
-  // costs more: C4g -1%)
+  // adjoint passes without adjoint dense stages: the single-buffered, 4-CTA instantiation
   const bool single_buf = dual && n_da == 0 && n_local <= SV_DUAL_SINGLE_BUF_MAX_N;
   if (single_buf) plan.pass_acc[i] |= kPassSingleBuf;
   const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
