@@ -2,7 +2,7 @@
 # Round-2 evidence batch (run under gpurun from the repo root): GPU tests, smoke, every bench line,
 # the ncu launch list of the default bench command and full captures of the dominant kernels.
 set -x
-O=gpurun_out/r02f
+O=gpurun_out/${R02_OUT:-r02f}
 mkdir -p $O
 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
@@ -20,7 +20,7 @@ ncu --set full --clock-control none --import-source on -k regex:k_pass_dense -s 
 ncu --set full --clock-control none --import-source on -k regex:k_pass_c64 -s 20 -c 1 \
     -o $O/prof_c64 python bench.py --precision c64 --no-cpu-baseline --no-grad --steps 1 --warmup 1 > $O/ncu_c64.log 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:k_pass_reg<\(int\)3, \(bool\)1>' -s 7 -c 1 -o $O/prof_dual_da python tools/prof_config.py C4g 1 > $O/ncu_dual_da.log 2>&1
+    -k 'regex:k_pass_reg<\(int\)3, \(bool\)1, \(bool\)0>' -s 3 -c 1 -o $O/prof_dual_da python tools/prof_config.py C4g 1 > $O/ncu_dual_da.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pauli_tile -s 3 -c 1 \
     -o $O/prof_pauli python tools/prof_config.py C4g 1 > $O/ncu_pauli.log 2>&1
 echo done
