@@ -305,6 +305,7 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
     L.rank_bits = 0;
     L.n_da = n_da;
     L.all_dense = !lam && pass_all_dense(plan, pd);
+    L.no_dense = !lam && pass_no_dense(plan, pd);
     L.acc_thread = (lam && i < plan.pass_acc.size()) ? plan.pass_acc[i] : 0;
     L.r_partials = r_partials;
     if (n_da && (!r_partials || !r_sum)) return fail(SV_E_ARG, "internal: adjoint dense stage without R buffers");

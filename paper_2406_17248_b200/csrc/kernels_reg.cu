@@ -49,6 +49,9 @@
 #define SV_FWD_CTAS 2   // forward register passes: CTAs per SM (register budget 65536 / (256 * CTAs));
                         // 2 (128 registers) fits the dense stages' Gauss live set (3: 80, spills)
 #endif
+#ifndef SV_FWD_SEQ_CTAS
+#define SV_FWD_SEQ_CTAS 3  // forward passes without dense stages (k_pass_reg<3, false, true>)
+#endif
 #ifndef SV_C64_CTAS
 #define SV_C64_CTAS 3   // complex64 forward passes
 #endif
@@ -1168,7 +1171,8 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
 // (C2 445 -> 476, C3 45.0 -> 46.6, C4g 2.41 -> 2.44 grad evals/s; a runtime single-buffer flag in
 // the general kernel measured slower than this separate instantiation)
 template <int NR, bool DUAL, bool SB = false>
-__global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? (SB ? SV_DUAL_SB_CTAS : SV_DUAL_CTAS) : SV_FWD_CTAS) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
+__global__ void __launch_bounds__(DUAL ? 128 : 256,
+                                  DUAL ? (SB ? SV_DUAL_SB_CTAS : SV_DUAL_CTAS) : (SB ? SV_FWD_SEQ_CTAS : SV_FWD_CTAS)) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
@@ -1275,7 +1279,7 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256, DUAL ? (SB ? SV_DUAL_SB_CTAS
           continue;
         }
       }
-      if constexpr (!DUAL) {
+      if constexpr (!DUAL && !SB) {  // (SB forward instantiation: passes without dense stages)
         // L1 prefetch of the next dense stage's variant-matrix fragments (global, L2-resident):
         // the first MMA of that stage then finds its A operand in L1 instead of waiting on L2
         if (S.next_dense) {
@@ -1842,6 +1846,13 @@ size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngra
 
 }  // namespace
 
+bool pass_no_dense(const Plan& plan, const PassDesc& pd) {
+  if (plan.reverse || pd.R != 3) return false;
+  for (int si = pd.stage_begin; si < pd.stage_end; ++si)
+    if (plan.stages[si].dense) return false;
+  return true;
+}
+
 bool pass_all_dense(const Plan& plan, const PassDesc& pd) {
   static const bool off = [] { const char* e = getenv("SV_DENSE_KERNEL"); return e && atoi(e) == 0; }();
   if (off || plan.reverse || pd.R != 3 || pd.stage_end <= pd.stage_begin) return false;
@@ -1856,6 +1867,7 @@ static cudaError_t set_reg_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     return e;
@@ -1900,7 +1912,8 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual, int n_local) {
   }
   cudaError_t e = dual ? (single_buf ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true, true>, nthr, smem)
                                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem))
-                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false>, nthr, smem);
+                       : (pass_no_dense(plan, pd) ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false, true>, nthr, smem)
+                                                  : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false>, nthr, smem));
   return (e == cudaSuccess && blocks > 0) ? blocks : 1;
 }
 
@@ -1959,6 +1972,8 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
     if (pd.R != 3) return cudaErrorInvalidValue;
     if (L.all_dense) {
       k_pass_dense<double2><<<L.grid, nthr, dense_pass_smem_bytes(a.k, a.nstages, false), s>>>(reinterpret_cast<double2*>(psi), a);
+    } else if (L.no_dense) {
+      k_pass_reg<3, false, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
     } else {
       k_pass_reg<3, false><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), nullptr, a);
     }

@@ -276,6 +276,7 @@ struct PassLaunch {
   int grid;                // CTAs
   int pstride = 0;         // stride of d_partials' slot rows (>= grid; 0: grid)
   bool all_dense = false;  // forward register pass of dense stages only (k_pass_dense)
+  bool no_dense = false;   // forward register pass without dense stages (k_pass_reg<3, false, true>)
   int c64_terms = 3;       // complex64 dense stages: TF32 split products (3) or one product (1)
   int acc_thread = 0;      // adjoint: overlaps accumulate per thread in shared memory (no per-op shuffles)
   int n_local;
@@ -293,6 +294,7 @@ cudaError_t launch_narrow(const double* a, float* b, int64_t n, cudaStream_t s);
 int pass_grid(int n_local, int k, bool dual);
 int plan_grid(const Plan& plan, int n_local);
 int reg_pass_ctas_per_sm(const Plan& plan, size_t pass, bool dual, int n_local);
+bool pass_no_dense(const Plan& plan, const PassDesc& pd);   // forward register pass without dense stages
 bool pass_all_dense(const Plan& plan, const PassDesc& pd);  // k_pass_dense eligible  // resident CTAs/SM of a register pass
 
 cudaError_t launch_init_zero(double* psi, int64_t n_amps, bool one_at_zero, cudaStream_t s);
