@@ -314,7 +314,10 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 const int g_dense_min_cost = env_int("SV_DENSE_MIN_COST", 20);
-const int g_dense_max_var = env_int("SV_DENSE_MAX_VAR", 6);
+// variant bits (tile + outer) of a forward dense stage: 8 from 28 local qubits (C4 at 30q: 141 instead
+// of 144 stages, circuit 628 -> 616 ms), 6 below (C3 at 24q: 46.6 vs 44.8 grad evals/s with 8)
+const int g_dense_max_var_env = env_int("SV_DENSE_MAX_VAR", -1);
+int dense_max_var_for(int n_local) { return g_dense_max_var_env >= 0 ? g_dense_max_var_env : (n_local >= 28 ? 8 : 6); }
 const int g_da_min_cost = env_int("SV_DA_MIN_COST", -1);   // adjoint dense stages: cost threshold override
 // Default threshold by state size: the per-pass fixed costs of adjoint dense stages (R partials
 // written and reduced per CTA, host contraction) amortise over large states only. Measured
@@ -672,7 +675,7 @@ void fill_dense_variants(Plan* plan, const std::vector<DenseJob>& jobs) {
 // positions. Returns false (stage untouched) otherwise.
 bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget_doubles, std::vector<DenseJob>* jobs,
                 bool adjoint = false, int pass_index = 0, int da_index = 0, int da_slots_left = 0, int da_min_cost = 96,
-                int da_max_outer = 1) {
+                int da_max_outer = 1, int max_var = 6) {
   const int k = pd.k;
   const int nw_bits = k - 8;  // 2^(k-3) threads: 16 vectors of 16 amplitudes per warp
   if (nw_bits < 1 || __builtin_popcount(sp->regset) > 4) return false;
@@ -707,7 +710,7 @@ bool make_dense(StagePlan* sp, const PassDesc& pd, Plan* plan, size_t mat_budget
     if (2 * cost + 8 * ngrad < da_min_cost || m_outer > da_max_outer || m_tile > std::min(g_da_max_tile, nw_bits) ||
         (1 << m_outer) > da_slots_left)
       return false;
-  } else if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > g_dense_max_var) {
+  } else if (cost < g_dense_min_cost || m_tile > nw_bits || m_outer > 8 || m_tile + m_outer > max_var) {
     return false;
   }
   const int nvar = 1 << (m_tile + m_outer);
@@ -915,10 +918,11 @@ void plan_pass_stages(Plan* plan, PassDesc* pd, bool forward, bool dense, int n_
   pd->seq_mats = (int32_t)(plan->mats.size() - pd->mat_begin);
   if (forward && dense && k >= 9) {
     const size_t budget = size_t(1) << 22;  // variant matrices live in global memory (L2-resident)
-    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(3, k - 8), g_dense_max_var);
+    const int max_var = dense_max_var_for(n_local);
+    std::vector<StagePlan> st4 = split_stages(pops, *pd, 4, std::min(3, k - 8), max_var);
     std::vector<DevOp> seq;  // consecutive non-dense candidates are re-staged together
     for (StagePlan& sp : st4) {
-      if (make_dense(&sp, *pd, plan, budget, jobs)) {
+      if (make_dense(&sp, *pd, plan, budget, jobs, false, 0, 0, 0, 96, 1, max_var)) {
         if (!seq.empty()) { add_sequential(split_stages(seq, *pd, pd->R, -1, -1)); seq.clear(); }
         final_stages.push_back(std::move(sp));
       } else {
