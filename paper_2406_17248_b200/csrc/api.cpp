@@ -314,7 +314,11 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
     h->stats.kernel_launches += 1;
     if (n_da) {
       const int nw = (1 << (pd.k - pd.R)) / 32;
-      e = launch_reduce_slots(r_partials, n_da * nw * 512, L.grid, r_sum + da_done * (size_t)nw * 512, h->stream);
+      // R partials: per-CTA contiguous when accumulated in global memory, slot-major otherwise
+      e = da_r_global(h->n_local)
+              ? launch_reduce_strided(r_partials, (int64_t)n_da * nw * 512, L.grid, r_sum + da_done * (size_t)nw * 512,
+                                      h->stream)
+              : launch_reduce_slots(r_partials, n_da * nw * 512, L.grid, r_sum + da_done * (size_t)nw * 512, h->stream);
       if (e != cudaSuccess) return cuda_fail(h, e, "R reduction");
       h->stats.kernel_launches += 1;
       da_done += (size_t)n_da;

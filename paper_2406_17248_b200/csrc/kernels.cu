@@ -901,6 +901,16 @@ __global__ void __launch_bounds__(kThreads) k_reduce_slots(const double* __restr
   if (threadIdx.x == 0) out[blockIdx.x] = acc;
 }
 
+// out[i] = sum over g < n_cta of p[g * per + i], in g order (per-CTA contiguous partials)
+__global__ void __launch_bounds__(kThreads) k_reduce_strided(const double* __restrict__ p, int64_t per, int n_cta,
+                                                             double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int g = 0; g < n_cta; ++g) acc += p[(int64_t)g * per + i];
+    out[i] = acc;
+  }
+}
+
 size_t pass_smem_bytes(int k, int low, int nops, int nmats, bool dual) {
   const size_t N = size_t(1) << k;
   size_t b = N * 16 * (dual ? 2 : 1);
@@ -1039,6 +1049,13 @@ cudaError_t launch_pauli_group(const double* psi, double* lam, bool lam_accumula
 
 cudaError_t launch_redot(const double* x, const double* y, int64_t n, double* d_partials, int grid, cudaStream_t s) {
   k_redot<<<grid, kThreads, 0, s>>>(reinterpret_cast<const double2*>(x), reinterpret_cast<const double2*>(y), n, d_partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_strided(const double* d_partials, int64_t per, int n_cta, double* d_out, cudaStream_t s) {
+  if (per <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((per + kThreads - 1) / kThreads, (int64_t)num_sms() * 4);
+  k_reduce_strided<<<blocks, kThreads, 0, s>>>(d_partials, per, n_cta, d_out);
   return cudaGetLastError();
 }
 

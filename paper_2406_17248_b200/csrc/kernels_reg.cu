@@ -1170,7 +1170,9 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
 // and no adjoint-dense-stage code, so the instantiation fits 128 registers and 4 CTAs per SM
 // (C2 445 -> 476, C3 45.0 -> 46.6, C4g 2.41 -> 2.44 grad evals/s; a runtime single-buffer flag in
 // the general kernel measured slower than this separate instantiation)
-template <int NR, bool DUAL, bool SB = false>
+// RG (adjoint, compile-time): the adjoint dense stages' R accumulators live in the CTA's own
+// L2-resident region of r_partials instead of shared memory (da_r_global: from 26 local qubits)
+template <int NR, bool DUAL, bool SB = false, bool RG = false>
 __global__ void __launch_bounds__(DUAL ? 128 : 256,
                                   DUAL ? (SB ? SV_DUAL_SB_CTAS : SV_DUAL_CTAS) : (SB ? SV_FWD_SEQ_CTAS : SV_FWD_CTAS)) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
@@ -1188,7 +1190,11 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256,
   uint64_t* s_ob = reinterpret_cast<uint64_t*>(s_mats + a.nmats);
   const int nacc = a.acc_thread ? nthr : nwarps;            // overlap accumulators per grad op
   double* s_acc = reinterpret_cast<double*>(s_ob + 4 * 64);  // [ngrad][nacc]
-  double* s_racc = s_acc + (DUAL ? a.ngrad * nacc : 0);     // [n_da][nwarps][512]
+  // adjoint dense stages' R accumulators [n_da][nwarps][512]: shared memory, or (RG) this CTA's own
+  // L2-resident region of r_partials ([grid][n_da][nwarps][512]), which frees their 16 KiB per slot
+  // of shared memory for a third CTA
+  double* s_racc = (DUAL && RG) ? a.r_partials + (size_t)blockIdx.x * ((size_t)a.n_da * nwarps * 512)
+                                : s_acc + (DUAL ? a.ngrad * nacc : 0);
 
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.ops);
@@ -1379,8 +1385,9 @@ __global__ void __launch_bounds__(DUAL ? 128 : 256,
     // last stage ended with one
   }
   if (DUAL) {
-    for (int i = tid; i < a.n_da * nwarps * 512; i += nthr)
-      a.r_partials[(int64_t)i * a.grid + blockIdx.x] = s_racc[i];
+    if constexpr (!RG)
+      for (int i = tid; i < a.n_da * nwarps * 512; i += nthr)
+        a.r_partials[(int64_t)i * a.grid + blockIdx.x] = s_racc[i];
     for (int i = tid; i < a.nops; i += nthr) {
       const Op o = load_op(s_ops + i);
       if (!o.gen()) continue;
@@ -1835,9 +1842,9 @@ size_t dense_pass_smem_bytes(int k, int nstages, bool c64) {
 
 
 size_t reg_smem_bytes(int k, int low, int nops, int nstages, int nmats, int ngrad, int nthr, bool dual, int n_da,
-                      bool acc_thread, bool single_buf) {
+                      bool acc_thread, bool single_buf, bool r_global) {
   size_t b = (size_t(16) << k) * (dual ? 2 : 1) * ((dual && (n_da > 0 || single_buf)) ? 1 : 2);  // tile buffers
-  b += dual ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
+  b += (dual && !r_global) ? (size_t)n_da * (nthr / 32) * 512 * 8 : 0;
   b += (size_t)nops * sizeof(RegOp) + (size_t)nstages * sizeof(StageDesc) + 16;
   b += (size_t)nmats * 8 + 4 * 64 * 8;
   b += dual ? (size_t)ngrad * (acc_thread ? nthr : nthr / 32) * 8 : 0;
@@ -1866,6 +1873,7 @@ static cudaError_t set_reg_attrs() {
   return once_per_device(done, [] {
     cudaError_t e = cudaFuncSetAttribute(k_pass_reg<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_reg<3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pass_dense<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1890,9 +1898,9 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual, int n_local) {
   if (dual) {
     int b_warp = 0, b_thr = 0;
     const size_t sw = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, false, false);
+                                     pd.n_grad, nthr, dual, n_da, false, false, da_r_global(n_local));
     const size_t st = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, true, false);
+                                     pd.n_grad, nthr, dual, n_da, true, false, da_r_global(n_local));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_warp, k_pass_reg<3, true>, nthr, sw);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_thr, k_pass_reg<3, true>, nthr, st);
     acc_thread = b_thr >= b_warp && b_thr > 0 && pd.n_grad > 0;
@@ -1903,7 +1911,7 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual, int n_local) {
   const bool single_buf = dual && n_da == 0 && n_local <= SV_DUAL_SINGLE_BUF_MAX_N;
   if (single_buf) plan.pass_acc[i] |= kPassSingleBuf;
   const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, acc_thread, single_buf);
+                                     pd.n_grad, nthr, dual, n_da, acc_thread, single_buf, da_r_global(n_local));
   int blocks = 0;
   if (pass_all_dense(plan, pd)) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense<double2>, nthr,
@@ -1911,7 +1919,9 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual, int n_local) {
     return (e == cudaSuccess && blocks > 0) ? blocks : 1;
   }
   cudaError_t e = dual ? (single_buf ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true, true>, nthr, smem)
-                                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem))
+                          : da_r_global(n_local)
+                              ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true, false, true>, nthr, smem)
+                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem))
                        : (pass_no_dense(plan, pd) ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false, true>, nthr, smem)
                                                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false>, nthr, smem));
   return (e == cudaSuccess && blocks > 0) ? blocks : 1;
@@ -1955,7 +1965,7 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
   a.acc_thread = dual ? (L.acc_thread & kPassAccThread) : 0;
   a.single_buf = dual ? ((L.acc_thread & kPassSingleBuf) ? 1 : 0) : 0;
   const size_t smem = reg_smem_bytes(a.k, a.low, a.nops, a.nstages, a.nmats, a.ngrad, nthr, dual, a.n_da, a.acc_thread != 0,
-                                     a.single_buf != 0);
+                                     a.single_buf != 0, dual && da_r_global(L.n_local));
   {
     cudaError_t e = set_reg_attrs();
     if (e != cudaSuccess) return e;
@@ -1966,6 +1976,8 @@ cudaError_t launch_pass_reg(double* psi, double* lam, const PassLaunch& L, cudaS
     if (pd.R != 3) return cudaErrorInvalidValue;
     if (a.single_buf && a.n_da == 0)
       k_pass_reg<3, true, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
+    else if (da_r_global(L.n_local))
+      k_pass_reg<3, true, false, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
     else
       k_pass_reg<3, true><<<L.grid, nthr, smem, s>>>(reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(lam), a);
   } else {

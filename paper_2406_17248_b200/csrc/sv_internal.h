@@ -127,6 +127,10 @@ struct StageDesc {
 };
 static_assert(sizeof(StageDesc) == 312, "StageDesc layout");
 constexpr uint8_t kPassAccThread = 1, kPassSingleBuf = 2;  // Plan::pass_acc flags
+// adjoint dense stages accumulate R in global (L2-resident, per CTA) instead of shared memory from
+// this many local qubits (C4g 2.45 -> 2.57 grad evals/s: a third CTA per SM; C2 at 20q loses 2%)
+constexpr int kDARGlobalMinN = 26;
+inline bool da_r_global(int n_local) { return n_local >= kDARGlobalMinN; }
 
 
 // Compact op of the register kernel (32 bytes: two 16-byte shared loads per op).
@@ -349,6 +353,8 @@ cudaError_t launch_pauli_cross(const double* psi, const double* partner, double*
                                int grid, bool first, cudaStream_t s);
 cudaError_t launch_reduce_slots(const double* d_partials, int n_slots, int per_slot, double* d_out,
                                 cudaStream_t s);
+// out[i] = sum over g < n_cta of partials[g * per + i] (per-CTA contiguous partials, fixed order)
+cudaError_t launch_reduce_strided(const double* d_partials, int64_t per, int n_cta, double* d_out, cudaStream_t s);
 // Re<x|y> per-CTA partials (grid of them)
 cudaError_t launch_redot(const double* x, const double* y, int64_t n, double* d_partials, int grid, cudaStream_t s);
 
