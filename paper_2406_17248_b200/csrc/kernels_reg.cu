@@ -68,6 +68,10 @@
 #define SV_DUAL_SB_CTAS 4  // single-buffered adjoint instantiation: CTAs per SM of its register cap
                            // (4: 128 registers, a few spills, still +3-7% over 3 at 168)
 #endif
+#ifndef SV_DUAL_RG_CTAS
+#define SV_DUAL_RG_CTAS 4  // adjoint passes with L2 R accumulators: CTAs per SM of the register cap
+                           // (4: 128 registers with spills, C4g 2.57 -> 2.62 over 3)
+#endif
 #ifndef SV_DUAL_SINGLE_BUF_MAX_N
 #define SV_DUAL_SINGLE_BUF_MAX_N 64  // adjoint passes up to this many local qubits single-buffer
 #endif
@@ -1174,7 +1178,8 @@ __device__ __forceinline__ void da_stage(double2* tp, double2* tl, const StageDe
 // L2-resident region of r_partials instead of shared memory (da_r_global: from 26 local qubits)
 template <int NR, bool DUAL, bool SB = false, bool RG = false>
 __global__ void __launch_bounds__(DUAL ? 128 : 256,
-                                  DUAL ? (SB ? SV_DUAL_SB_CTAS : SV_DUAL_CTAS) : (SB ? SV_FWD_SEQ_CTAS : SV_FWD_CTAS)) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
+                                  DUAL ? (SB ? SV_DUAL_SB_CTAS : (RG ? SV_DUAL_RG_CTAS : SV_DUAL_CTAS))
+                                       : (SB ? SV_FWD_SEQ_CTAS : SV_FWD_CTAS)) k_pass_reg(double2* __restrict__ psi, double2* __restrict__ lam,
                                                                   RegArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t N = 1u << a.k;
@@ -1893,35 +1898,37 @@ int reg_pass_ctas_per_sm(const Plan& plan, size_t i, bool dual, int n_local) {
   int n_da = 0;
   for (int si = pd.stage_begin; si < pd.stage_end; ++si) n_da += plan.stages[si].dense == 2 ? (1 << plan.stages[si].m_outer) : 0;
   const int nthr = 1 << (pd.k - pd.R);
-  // adjoint passes: per-thread overlap accumulators when they cost no resident CTA
+  // adjoint passes without adjoint dense stages: the single-buffered, 4-CTA instantiation; with
+  // them, from 26 local qubits the instantiation with L2 R accumulators
+  const bool single_buf = dual && n_da == 0 && n_local <= SV_DUAL_SINGLE_BUF_MAX_N;
+  const bool r_global = dual && da_r_global(n_local);
+  void (*dual_fn)(double2*, double2*, RegArgs) =
+      single_buf ? k_pass_reg<3, true, true> : r_global ? k_pass_reg<3, true, false, true> : k_pass_reg<3, true>;
+  // adjoint passes: per-thread overlap accumulators when they cost no resident CTA (queried on the
+  // instantiation that will run)
   bool acc_thread = false;
   if (dual) {
     int b_warp = 0, b_thr = 0;
     const size_t sw = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, false, false, da_r_global(n_local));
+                                     pd.n_grad, nthr, dual, n_da, false, single_buf, r_global);
     const size_t st = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, true, false, da_r_global(n_local));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_warp, k_pass_reg<3, true>, nthr, sw);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_thr, k_pass_reg<3, true>, nthr, st);
+                                     pd.n_grad, nthr, dual, n_da, true, single_buf, r_global);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_warp, dual_fn, nthr, sw);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_thr, dual_fn, nthr, st);
     acc_thread = b_thr >= b_warp && b_thr > 0 && pd.n_grad > 0;
     if (plan.pass_acc.size() != plan.passes.size()) plan.pass_acc.assign(plan.passes.size(), 0);
     plan.pass_acc[i] = acc_thread ? kPassAccThread : 0;
   }
-  // adjoint passes without adjoint dense stages: the single-buffered, 4-CTA instantiation
-  const bool single_buf = dual && n_da == 0 && n_local <= SV_DUAL_SINGLE_BUF_MAX_N;
   if (single_buf) plan.pass_acc[i] |= kPassSingleBuf;
   const size_t smem = reg_smem_bytes(pd.k, pd.low, pd.op_end - pd.op_begin, pd.stage_end - pd.stage_begin, nm,
-                                     pd.n_grad, nthr, dual, n_da, acc_thread, single_buf, da_r_global(n_local));
+                                     pd.n_grad, nthr, dual, n_da, acc_thread, single_buf, r_global);
   int blocks = 0;
   if (pass_all_dense(plan, pd)) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_dense<double2>, nthr,
                                                                   dense_pass_smem_bytes(pd.k, pd.stage_end - pd.stage_begin, false));
     return (e == cudaSuccess && blocks > 0) ? blocks : 1;
   }
-  cudaError_t e = dual ? (single_buf ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true, true>, nthr, smem)
-                          : da_r_global(n_local)
-                              ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true, false, true>, nthr, smem)
-                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, true>, nthr, smem))
+  cudaError_t e = dual ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dual_fn, nthr, smem)
                        : (pass_no_dense(plan, pd) ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false, true>, nthr, smem)
                                                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_pass_reg<3, false>, nthr, smem));
   return (e == cudaSuccess && blocks > 0) ? blocks : 1;
