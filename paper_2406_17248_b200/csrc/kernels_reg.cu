@@ -1602,9 +1602,26 @@ __constant__ uint32_t kPerm24[24] = {228, 180, 216, 120, 156, 108, 225, 177, 201
 // hi keeps the top 10 mantissa bits (truncation: one LOP3; cvt.rna.tf32 is a multi-instruction
 // sequence on sm_100a), lo = v - hi is exact in FP32 and the MMA reads its top 10 mantissa bits:
 // together ~21 bits, the dropped remainder is <= 2^-21 relative.
+#ifndef SV_TF32_RNA
+#define SV_TF32_RNA 2  // 2: hi rounded to nearest by an integer add (measured 2.5x smaller error than
+                       // truncation, +1% speed); 1: cvt.rna for hi and lo (same error, 10% slower)
+#endif
 __device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
+#if SV_TF32_RNA == 1
+  // hi and lo rounded to nearest TF32 (cvt.rna): |v - hi - lo| <= 2^-22 |v| instead of the
+  // truncation's lo read to 10 of its up to 13 bits
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v));
+  const float r = v - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+#elif SV_TF32_RNA == 2
+  // hi rounded to nearest by integer add on the bit pattern (ties away; |v| << FLT_MAX here):
+  // |lo| <= 2^-11 |v|, so the tensor core's 10-bit read of lo errs by <= 2^-21 |v|
+  hi = (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
+#else
   hi = __float_as_uint(v) & 0xFFFFE000u;
   lo = __float_as_uint(v - __uint_as_float(hi));
+#endif
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {

@@ -4,8 +4,8 @@ simulation modes") vs the complex128 CPU oracle.
 Tolerances are RELATIVE to the state (an absolute 1e-4 on amplitudes of size 2^(-n/2) would let a
 5% error per amplitude through). Derivation: a stored complex64 value carries 2^-24 ~ 6e-8
 relative rounding; a dense stage's 16-term products use the 3-product TF32 hi/lo split
-(hi = top 10 mantissa bits, lo = the rest, read by the tensor core to 10 bits) whose per-product
-error is ~2^-21 ~ 5e-7 relative, FP32 accumulation adds ~2^-24 per term. Over the <= ~30 stages of
+(hi = v rounded to 10 mantissa bits, lo = v - hi exact with |lo| <= 2^-11 |v|, read by the tensor
+core to 10 bits) whose per-product error is ~2^-21 ~ 5e-7 relative, FP32 accumulation adds ~2^-24 per term. Over the <= ~30 stages of
 these circuits, independent errors add in quadrature: ||d psi||_2 / ||psi||_2 ~ sqrt(30) * 6e-7
 ~ 3e-6, so REL = 1e-5 holds with margin. A single hi x hi TF32 product (2^-11 ~ 5e-4 relative)
 gives ~1e-3: `test_c64_tolerance_detects_single_tf32` shows the bound catches it. Energies are

@@ -20,7 +20,7 @@ ncu --set full --clock-control none --import-source on -k regex:k_pass_dense -s 
 ncu --set full --clock-control none --import-source on -k regex:k_pass_c64 -s 20 -c 1 \
     -o $O/prof_c64 python bench.py --precision c64 --no-cpu-baseline --no-grad --steps 1 --warmup 1 > $O/ncu_c64.log 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:k_pass_reg<\(int\)3, \(bool\)1, \(bool\)0>' -s 3 -c 1 -o $O/prof_dual_da python tools/prof_config.py C4g 1 > $O/ncu_dual_da.log 2>&1
+    -k 'regex:k_pass_reg<\(int\)3, \(bool\)1, \(bool\)0' -s 3 -c 1 -o $O/prof_dual_da python tools/prof_config.py C4g 1 > $O/ncu_dual_da.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pauli_tile -s 3 -c 1 \
     -o $O/prof_pauli python tools/prof_config.py C4g 1 > $O/ncu_pauli.log 2>&1
 echo done
