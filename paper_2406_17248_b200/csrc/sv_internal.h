@@ -129,7 +129,10 @@ static_assert(sizeof(StageDesc) == 312, "StageDesc layout");
 constexpr uint8_t kPassAccThread = 1, kPassSingleBuf = 2;  // Plan::pass_acc flags
 // adjoint dense stages accumulate R in global (L2-resident, per CTA) instead of shared memory from
 // this many local qubits (C4g 2.45 -> 2.57 grad evals/s: a third CTA per SM; C2 at 20q loses 2%)
-constexpr int kDARGlobalMinN = 26;
+#ifndef SV_DA_R_GLOBAL_MIN_N
+#define SV_DA_R_GLOBAL_MIN_N 26
+#endif
+constexpr int kDARGlobalMinN = SV_DA_R_GLOBAL_MIN_N;
 inline bool da_r_global(int n_local) { return n_local >= kDARGlobalMinN; }
 
 
