@@ -136,8 +136,26 @@ static uint64_t hash_bytes(const void* data, size_t n, uint64_t h) {
 }
 
 void release_plan_cache(sv_state_s* h) {
-  for (CachedPlan* c : h->plan_cache) { c->buf.release(); delete c; }
+  for (CachedPlan* c : h->plan_cache) {
+    c->buf.release();
+    if (c->used_ev) cudaEventDestroy(c->used_ev);
+    if (c->ready_ev) cudaEventDestroy(c->ready_ev);
+    delete c;
+  }
   h->plan_cache.clear();
+}
+
+// Records the plan's last use on the handle's stream (see CachedPlan::used_ev).
+static void mark_plan_used(sv_state_s* h, const CachedPlan& cp) {
+  CachedPlan& c = const_cast<CachedPlan&>(cp);
+  if (!c.used_ev && cudaEventCreateWithFlags(&c.used_ev, cudaEventDisableTiming) != cudaSuccess) {
+    c.used_ev = nullptr;
+    c.used_rec = false;
+    cudaGetLastError();
+    return;
+  }
+  c.used_rec = cudaEventRecord(c.used_ev, h->stream) == cudaSuccess;
+  if (!c.used_rec) cudaGetLastError();
 }
 
 struct PlanMeta {
@@ -241,7 +259,23 @@ static int upload_plan(sv_state_s* h, CachedPlan* c, uint64_t key, const CachedP
   const size_t ob = plan.ops.size() * sizeof(DevOp), sb = plan.stages.size() * sizeof(StageDesc),
                mb = plan.mats.size() * sizeof(double), rb = plan.rops.size() * sizeof(RegOp);
   const size_t so = al(ob), mo = so + al(sb), ro = mo + al(mb), total = ro + al(rb);
+  const void* old_p = c->buf.p;
+  const size_t old_cap = c->buf.cap;
   if (!c->buf.ensure_async(total + 64, h->stream)) return fail(SV_E_OOM, "plan buffers");
+  // an existing buffer whose last use is recorded is refilled on the upload stream (after that use)
+  // and the handle's stream waits for the copy: the copy overlaps the kernels queued before it; a
+  // (re)allocated buffer is stream-ordered on the handle's stream and is filled there
+  bool side = old_p != nullptr && c->buf.p == old_p && c->buf.cap == old_cap && c->used_rec;
+  if (side && !h->upload_stream &&
+      cudaStreamCreateWithFlags(&h->upload_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    h->upload_stream = nullptr;
+    cudaGetLastError();
+  }
+  if (side && !c->ready_ev && cudaEventCreateWithFlags(&c->ready_ev, cudaEventDisableTiming) != cudaSuccess) {
+    c->ready_ev = nullptr;
+    cudaGetLastError();
+  }
+  side = side && h->upload_stream && c->ready_ev;
   // page-locked staging: the copy is truly asynchronous (a pageable source would hold the host
   // until the stream reaches it); the previous upload from the same buffer must have completed
   cudaError_t e = cudaSuccess;
@@ -270,8 +304,16 @@ static int upload_plan(sv_state_s* h, CachedPlan* c, uint64_t key, const CachedP
   c->so = so;
   c->mo = mo;
   c->ro = ro;
-  if (total) e = cudaMemcpyAsync(c->buf.p, hs, total, cudaMemcpyHostToDevice, h->stream);
-  if (e == cudaSuccess) e = cudaEventRecord(h->plan_upload_done, h->stream);
+  if (side) {
+    e = cudaStreamWaitEvent(h->upload_stream, c->used_ev, 0);
+    if (e == cudaSuccess && total) e = cudaMemcpyAsync(c->buf.p, hs, total, cudaMemcpyHostToDevice, h->upload_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(h->plan_upload_done, h->upload_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ready_ev, h->upload_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, c->ready_ev, 0);
+  } else {
+    if (total) e = cudaMemcpyAsync(c->buf.p, hs, total, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(h->plan_upload_done, h->stream);
+  }
   if (e != cudaSuccess) return cuda_fail(h, e, "plan upload");
   c->key = key;
   c->stamp = ++h->plan_clock;
@@ -284,6 +326,7 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
              double* r_partials, double* r_sum) {
   const Plan& plan = cp.plan;
   const char* base = static_cast<const char*>(cp.buf.p);
+  const_cast<CachedPlan&>(cp).used_rec = false;  // (until all passes are enqueued: mark_plan_used)
   size_t da_done = 0;
   for (size_t i = 0; i < plan.passes.size(); ++i) {
     const PassDesc& pd = plan.passes[i];
@@ -333,6 +376,7 @@ int run_plan(sv_state_s* h, const CachedPlan& cp, double* psi, double* lam, doub
       h->stats.algorithmic_bytes += 32.0 * amps;
     }
   }
+  mark_plan_used(h, cp);
   return SV_OK;
 }
 
@@ -360,6 +404,7 @@ static int c64_demote(sv_state_s* h) {
 // position 0 = qubit 0, 2^9..2^11-amplitude tiles); otherwise the circuit runs on a complex128
 // scratch copy (widen, complex128 passes, narrow).
 static int run_plan_c64(sv_state_s* h, const CachedPlan& cp) {
+  const_cast<CachedPlan&>(cp).used_rec = false;
   const Plan& plan = cp.plan;
   bool native = true;
   for (const PassDesc& pd : plan.passes) native &= c64_pass_ok(pd);
@@ -394,6 +439,7 @@ static int run_plan_c64(sv_state_s* h, const CachedPlan& cp) {
     h->stats.gate_passes += 1;
     h->stats.algorithmic_bytes += 16.0 * (double)(int64_t(1) << h->n_local);
   }
+  mark_plan_used(h, cp);
   return SV_OK;
 }
 
@@ -866,6 +912,10 @@ sv_status sv_destroy(sv_handle h) {
   h->pin_terms.release();
   h->pin_e.release();
   if (h->plan_upload_done) cudaEventDestroy(h->plan_upload_done);
+  if (h->upload_stream) {
+    cudaStreamSynchronize(h->upload_stream);
+    cudaStreamDestroy(h->upload_stream);
+  }
   if (h->terms_upload_done) cudaEventDestroy(h->terms_upload_done);
   h->work_psi.release();
   h->work_lam.release();

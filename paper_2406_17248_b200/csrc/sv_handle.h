@@ -54,6 +54,11 @@ struct CachedPlan {
   Plan plan;
   DevBuf buf;
   size_t so = 0, mo = 0, ro = 0;
+  // the plan's last use on the handle's stream (recorded after its passes are enqueued) and the
+  // completion of its latest upload on the upload stream: an upload of a refreshed plan overlaps
+  // the kernels already queued (the gradient's forward passes) instead of queuing behind them
+  cudaEvent_t used_ev = nullptr, ready_ev = nullptr;
+  bool used_rec = false;
 };
 
 }  // namespace sv
@@ -78,6 +83,7 @@ struct sv_state_s {
   sv::PinnedBuf pin_in, pin_out;  // batch-mode staging
   sv::PinnedBuf pin_plan;         // plan upload staging
   cudaEvent_t plan_upload_done = nullptr;
+  cudaStream_t upload_stream = nullptr;  // plan uploads of refreshed plans (non-blocking, created lazily)
   sv::PinnedBuf pin_terms;        // Pauli term upload staging
   sv::PinnedBuf pin_e;            // energy partials read-back (gradient)
   cudaEvent_t terms_upload_done = nullptr;
