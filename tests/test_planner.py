@@ -49,6 +49,33 @@ def test_fusion_reduces_passes_for_c4():
     assert sum(p["n_dense"] for p in fused) > 0.5 * sum(p["n_stages"] for p in fused)
 
 
+def test_dense_stage_work_accounting():
+    """The roofline's FP64 work per pass (bench.py): a forward dense stage executes 48 DMMA FMAs
+    and 3 additions per amplitude (three-product form: 3 x 16 complex-entry fragments per 16
+    amplitudes, one sum per input element and two per A entry over the warp's 16 vectors); an
+    adjoint dense stage three times that (R, U^+ psi, U^+ lambda). Sequential ops add FMAs only."""
+    w = W.config("C4")
+    for p in P.sv_plan_info(w.n, w.gates):
+        assert p["add_per_amp"] == 3 * p["n_dense"]
+        assert p["fma_per_amp"] >= 48 * p["n_dense"]
+        if p["n_dense"] == p["n_stages"]:
+            assert p["fma_per_amp"] == 48 * p["n_dense"]
+    g = W.config("C4g")
+    rev = P.sv_plan_info(g.n, g.gates, g.params, adjoint=1)
+    assert any(p["n_dense"] for p in rev)  # adjoint dense stages at 30 qubits
+    for p in rev:
+        assert p["add_per_amp"] == 9 * p["n_dense"]
+        assert p["fma_per_amp"] >= 144 * p["n_dense"]
+
+
+def test_forward_variant_bits_by_size():
+    """Forward dense stages take up to 8 variant bits from 28 local qubits (plan.cpp
+    dense_max_var_for): C4 at 30 qubits plans fewer stages than the same generator would with 6."""
+    w = W.config("C4")
+    plan = P.sv_plan_info(w.n, w.gates)
+    assert sum(p["n_stages"] for p in plan) <= 141
+
+
 def test_adjoint_slots_match_parametrised_gates():
     w = W.config("C2")
     plan = P.sv_plan_info(w.n, w.gates, w.params, adjoint=1)
