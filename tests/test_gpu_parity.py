@@ -422,3 +422,13 @@ def test_structural_plan_refresh(P):
     sv.close()
     assert st["plan_refreshes"] >= 1
     assert np.max(np.abs(got - oracle.apply_circuit(18, b.gates))) <= 1e-10
+    # back to back without a synchronisation: b's refreshed plan is uploaded on the side stream into
+    # the buffer a's passes are still reading; the copy must wait for them (CachedPlan::used_ev)
+    sv = P.StateVector(18)
+    sv.apply_circuit(a.gates)
+    sv.apply_circuit(b.gates)
+    sv.apply_circuit(a.gates)
+    got = sv.get_state()
+    sv.close()
+    ref = oracle.apply_circuit(18, a.gates, None, oracle.apply_circuit(18, b.gates, None, oracle.apply_circuit(18, a.gates)))
+    assert np.max(np.abs(got - ref)) <= 1e-10
