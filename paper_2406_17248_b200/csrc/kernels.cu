@@ -624,6 +624,14 @@ __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __rest
       base_next = tile_base(next);
       issue(base_next, tile_buf + (size_t)((it + 1) & 1) * N);
     }
+    // lambda modes 2 / 3: this tile's old lambda values are requested before the coefficient
+    // fold, the tile wait and the barrier, so their HBM latency overlaps all three
+    double2 l[EPT];
+    if (fast && a.mode != 0) {
+      const double2* lsrc = lam + (base | dep_t);
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) l[j] = a.mode >= 2 ? lsrc[a.hsub[j]] : make_double2(0.0, 0.0);
+    }
     // fold (-1)^{popc(base & z_out)} (outer part) and (-1)^{popc(xt & zt)} into the coefficients
     for (int t = (int)tid; t < a.nterms; t += blockDim.x) {
       const uint32_t neg = ((uint32_t)__popcll(base & s_zo[t]) ^ (s_zt[t] >> 31)) & 1u;
@@ -676,12 +684,8 @@ __global__ void __launch_bounds__(kPauliThreads, 1) k_pauli_tile(const T* __rest
       acc += entry_class<PR_ALL, true, T>(a, a.cls_beg[9], a.cls_beg[10], v, tpb, s_c, tid, esg);
     } else if (fast) {
       // ---- lambda modes: every element accumulates sum_g C_g(e) psi[e ^ x_g] ----
-      // modes 2 / 3 (lambda += this pass' groups): the old lambda values are loaded first, so
-      // their HBM latency overlaps the group evaluation, and the sum is stored once
-      const double2* lsrc = lam + (base | dep_t);
-      double2 l[EPT];
-#pragma unroll
-      for (int j = 0; j < EPT; ++j) l[j] = a.mode >= 2 ? lsrc[a.hsub[j]] : make_double2(0.0, 0.0);
+      // modes 2 / 3 (lambda += this pass' groups): l holds the old lambda values (requested
+      // above); the sum is stored once
       for (int g = 0; g < a.ngroups; ++g) {
         const uint32_t gk = a.gkind[g];
         const uint32_t xt = a.xtile[g];
